@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""FS-FEM hot-path benchmark (BASELINE.json metric) on B200.
+
+One step = the whole hot path on one synthetic cantilever:
+    fsfem_build_faces -> fsfem_assemble_csr (symbolic + numeric) -> fsfem_apply_bc
+    -> fsfem_pcg_solve (Jacobi-PCG to ||r||/||f|| <= 1e-10)
+with inputs resident in HBM.  `value` = faces pushed through the whole path per second
+(N_f * steps / device time, max over ranks); the JSON line also carries the two throughputs
+the metric names (numeric-assembly faces/s and PCG iterations/s), the SpMV roofline,
+the end-to-end number through the C ABI with pinned host buffers, and the CPU oracle baseline.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl fsfem|reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from fsfem_inputs import CONFIGS, config_mesh  # noqa: E402
+
+E_MOD, NU = 1.0e6, 0.3
+METRIC = "FS-FEM faces assembled/s + PCG iterations/s at ~2M tets; % of HBM roofline"
+SAMPLE_X_CELLS = 25  # CPU-oracle sample: the first 25 of cfg4's 200 x-cells (same spacing)
+
+
+def workload_name(cfg: int) -> str:
+    nx, ny, nz = CONFIGS[cfg]["grid"]
+    extra = []
+    if CONFIGS[cfg].get("jitter"):
+        extra.append(f"jitter {CONFIGS[cfg]['jitter']}h")
+    if CONFIGS[cfg].get("node_perm_seed") is not None:
+        extra.append("random node/tet order")
+    return (f"cfg{cfg}: cantilever 10x1x1, {nx}x{ny}x{nz} hexes x 6 Kuhn T4, E=1e6 nu=0.3, clamped x=0, "
+            f"tip load P=-1" + (", " + ", ".join(extra) if extra else ""))
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+def oracle_sample(cfg: int, sample_iters: int = 20) -> dict:
+    """Time the oracle (as it stands) on a slab of the workload and scale to the full config.
+
+    Sample: cfg's first SAMPLE_X_CELLS x-cells at the same spacing.  Scaled per stage by
+    N_t (faces), N_f (assembly), nnz (BCs, PCG per iteration); the PCG iteration count of the
+    full problem is the oracle's own, recorded by scripts/oracle_full_solve.py."""
+    from oracle import Oracle
+    full = config_mesh(cfg)
+    m = config_mesh(cfg, x_cells=SAMPLE_X_CELLS if cfg >= 3 else None)
+    o = Oracle(m.xyz, m.tets)
+    t0 = time.perf_counter()
+    o.build_faces()
+    t_faces = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, rp, _, _ = o.assemble_fs(E_MOD, NU)
+    t_asm = time.perf_counter() - t0
+    nnz_s = int(rp[-1])
+    t0 = time.perf_counter()
+    o.apply_bc(m.dirichlet, m.loads, 0)
+    t_bc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, rep = o.pcg(1e-30, sample_iters, allow_not_converged=True)
+    t_pcg = time.perf_counter() - t0
+    it_s = max(1, rep["iterations"])
+    from fsfem_inputs import kuhn_counts
+    c = kuhn_counts(*full.grid)
+    cs = kuhn_counts(*m.grid)
+    gold = os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}.json")
+    iters_full = json.load(open(gold))["pcg"]["iterations"] if os.path.exists(gold) else None
+    t_full = (t_faces * c["n_tets"] / cs["n_tets"] + t_asm * c["n_faces"] / cs["n_faces"]
+              + t_bc * c["nnz_fs"] / nnz_s)
+    t_iter_full = t_pcg / it_s * c["nnz_fs"] / nnz_s
+    if iters_full is not None:
+        t_full += iters_full * t_iter_full
+    return dict(t_step_s=t_full, faces_per_s=c["n_faces"] / t_full if iters_full else None,
+                assembly_faces_per_s=cs["n_faces"] / t_asm, pcg_it_per_s=1.0 / t_iter_full,
+                iters_full=iters_full, wall_s=t_faces + t_asm + t_bc + t_pcg,
+                sample=(f"oracle on a slab of cfg{cfg} ({m.grid[0]}x{m.grid[1]}x{m.grid[2]} hexes, {m.n_tets} tets, "
+                        f"same spacing): faces + full assembly + BCs + {it_s} PCG iterations, scaled by N_t, N_f, "
+                        f"nnz and the oracle's own full-size iteration count ({iters_full})"))
+
+
+def cpu_cores() -> int:
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n else (os.cpu_count() or 1)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        oracle_sample(args.config, sample_iters=5)
+    vals = []
+    samples = []
+    for _ in range(args.steps):
+        s = oracle_sample(args.config)
+        vals.append(s["t_step_s"])
+        samples.append(s)
+    t = float(np.mean(vals))
+    nf = config_faces(args.config)
+    v = nf / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "faces/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "n_faces": nf},
+            "components": {"assembly_faces_per_s": samples[-1]["assembly_faces_per_s"],
+                           "pcg_it_per_s": samples[-1]["pcg_it_per_s"], "pcg_iterations": samples[-1]["iters_full"]},
+            "cpu_baseline": {"value": v, "unit": "faces/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": samples[-1]["sample"]},
+            "e2e": {"value": v, "unit": "faces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_faces(cfg: int) -> int:
+    from fsfem_inputs import kuhn_counts
+    return kuhn_counts(*CONFIGS[cfg]["grid"])["n_faces"]
+
+
+def load_peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def spmv_algorithmic_bytes(nnz: int, nblk: int, n_nodes_loc: int, n_nodes: int) -> int:
+    """Bytes one SpMV launch must move: values 8/nnz, one 4-byte column id per
+    3x3 block, node pointers, the gathered vector p once, q written once."""
+    return 8 * nnz + 4 * nblk + 8 * (n_nodes_loc + 1) + 24 * n_nodes + 24 * n_nodes_loc
+
+
+def traffic_from_profile(cfg: int):
+    p = os.path.join(ROOT, "profiles", "spmv_dram_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(f"cfg{cfg}")
+    return None
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    from paper_2001_08849_b200 import (FsFem, fsfem_apply_bc, fsfem_assemble_csr, fsfem_build_faces,
+                                       fsfem_nccl_get_unique_id, fsfem_pcg_solve, load_library)
+    load_library()
+    m = config_mesh(args.config)
+    stream = torch.cuda.current_stream()
+    g = FsFem(device=local, stream=stream.cuda_stream)
+    if world > 1:
+        uid = [fsfem_nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        g.comm_init(uid[0], rank, world)
+    dev = torch.device("cuda", local)
+    xyz_d = torch.from_numpy(m.xyz).to(dev)
+    tets_d = torch.from_numpy(m.tets).to(dev)
+    dir_d = torch.from_numpy(m.dirichlet).to(dev)
+    loads_d = torch.from_numpy(m.loads.reshape(-1).copy()).to(dev)
+    u_d = torch.zeros(3 * m.n_nodes, dtype=torch.float64, device=dev)
+
+    def step(xyz, tets, dirichlet, loads, u):
+        nf, ni = fsfem_build_faces(g.ctx, xyz, tets)
+        rb, nr, nnz = fsfem_assemble_csr(g.ctx, E_MOD, NU)
+        fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
+        rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, 0)
+        return nf, nnz, rep
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(k, inputs):
+        reps = []
+        barrier()
+        l0 = g.report()["kernel_launches"]
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(k):
+            reps.append(step(*inputs))
+        ev1.record(stream)
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = g.report()["kernel_launches"] - l0
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, reps, launches
+
+    dev_inputs = (xyz_d, tets_d, dir_d, loads_d, u_d)
+    for _ in range(args.warmup):
+        step(*dev_inputs)
+    with ClockSampler(local) as clk:
+        ms, reps, launches = timed(args.steps, dev_inputs)
+    nf, nnz, _ = reps[-1]
+    value = nf * args.steps / (ms / 1e3)
+
+    def agg(key):
+        return float(np.mean([r[2][key] for r in reps]))
+
+    t_num, t_pcg = agg("t_numeric_ms"), agg("t_pcg_ms")
+    iters = agg("iterations")
+    spmv_ms = sum(r[2]["t_spmv_ms"] for r in reps)
+    spmv_n = sum(r[2]["spmv_launches"] for r in reps)
+    vals_local = torch.tensor([t_num, t_pcg, spmv_ms / max(spmv_n, 1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals_local, op=dist.ReduceOp.MAX)
+    t_num, t_pcg, spmv_avg_ms = [float(x) for x in vals_local.tolist()]
+
+    # end to end through the C ABI with pinned host buffers (H2D of inputs, D2H of u per step)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    host_inputs = (pin(m.xyz), pin(m.tets), pin(m.dirichlet), pin(m.loads.reshape(-1)),
+                   torch.zeros(3 * m.n_nodes, dtype=torch.float64).pin_memory())
+    e2e = None
+    if not args.no_e2e:
+        step(*host_inputs)
+        ms_e2e, _, _ = timed(args.steps, host_inputs)
+        e2e = {"value": nf * args.steps / (ms_e2e / 1e3), "unit": "faces/s",
+               "h2d_bytes_per_step": int(m.xyz.nbytes + m.tets.nbytes + m.dirichlet.nbytes + m.loads.nbytes),
+               "d2h_bytes_per_step": int(8 * 3 * m.n_nodes)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_kind = load_peaks()
+    nblk = nnz // 9
+    nloc = m.n_nodes if world == 1 else -(-m.n_nodes // world)
+    spmv_bytes = spmv_algorithmic_bytes(nnz if world == 1 else nnz, nblk, nloc, m.n_nodes)
+    achieved = spmv_bytes / (spmv_avg_ms / 1e3) / 1e9
+    roof = {"kernel": "k_spmv<true> (PCG SpMV + p.q)", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(args.config),
+            "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms, "launches_timed": spmv_n,
+            "peak_kind": peak_kind, "share_of_step": spmv_ms / args.steps / (ms / args.steps)}
+    asm_bytes = 24 * m.n_nodes + 16 * m.n_tets + 8 * nnz
+    line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "n_nodes": m.n_nodes, "n_tets": m.n_tets,
+                       "n_faces": nf, "nnz": nnz, "parallelism": f"row-block x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)"},
+            "components": {"assembly_faces_per_s": nf / (t_num / 1e3), "assembly_ms": t_num,
+                           "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,
+                           "pcg_it_per_s": iters / (t_pcg / 1e3), "pcg_iterations": iters, "pcg_ms": t_pcg,
+                           "faces_ms": agg("t_faces_ms"), "symbolic_ms": agg("t_symbolic_ms"), "bc_ms": agg("t_bc_ms"),
+                           "true_rel_residual": reps[-1][2]["true_rel_residual"]},
+            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        s = oracle_sample(args.config)
+        line["cpu_baseline"] = {"value": s["faces_per_s"], "unit": "faces/s", "cores": cpu_cores(), "kind": "oracle",
+                                "sample": s["sample"], "assembly_faces_per_s": s["assembly_faces_per_s"],
+                                "pcg_it_per_s": s["pcg_it_per_s"], "wall_s": s["wall_s"]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="fsfem", choices=["fsfem", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,150 @@
+/* fsfem.h — C ABI of the B200 (sm_100a) FS-FEM hot path.
+ *
+ * Method: face-based smoothed FEM (FS-FEM) for 3D linear elasticity on 4-node tetrahedra,
+ * arxiv 2001.08849 (juSFEM), §2.1 STEPs 1-5 (lines 124-245) and §3.2-3.3 (303-449).
+ * The library computes, on one GPU per process:
+ *   S1  the unique faces (smoothing domains) of the mesh         (Alg. 1)
+ *   S2-S4 per-face smoothed gradients b_I and V_f                  (Eqs. 2-7)
+ *   S5-S6 the global smoothed stiffness K = sum_f B^T c B V_f     (Eqs. 8-9)
+ *         as CSR with a fixed (deterministic) summation order
+ *   S7  essential boundary conditions
+ *   S8-S9 K d = f by Jacobi-preconditioned CG                     (replaces PARDISO)
+ *
+ * Conventions:
+ *   - dof numbering: dof = 3*node + component (x, y, z)                                (Q12)
+ *   - material: isotropic, Voigt (xx, yy, zz, yz, xz, xy), engineering shear strains   (Q1)
+ *   - faces are ordered by their sorted vertex triple (a < b < c); an interior face lists
+ *     its two tets with t0 < t1; exterior faces have t1 = opp1 = -1                     (Q11)
+ *   - CSR keeps every structural entry (full 3x3 blocks for every pair of nodes sharing a
+ *     smoothing domain), columns ascending                                             (Q13)
+ *   - either tet orientation is accepted (volumes use |det|)                           (Q6)
+ *
+ * Memory: every array argument may point to HOST memory (pageable or pinned) or to DEVICE
+ * memory of the context's device; the library tells them apart with cudaPointerGetAttributes
+ * and copies host data in/out itself (copies are stream-ordered on the context stream).
+ * The caller owns all its buffers; the context owns every intermediate it allocates until
+ * fsfem_destroy or the next fsfem_build_faces.  Calls are asynchronous on the context stream
+ * except where they return host scalars, which synchronize that stream.  No C++ exception
+ * crosses the ABI; every call returns an fsfem_status and fsfem_last_error() explains it.
+ *
+ * Call order: create -> [comm_init] -> build_faces -> assemble_csr -> apply_bc -> pcg_solve.
+ * A violation returns FSFEM_ERR_STATE.  Re-calling assemble_csr re-runs only the numeric
+ * assembly (S6) on the cached pattern; it invalidates earlier BCs.
+ */
+#ifndef FSFEM_H
+#define FSFEM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FSFEM_OK = 0,
+  FSFEM_ERR_INVALID_ARG = 1,   /* null pointer, size <= 0, node id out of range, E <= 0,
+                                  nu outside (-1, 0.5), bad mode, unknown pointer kind       */
+  FSFEM_ERR_TOPOLOGY = 2,      /* a face shared by more than two tets (non-manifold mesh)    */
+  FSFEM_ERR_DEGENERATE = 3,    /* a tet repeats a node or |V_e| <= 1e-14 * diag(bbox)^3      */
+  FSFEM_ERR_UNSUPPORTED = 4,   /* n_nodes >= 2^31/3, nnz >= 2^31, a node in > 4096 faces, ... */
+  FSFEM_ERR_NOT_CONVERGED = 5, /* max_iter reached: u holds the last iterate, report filled   */
+  FSFEM_ERR_BREAKDOWN = 6,     /* non-finite value or p.q <= 0 in PCG (K not SPD after BCs)  */
+  FSFEM_ERR_STATE = 7,         /* call order violated                                        */
+  FSFEM_ERR_CUDA = 8,          /* a CUDA runtime error (message has the CUDA error string)   */
+  FSFEM_ERR_NCCL = 9,          /* an NCCL error                                              */
+  FSFEM_ERR_OOM = 10           /* device allocation failed                                   */
+} fsfem_status;
+
+typedef struct fsfem_ctx fsfem_ctx; /* opaque */
+
+typedef struct {
+  int64_t iterations;        /* PCG iterations performed (SpMVs inside the loop)            */
+  int32_t converged;         /* 1 if ||r||_2 <= rel_tol * ||f||_2 was reached               */
+  int32_t _pad;
+  double rel_residual;       /* recurrence residual ||r|| / ||f|| at exit                    */
+  double true_rel_residual;  /* ||f - K u|| / ||f|| recomputed at exit                       */
+  double t_faces_ms;         /* device time (CUDA events) of the last build_faces (S1)       */
+  double t_symbolic_ms;      /* ... of the symbolic CSR pass (S5, first assemble only)       */
+  double t_numeric_ms;       /* ... of the last numeric assembly (S2-S4, S6)                 */
+  double t_bc_ms;            /* ... of the last apply_bc (S7)                                */
+  double t_pcg_ms;           /* ... of the last pcg_solve loop (S8-S9)                       */
+  double t_spmv_ms;          /* summed device time of the SpMV launches of that loop         */
+  int64_t spmv_launches;     /* number of SpMV launches timed in t_spmv_ms                   */
+  int64_t kernel_launches;   /* kernels launched by libfsfem in this process so far (monotonic;
+                                graph replays count their kernels, early-exit ones included) */
+} fsfem_report;
+
+/* Human-readable name of a status code (static string). */
+const char* fsfem_status_string(fsfem_status s);
+
+/* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a cudaStream_t (e.g.
+ * torch.cuda.current_stream().cuda_stream) or NULL, in which case the context creates its own
+ * non-blocking stream.  *out receives the context. */
+fsfem_status fsfem_create(int cuda_device, void* cuda_stream, fsfem_ctx** out);
+/* Frees every device buffer of the context.  NULL-safe. */
+fsfem_status fsfem_destroy(fsfem_ctx* ctx);
+/* Last error message of the context ("" if none); valid until the next call on ctx. */
+const char* fsfem_last_error(const fsfem_ctx* ctx);
+
+/* Multi-GPU: join an NCCL communicator of `nranks` processes, one GPU each.
+ * `nccl_unique_id` is the 128-byte ncclUniqueId (host memory) created by rank 0 and
+ * broadcast by the caller.  Rank r then owns the contiguous node range
+ * [r*ceil(N_n/nranks), min(N_n, (r+1)*ceil(N_n/nranks))) and builds only those rows. */
+fsfem_status fsfem_comm_init(fsfem_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
+/* Rank 0 helper: write a fresh 128-byte ncclUniqueId to out [host].  Needs libnccl.so.2
+ * (resolved at run time).  Errors: INVALID_ARG (NULL), NCCL. */
+fsfem_status fsfem_nccl_get_unique_id(void* out);
+
+/* S1: extract the unique faces of the mesh.
+ *   xyz  [3*n_nodes] double, node coordinates (x, y, z per node)            (Node matrix)
+ *   tets [4*n_tets]  int32, 0-based node ids; face l of a tet is the face
+ *        opposite its vertex l                                               (Element matrix)
+ *   n_faces, n_interior [host] receive N_f = N_i + N_e and N_i.
+ * The mesh is copied into the context.  Errors: INVALID_ARG, DEGENERATE, TOPOLOGY, UNSUPPORTED. */
+fsfem_status fsfem_build_faces(fsfem_ctx* ctx, const double* xyz, int64_t n_nodes,
+                               const int32_t* tets, int64_t n_tets,
+                               int64_t* n_faces, int64_t* n_interior);
+/* Copy out the face table (Face_in / Face_out of PAPER.md:317, Fig. 7), ascending by (a,b,c):
+ *   face_nodes [3*N_f] (a < b < c), face_tet [2*N_f] (t0 < t1, t1 = -1 exterior),
+ *   face_opp [2*N_f] (node of t_k opposite the face, -1 exterior).  Any pointer may be NULL. */
+fsfem_status fsfem_get_faces(const fsfem_ctx* ctx, int32_t* face_nodes, int32_t* face_tet,
+                             int32_t* face_opp);
+
+/* S2-S6 (Eqs. 8-9, 403-449): assemble the smoothed stiffness for Young's
+ * modulus E > 0 and Poisson ratio nu in (-1, 0.5).  The first call also builds the symbolic
+ * pattern (S5).  Every entry K[3i+a, 3j+c] = sum over faces f containing both i and j in
+ * their field, in ascending face order, of V_f * (B_i^T c B_j)[a][c].
+ *   row_begin, n_rows, nnz [host]: this rank's first global row, its row count, its nnz. */
+fsfem_status fsfem_assemble_csr(fsfem_ctx* ctx, double E, double nu, int64_t* row_begin,
+                                int64_t* n_rows, int64_t* nnz);
+/* Copy out this rank's CSR rows: row_ptr [n_rows+1] (0-based, int64), col_idx [nnz] (global
+ * column ids, ascending per row), vals [nnz].  Any pointer may be NULL. */
+fsfem_status fsfem_get_csr(const fsfem_ctx* ctx, int64_t* row_ptr, int32_t* col_idx, double* vals);
+
+/* S7: clamp every dof of the nodes dirichlet_nodes[n_dirichlet]
+ * (prescribed displacement 0) and take nodal loads loads[3*n_nodes] (forces per dof).
+ *   mode 0 = MODIFY (default): zero the constrained rows and columns except the diagonal,
+ *            f_r = 0 on constrained dofs;
+ *   mode 1 = PENALTY: K_rr += alpha, alpha = penalty_scale * max_i K_ii (penalty_scale <= 0
+ *            means 1e8).
+ * Also extracts the Jacobi preconditioner 1/K_ii.  Modifies the context's K in place. */
+fsfem_status fsfem_apply_bc(fsfem_ctx* ctx, const int32_t* dirichlet_nodes, int64_t n_dirichlet,
+                            const double* loads, int mode, double penalty_scale);
+
+/* S8-S9: solve K u = f by Jacobi-PCG, stopping when ||r||_2 <= rel_tol * ||f||_2 on the
+ * recurrence residual (rel_tol <= 0 means 1e-10; max_iter <= 0 means max(1000, 20*sqrt(n))).
+ *   u [3*n_nodes]: in = initial guess unless u0_is_zero, out = solution (full vector on every
+ *   rank).  rep [host] may be NULL.  NOT_CONVERGED still writes u and rep. */
+fsfem_status fsfem_pcg_solve(fsfem_ctx* ctx, double* u, int u0_is_zero, double rel_tol,
+                             int64_t max_iter, fsfem_report* rep);
+
+/* Report of the last calls (timings and last PCG data); rep [host]. */
+fsfem_status fsfem_get_report(const fsfem_ctx* ctx, fsfem_report* rep);
+
+/* q = K p on the assembled matrix (before or after BCs): p [3*n_nodes], q [3*n_nodes] (this
+ * rank's rows are written).  Used by tests for residual checks. */
+fsfem_status fsfem_spmv(fsfem_ctx* ctx, const double* p, double* q);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSFEM_H */

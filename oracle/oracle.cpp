@@ -365,13 +365,17 @@ int ora_face_domain(ora_mesh* m, int64_t f, int32_t* field, double* bbar, double
   for (int i = 0; i < 5; ++i) field[i] = fld[i];
 
   // A point is carried with its coordinates and its shape-function values on the field nodes.
+  // Coordinates are taken relative to face node A (reading Q24: Eq. 7 does not depend on the
+  // origin; a face-local origin keeps the far-from-origin tip faces accurate to ~1e-15).
+  const V3 origin = node(m, a);
+  auto local = [&](int32_t i) { return sub(node(m, i), origin); };
   struct Pt {
     V3 x;
     double N[5];
   };
   auto field_pt = [&](int I) {
     Pt p;
-    p.x = node(m, fld[I]);
+    p.x = local(fld[I]);
     for (int J = 0; J < 5; ++J) p.N[J] = (J == I) ? 1.0 : 0.0;
     return p;
   };
@@ -381,7 +385,7 @@ int ora_face_domain(ora_mesh* m, int64_t f, int32_t* field, double* bbar, double
     const int32_t* v = &m->tets[4 * t[k]];
     V3 s = {0, 0, 0};
     for (int q = 0; q < 4; ++q) {
-      const V3 x = node(m, v[q]);
+      const V3 x = local(v[q]);
       s.x += x.x;
       s.y += x.y;
       s.z += x.z;

@@ -1,0 +1,25 @@
+"""B200 (sm_100a) FS-FEM hot path: faces -> smoothed stiffness (CSR) -> BCs -> Jacobi-PCG.
+
+The compute lives in libfsfem.so (csrc/*.cu, C ABI in include/fsfem.h); fsfem.py is a ctypes
+binding.  Method: arxiv 2001.08849 (juSFEM), see DESIGN.md.
+"""
+from .fsfem import (  # noqa: F401
+    EXPORTS,
+    LIB_PATH,
+    Csr,
+    FsFem,
+    FsfemError,
+    fsfem_apply_bc,
+    fsfem_assemble_csr,
+    fsfem_build_faces,
+    fsfem_comm_init,
+    fsfem_create,
+    fsfem_destroy,
+    fsfem_get_csr,
+    fsfem_get_faces,
+    fsfem_get_report,
+    fsfem_nccl_get_unique_id,
+    fsfem_pcg_solve,
+    fsfem_spmv,
+    load_library,
+)

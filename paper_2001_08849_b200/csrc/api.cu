@@ -1,0 +1,612 @@
+// C ABI of the FS-FEM hot path (include/fsfem.h): context, call-order state machine,
+// host/device pointer handling, stage timing, PCG batching in CUDA graphs, NCCL row partition.
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "nccl.h"
+#include "pcg.cuh"
+
+namespace fsfem {
+
+// kernels' host drivers (faces.cu, symbolic.cu, assemble.cu, bc.cu)
+void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, int64_t nt, cudaStream_t s,
+                        DevBuf<unsigned char>& scratch, DevBuf<int32_t>& face_nodes, DevBuf<int32_t>& face_tet,
+                        DevBuf<int32_t>& face_opp, DevBuf<int32_t>& tet_face, int64_t* n_faces, int64_t* n_interior,
+                        unsigned long long* h_flags);
+void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
+                          const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
+                          DevBuf<unsigned char>& scratch, DevBuf<int64_t>& node_ptr, DevBuf<int32_t>& nbr,
+                          DevBuf<int64_t>& nf_ptr, DevBuf<int32_t>& nf_idx, DevBuf<int32_t>& diag_slot,
+                          unsigned long long* h_flags, int64_t* nblk_out, int64_t* nfi_out);
+void expand_csr_device(const int64_t* node_ptr, const int32_t* nbr, int64_t nloc, int64_t* row_ptr, int32_t* col_idx,
+                       cudaStream_t s);
+void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
+                   const int32_t* face_opp, int64_t nf, double* face_s, cudaStream_t s);
+void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
+                          const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
+                          int64_t nloc, double lam, double mu, double* vals, cudaStream_t s);
+void apply_bc_device(const int64_t* node_ptr, const int32_t* nbr, const int32_t* diag_slot, int64_t n_lo, int64_t nloc,
+                     int64_t nn, const int32_t* dir, int64_t nd, const double* loads, int mode, double penalty_scale,
+                     double* vals, double* f, double* dinv, uint8_t* fixed, unsigned long long* flags, cudaStream_t s);
+
+static std::atomic<long long> g_launches{0};
+static thread_local bool g_capturing = false;
+void count_launch(long long n) {
+  if (!g_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
+}
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void set_capturing(bool on) { g_capturing = on; }
+
+static int g_sms = 0;
+int num_sms() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// ---- NCCL, resolved at run time (torch has already loaded libnccl.so.2 in practice) ----
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString;
+  });
+  return api;
+}
+#define FS_NCCL(call)                                                                                   \
+  do {                                                                                                  \
+    ncclResult_t r_ = (call);                                                                           \
+    if (r_ != ncclSuccess) throw ::fsfem::Error(FSFEM_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+}  // namespace fsfem
+
+using namespace fsfem;
+
+enum Stage { kCreated = 0, kFaces = 1, kAssembled = 2, kBc = 3 };
+
+struct fsfem_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int stage = kCreated;
+  // partition
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  int64_t n_lo = 0, nloc = 0, chunk = 0;
+  // mesh
+  int64_t nn = 0, nt = 0, nf = 0, ni = 0;
+  DevBuf<double> xyz;
+  DevBuf<int32_t> tets;
+  DevBuf<int32_t> face_nodes, face_tet, face_opp, tet_face;
+  // pattern
+  bool have_pattern = false;
+  int64_t nblk = 0, nfi = 0;
+  DevBuf<int64_t> node_ptr, nf_ptr;
+  DevBuf<int32_t> nbr, nf_idx, diag_slot;
+  // numeric
+  double E = 0, nu = 0;
+  DevBuf<double> face_s, vals;
+  // bc / pcg
+  DevBuf<double> f, dinv, x_full, r, p_full, q, part, all;
+  DevBuf<uint8_t> fixed;
+  DevBuf<PcgState> st;
+  DevBuf<unsigned char> scratch;
+  DevBuf<unsigned long long> flags;
+  DevBuf<double> staging;  // host->device staging for loads / u
+  DevBuf<int32_t> staging_i;
+  unsigned long long* h_flags = nullptr;  // pinned [8]
+  PcgState* h_st = nullptr;               // pinned
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> spmv_ev;
+  fsfem_report rep{};
+  // graph cache
+  cudaGraphExec_t graph = nullptr;
+  int graph_batch = 0;
+  const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+constexpr int kBatch = 32;  // PCG iterations per CUDA graph launch
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Copy `bytes` from a host-or-device source into device memory dst (stream ordered).
+void to_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  FS_CUDA(cudaMemcpyAsync(dst, src, bytes, is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+}
+void from_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0 || !dst) return;
+  FS_CUDA(cudaMemcpyAsync(dst, src, bytes, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+}
+
+fsfem_status fail(fsfem_ctx* c, fsfem_status code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+template <typename F>
+fsfem_status guarded(fsfem_ctx* c, F&& fn) {
+  if (!c) return FSFEM_ERR_INVALID_ARG;
+  try {
+    c->err.clear();
+    FS_CUDA(cudaSetDevice(c->device));
+    return fn();
+  } catch (const Error& e) {
+    c->err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return FSFEM_ERR_OOM;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return FSFEM_ERR_CUDA;
+  }
+}
+
+fsfem_status decode_flags(fsfem_ctx* c, unsigned long long v, const char* what) {
+  if (v == kNoError) return FSFEM_OK;
+  const int code = static_cast<int>(v >> 56);
+  const long long idx = static_cast<long long>(v & ((1ull << 56) - 1));
+  const char* item = "item";
+  switch (code) {
+    case FSFEM_ERR_INVALID_ARG: item = "entry"; break;
+    case FSFEM_ERR_DEGENERATE: item = "tet"; break;
+    case FSFEM_ERR_TOPOLOGY: item = "face bucket (smallest node id)"; break;
+    case FSFEM_ERR_UNSUPPORTED: item = "node"; break;
+    case FSFEM_ERR_BREAKDOWN: item = "dof"; break;
+    default: break;
+  }
+  c->err = std::string(what) + ": " + fsfem_status_string(static_cast<fsfem_status>(code)) + " at " + item + " " +
+           std::to_string(idx);
+  return static_cast<fsfem_status>(code);
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  FS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+void drop_graph(fsfem_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  c->graph = nullptr;
+}
+
+// allgather of the 4 per-rank partials and the combine step (multi-rank only)
+void combine(fsfem_ctx* c, int stage) {
+  FS_NCCL(nccl().AllGather(c->st.get()->local, c->all.get(), 4, ncclDouble, c->comm, c->stream));
+  launch_combine(c->st.get(), c->all.get(), stage, c->stream);
+}
+
+// p_full own slice -> everyone (in-place allgather, equal padded slices)
+void gather_full(fsfem_ctx* c, double* full) {
+  if (c->nranks == 1) return;
+  FS_NCCL(nccl().AllGather(full + 3 * c->chunk * c->rank, full, 3 * c->chunk, ncclDouble, c->comm, c->stream));
+}
+
+void pcg_iteration(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
+  PcgState* st = c->st.get();
+  double* own_p = c->p_full.get() + 3 * c->n_lo;
+  double* own_x = c->x_full.get() + 3 * c->n_lo;
+  const int64_t n = 3 * c->nloc;
+  if (e0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+  launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->p_full.get(), 3 * c->n_lo, c->q.get(), st,
+              c->part.get(), true, c->stream);
+  if (e1) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  if (c->nranks > 1) combine(c, 1);
+  launch_update(own_x, c->r.get(), own_p, c->q.get(), c->dinv.get(), n, st, c->part.get(), c->stream);
+  if (c->nranks > 1) combine(c, 2);
+  launch_direction(own_p, c->r.get(), c->dinv.get(), n, st, c->stream);
+  gather_full(c, c->p_full.get());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fsfem_status_string(fsfem_status s) {
+  switch (s) {
+    case FSFEM_OK: return "ok";
+    case FSFEM_ERR_INVALID_ARG: return "invalid argument";
+    case FSFEM_ERR_TOPOLOGY: return "topology error";
+    case FSFEM_ERR_DEGENERATE: return "degenerate element";
+    case FSFEM_ERR_UNSUPPORTED: return "unsupported size";
+    case FSFEM_ERR_NOT_CONVERGED: return "not converged";
+    case FSFEM_ERR_BREAKDOWN: return "breakdown";
+    case FSFEM_ERR_STATE: return "call order violated";
+    case FSFEM_ERR_CUDA: return "cuda error";
+    case FSFEM_ERR_NCCL: return "nccl error";
+    case FSFEM_ERR_OOM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+fsfem_status fsfem_create(int cuda_device, void* cuda_stream, fsfem_ctx** out) {
+  if (!out) return FSFEM_ERR_INVALID_ARG;
+  *out = nullptr;
+  fsfem_ctx* c = new (std::nothrow) fsfem_ctx();
+  if (!c) return FSFEM_ERR_OOM;
+  c->device = cuda_device;
+  fsfem_status st = guarded(c, [&]() -> fsfem_status {
+    if (cuda_stream) {
+      c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      FS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    FS_CUDA(cudaMallocHost(&c->h_flags, 8 * sizeof(unsigned long long)));
+    FS_CUDA(cudaMallocHost(&c->h_st, sizeof(PcgState)));
+    FS_CUDA(cudaEventCreate(&c->ev0));
+    FS_CUDA(cudaEventCreate(&c->ev1));
+    c->spmv_ev.resize(2 * kBatch);
+    for (auto& e : c->spmv_ev) FS_CUDA(cudaEventCreate(&e));
+    c->flags.ensure(8);
+    c->st.ensure(1);
+    num_sms();
+    return FSFEM_OK;
+  });
+  if (st != FSFEM_OK) {
+    fsfem_destroy(c);
+    return st;
+  }
+  *out = c;
+  return FSFEM_OK;
+}
+
+fsfem_status fsfem_destroy(fsfem_ctx* c) {
+  if (!c) return FSFEM_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto e : c->spmv_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return FSFEM_OK;
+}
+
+const char* fsfem_last_error(const fsfem_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+fsfem_status fsfem_nccl_get_unique_id(void* out) {
+  if (!out) return FSFEM_ERR_INVALID_ARG;
+  if (!nccl().ok) return FSFEM_ERR_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return FSFEM_ERR_NCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return FSFEM_OK;
+}
+
+fsfem_status fsfem_comm_init(fsfem_ctx* c, const void* uid, int rank, int nranks) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (!uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, FSFEM_ERR_INVALID_ARG, "bad rank/nranks/id");
+    if (c->stage != kCreated) return fail(c, FSFEM_ERR_STATE, "comm_init must precede build_faces");
+    if (nranks > 1) {
+      if (!nccl().ok) return fail(c, FSFEM_ERR_NCCL, "libnccl.so.2 not loadable");
+      ncclUniqueId id;
+      std::memcpy(&id, uid, sizeof(id));
+      FS_NCCL(nccl().CommInitRank(&c->comm, nranks, id, rank));
+    }
+    c->rank = rank;
+    c->nranks = nranks;
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes, const int32_t* tets, int64_t n_tets,
+                               int64_t* n_faces, int64_t* n_interior) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (!xyz || !tets || n_nodes < 4 || n_tets < 1) return fail(c, FSFEM_ERR_INVALID_ARG, "need >= 4 nodes and >= 1 tet");
+    if (n_nodes >= (1LL << 31) / 3 || 4 * n_tets >= (1LL << 31))
+      return fail(c, FSFEM_ERR_UNSUPPORTED, "mesh too large for 32-bit ids");
+    drop_graph(c);
+    c->stage = kCreated;
+    c->have_pattern = false;
+    c->nn = n_nodes;
+    c->nt = n_tets;
+    c->chunk = ceil_div(n_nodes, c->nranks);
+    c->n_lo = std::min<int64_t>(n_nodes, c->chunk * c->rank);
+    c->nloc = std::min<int64_t>(n_nodes, c->n_lo + c->chunk) - c->n_lo;
+    c->xyz.ensure(3 * n_nodes);
+    c->tets.ensure(4 * n_tets);
+    FS_CUDA(cudaEventRecord(c->ev0, c->stream));
+    to_device(c->xyz.get(), xyz, sizeof(double) * 3 * n_nodes, c->stream);
+    to_device(c->tets.get(), tets, sizeof(int32_t) * 4 * n_tets, c->stream);
+    int64_t nf = 0, ni = 0;
+    c->h_flags[0] = kNoError;
+    build_faces_device(c->xyz.get(), n_nodes, c->tets.get(), n_tets, c->stream, c->scratch, c->face_nodes, c->face_tet,
+                       c->face_opp, c->tet_face, &nf, &ni, c->h_flags);
+    fsfem_status s = decode_flags(c, c->h_flags[0], "build_faces");
+    if (s != FSFEM_OK) return s;
+    FS_CUDA(cudaEventRecord(c->ev1, c->stream));
+    FS_CUDA(cudaEventSynchronize(c->ev1));
+    c->rep.t_faces_ms = elapsed(c->ev0, c->ev1);
+    c->nf = nf;
+    c->ni = ni;
+    if (n_faces) *n_faces = nf;
+    if (n_interior) *n_interior = ni;
+    c->stage = kFaces;
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_get_faces(const fsfem_ctx* cc, int32_t* face_nodes, int32_t* face_tet, int32_t* face_opp) {
+  fsfem_ctx* c = const_cast<fsfem_ctx*>(cc);
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kFaces) return fail(c, FSFEM_ERR_STATE, "build_faces first");
+    from_device(face_nodes, c->face_nodes.get(), sizeof(int32_t) * 3 * c->nf, c->stream);
+    from_device(face_tet, c->face_tet.get(), sizeof(int32_t) * 2 * c->nf, c->stream);
+    from_device(face_opp, c->face_opp.get(), sizeof(int32_t) * 2 * c->nf, c->stream);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_begin, int64_t* n_rows, int64_t* nnz) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kFaces) return fail(c, FSFEM_ERR_STATE, "build_faces first");
+    if (!(E > 0.0) || !(nu > -1.0 && nu < 0.5) || !std::isfinite(E))
+      return fail(c, FSFEM_ERR_INVALID_ARG, "need E > 0 and -1 < nu < 0.5");
+    if (!c->have_pattern) {
+      FS_CUDA(cudaEventRecord(c->ev0, c->stream));
+      c->h_flags[0] = kNoError;
+      build_pattern_device(c->tets.get(), c->nt, c->tet_face.get(), c->face_tet.get(), c->face_opp.get(), c->n_lo,
+                           c->nloc, c->stream, c->scratch, c->node_ptr, c->nbr, c->nf_ptr, c->nf_idx, c->diag_slot,
+                           c->h_flags, &c->nblk, &c->nfi);
+      fsfem_status s = decode_flags(c, c->h_flags[0], "symbolic");
+      if (s != FSFEM_OK) return s;
+      if (9 * c->nblk >= (1LL << 31)) return fail(c, FSFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
+      FS_CUDA(cudaEventRecord(c->ev1, c->stream));
+      FS_CUDA(cudaEventSynchronize(c->ev1));
+      c->rep.t_symbolic_ms = elapsed(c->ev0, c->ev1);
+      c->vals.ensure(9 * c->nblk);
+      c->face_s.ensure(16 * c->nf);
+      c->have_pattern = true;
+      drop_graph(c);
+    }
+    const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double mu = E / (2.0 * (1.0 + nu));
+    FS_CUDA(cudaEventRecord(c->ev0, c->stream));
+    face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
+                  c->face_s.get(), c->stream);
+    assemble_rows_device(c->node_ptr.get(), c->nbr.get(), c->nf_ptr.get(), c->nf_idx.get(), c->face_nodes.get(),
+                         c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(), c->stream);
+    FS_CUDA(cudaEventRecord(c->ev1, c->stream));
+    FS_CUDA(cudaEventSynchronize(c->ev1));
+    c->rep.t_numeric_ms = elapsed(c->ev0, c->ev1);
+    c->E = E;
+    c->nu = nu;
+    if (row_begin) *row_begin = 3 * c->n_lo;
+    if (n_rows) *n_rows = 3 * c->nloc;
+    if (nnz) *nnz = 9 * c->nblk;
+    c->stage = kAssembled;
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_get_csr(const fsfem_ctx* cc, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  fsfem_ctx* c = const_cast<fsfem_ctx*>(cc);
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
+    const int64_t nnz = 9 * c->nblk, nr = 3 * c->nloc;
+    if (row_ptr || col_idx) {
+      DevBuf<int64_t> rp;
+      DevBuf<int32_t> ci;
+      rp.ensure(nr + 1);
+      ci.ensure(nnz);
+      if (c->nloc > 0) expand_csr_device(c->node_ptr.get(), c->nbr.get(), c->nloc, rp.get(), ci.get(), c->stream);
+      else FS_CUDA(cudaMemsetAsync(rp.get(), 0, sizeof(int64_t), c->stream));
+      from_device(row_ptr, rp.get(), sizeof(int64_t) * (nr + 1), c->stream);
+      from_device(col_idx, ci.get(), sizeof(int32_t) * nnz, c->stream);
+      FS_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    from_device(vals, c->vals.get(), sizeof(double) * nnz, c->stream);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_apply_bc(fsfem_ctx* c, const int32_t* dirichlet, int64_t n_dir, const double* loads, int mode,
+                            double penalty_scale) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
+    if (c->stage >= kBc) return fail(c, FSFEM_ERR_STATE, "BCs already applied: re-assemble first");
+    if (!loads || n_dir < 0 || (n_dir > 0 && !dirichlet) || (mode != 0 && mode != 1))
+      return fail(c, FSFEM_ERR_INVALID_ARG, "bad dirichlet/loads/mode");
+    if (mode == 1 && c->nranks > 1) return fail(c, FSFEM_ERR_UNSUPPORTED, "PENALTY mode is single-GPU only");
+    const int64_t n = 3 * c->nloc;
+    c->f.ensure(std::max<int64_t>(n, 1));
+    c->dinv.ensure(std::max<int64_t>(n, 1));
+    c->fixed.ensure(c->nn);
+    c->staging.ensure(3 * c->nn);
+    c->staging_i.ensure(std::max<int64_t>(n_dir, 1));
+    FS_CUDA(cudaEventRecord(c->ev0, c->stream));
+    to_device(c->staging.get(), loads, sizeof(double) * 3 * c->nn, c->stream);
+    to_device(c->staging_i.get(), dirichlet, sizeof(int32_t) * n_dir, c->stream);
+    apply_bc_device(c->node_ptr.get(), c->nbr.get(), c->diag_slot.get(), c->n_lo, c->nloc, c->nn, c->staging_i.get(),
+                    n_dir, c->staging.get(), mode, penalty_scale, c->vals.get(), c->f.get(), c->dinv.get(),
+                    c->fixed.get(), c->flags.get(), c->stream);
+    FS_CUDA(cudaEventRecord(c->ev1, c->stream));
+    FS_CUDA(cudaMemcpyAsync(c->h_flags, c->flags.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    fsfem_status s = decode_flags(c, c->h_flags[0], "apply_bc");
+    if (s != FSFEM_OK) return s;
+    c->rep.t_bc_ms = elapsed(c->ev0, c->ev1);
+    c->stage = kBc;
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_spmv(fsfem_ctx* c, const double* p, double* q) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
+    if (!p || !q) return fail(c, FSFEM_ERR_INVALID_ARG, "null vector");
+    const int64_t nfull = 3 * c->chunk * c->nranks;
+    c->x_full.ensure(nfull);
+    c->q.ensure(std::max<int64_t>(3 * c->nloc, 1));
+    to_device(c->x_full.get(), p, sizeof(double) * 3 * c->nn, c->stream);
+    launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->x_full.get(), 0, c->q.get(), nullptr,
+                nullptr, false, c->stream);
+    from_device(q + 3 * c->n_lo, c->q.get(), sizeof(double) * 3 * c->nloc, c->stream);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel_tol, int64_t max_iter,
+                             fsfem_report* rep) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kBc) return fail(c, FSFEM_ERR_STATE, "apply_bc first");
+    if (!u) return fail(c, FSFEM_ERR_INVALID_ARG, "null u");
+    const int64_t n = 3 * c->nloc;
+    const int64_t nglob = 3 * c->nn;
+    const int64_t nfull = 3 * c->chunk * c->nranks;
+    if (rel_tol <= 0.0) rel_tol = 1e-10;
+    if (max_iter <= 0) max_iter = std::max<int64_t>(1000, static_cast<int64_t>(20.0 * std::sqrt(double(nglob))));
+    c->x_full.ensure(nfull);
+    c->p_full.ensure(nfull);
+    c->r.ensure(std::max<int64_t>(n, 1));
+    c->q.ensure(std::max<int64_t>(n, 1));
+    c->part.ensure(4 * static_cast<size_t>(pcg_grid()));
+    c->all.ensure(4 * static_cast<size_t>(c->nranks));
+    PcgState* st = c->st.get();
+    std::memset(c->h_st, 0, sizeof(PcgState));
+    c->h_st->tol = rel_tol;
+    c->h_st->max_iter = max_iter;
+    c->h_st->nranks = c->nranks;
+
+    FS_CUDA(cudaEventRecord(c->ev0, c->stream));
+    FS_CUDA(cudaMemcpyAsync(st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
+    FS_CUDA(cudaMemsetAsync(c->x_full.get(), 0, sizeof(double) * nfull, c->stream));
+    FS_CUDA(cudaMemsetAsync(c->p_full.get(), 0, sizeof(double) * nfull, c->stream));
+    double* own_x = c->x_full.get() + 3 * c->n_lo;
+    double* own_p = c->p_full.get() + 3 * c->n_lo;
+    const double* q0 = nullptr;
+    if (!u0_is_zero) {
+      to_device(c->x_full.get(), u, sizeof(double) * nglob, c->stream);
+      launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->x_full.get(), 0, c->q.get(), nullptr,
+                  nullptr, false, c->stream);
+      q0 = c->q.get();
+    }
+    launch_init(c->f.get(), q0, c->dinv.get(), c->r.get(), own_p, n, st, c->part.get(), c->stream);
+    if (c->nranks > 1) {
+      combine(c, 0);
+      gather_full(c, c->p_full.get());
+    }
+    FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+
+    // graph of kBatch iterations with event pairs around each SpMV
+    const void* key[4] = {c->vals.get(), c->x_full.get(), c->p_full.get(), c->r.get()};
+    if (!c->graph || std::memcmp(key, c->graph_key, sizeof(key)) != 0) {
+      drop_graph(c);
+      cudaGraph_t g;
+      FS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      set_capturing(true);
+      try {
+        for (int it = 0; it < kBatch; ++it) pcg_iteration(c, c->spmv_ev[2 * it], c->spmv_ev[2 * it + 1]);
+      } catch (...) {
+        set_capturing(false);
+        cudaStreamEndCapture(c->stream, &g);
+        throw;
+      }
+      set_capturing(false);
+      FS_CUDA(cudaStreamEndCapture(c->stream, &g));
+      FS_CUDA(cudaGraphInstantiate(&c->graph, g, 0));
+      cudaGraphDestroy(g);
+      std::memcpy(c->graph_key, key, sizeof(key));
+    }
+    double spmv_ms = 0.0;
+    int64_t spmv_n = 0;
+    while (c->h_st->done_d == 0.0) {
+      const long long before = c->h_st->iters;
+      FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
+      count_launch((c->nranks > 1 ? 5 : 3) * kBatch);
+      FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+      FS_CUDA(cudaStreamSynchronize(c->stream));
+      const long long ran = std::min<long long>(kBatch, c->h_st->iters - before);
+      for (long long it = 0; it < ran; ++it) {
+        spmv_ms += elapsed(c->spmv_ev[2 * it], c->spmv_ev[2 * it + 1]);
+        ++spmv_n;
+      }
+      if (c->h_st->iters == before && c->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg made no progress");
+    }
+    FS_CUDA(cudaEventRecord(c->ev1, c->stream));
+    // true residual ||f - K x|| / ||f||
+    gather_full(c, c->x_full.get());
+    launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->x_full.get(), 0, c->q.get(), nullptr, nullptr,
+                false, c->stream);
+    launch_resid(c->f.get(), c->q.get(), n, st, c->part.get(), c->stream);
+    if (c->nranks > 1) combine(c, 3);
+    from_device(u, c->x_full.get(), sizeof(double) * nglob, c->stream);
+    FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    (void)own_x;
+    const PcgState& h = *c->h_st;
+    c->rep.iterations = h.iters;
+    c->rep.converged = (h.status == FSFEM_OK) ? 1 : 0;
+    c->rep.rel_residual = h.ff > 0 ? std::sqrt(h.rr / h.ff) : 0.0;
+    c->rep.true_rel_residual = h.ff > 0 ? std::sqrt(h.local[3] / h.ff) : 0.0;
+    c->rep.t_pcg_ms = elapsed(c->ev0, c->ev1);
+    c->rep.t_spmv_ms = spmv_ms;
+    c->rep.spmv_launches = spmv_n;
+    c->rep.kernel_launches = launch_count();
+    if (rep) *rep = c->rep;
+    if (h.status == FSFEM_ERR_BREAKDOWN) return fail(c, FSFEM_ERR_BREAKDOWN, "pcg breakdown (p.q <= 0 or non-finite)");
+    if (h.status == FSFEM_ERR_NOT_CONVERGED)
+      return fail(c, FSFEM_ERR_NOT_CONVERGED, "pcg reached max_iter=" + std::to_string(max_iter));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_get_report(const fsfem_ctx* c, fsfem_report* rep) {
+  if (!c || !rep) return FSFEM_ERR_INVALID_ARG;
+  *rep = c->rep;
+  return FSFEM_OK;
+}
+
+}  // extern "C"

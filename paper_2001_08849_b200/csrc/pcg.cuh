@@ -1,0 +1,79 @@
+// Device-resident PCG scalars and the scalar steps of the recurrence.
+#pragma once
+#include "common.cuh"
+
+namespace fsfem {
+
+struct PcgState {
+  double rho;       // r.z
+  double alpha, beta;
+  double rr;        // r.r (recurrence residual squared)
+  double ff;        // f.f
+  double tol;       // relative tolerance on ||r|| / ||f||
+  double pq;        // p.q
+  double done_d;    // != 0: stop (converged, breakdown or max_iter)
+  double local[4];  // this rank's partial sums (multi-rank) / true residual^2 (slot 3)
+  long long iters;
+  long long max_iter;
+  int status;       // FSFEM_OK, FSFEM_ERR_NOT_CONVERGED or FSFEM_ERR_BREAKDOWN
+  int nranks;
+  unsigned int ticket[4];
+};
+
+__device__ __forceinline__ void pcg_stop(PcgState* st, int status) {
+  st->status = status;
+  st->done_d = 1.0;
+}
+
+__device__ __forceinline__ void finish_init(PcgState* st, double rz, double rr, double ff) {
+  st->rho = rz;
+  st->rr = rr;
+  st->ff = ff;
+  st->iters = 0;
+  st->status = FSFEM_OK;
+  st->done_d = 0.0;
+  if (!isfinite(rz) || !isfinite(rr) || !isfinite(ff)) {
+    pcg_stop(st, FSFEM_ERR_BREAKDOWN);
+  } else if (ff == 0.0 || sqrt(rr) <= st->tol * sqrt(ff)) {
+    pcg_stop(st, FSFEM_OK);
+  } else if (st->max_iter <= 0) {
+    pcg_stop(st, FSFEM_ERR_NOT_CONVERGED);
+  }
+}
+
+__device__ __forceinline__ void finish_alpha(PcgState* st, double pq) {
+  st->pq = pq;
+  if (!(pq > 0.0) || !isfinite(pq)) {
+    pcg_stop(st, FSFEM_ERR_BREAKDOWN);
+  } else {
+    st->alpha = st->rho / pq;
+  }
+}
+
+__device__ __forceinline__ void finish_beta(PcgState* st, double rr, double rz) {
+  st->iters += 1;
+  st->rr = rr;
+  if (!isfinite(rr) || !isfinite(rz)) {
+    pcg_stop(st, FSFEM_ERR_BREAKDOWN);
+  } else if (sqrt(rr) <= st->tol * sqrt(st->ff)) {
+    pcg_stop(st, FSFEM_OK);
+  } else if (st->iters >= st->max_iter) {
+    pcg_stop(st, FSFEM_ERR_NOT_CONVERGED);
+  } else {
+    st->beta = rz / st->rho;
+    st->rho = rz;
+  }
+}
+
+int pcg_grid();
+void launch_spmv(const int64_t* node_ptr, const int32_t* nbr, const double* vals, int64_t nloc, const double* x_full,
+                 int64_t own_off, double* y, PcgState* st, double* part, bool pcg, cudaStream_t s);
+void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,
+                   double* part, cudaStream_t s);
+void launch_direction(double* p, const double* r, const double* dinv, int64_t n, PcgState* st, cudaStream_t s);
+void launch_init(const double* f, const double* q, const double* dinv, double* r, double* p, int64_t n, PcgState* st,
+                 double* part, cudaStream_t s);
+void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s);
+void launch_combine(PcgState* st, const double* all, int stage, cudaStream_t s);
+
+}  // namespace fsfem

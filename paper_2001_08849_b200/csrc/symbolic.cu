@@ -1,0 +1,257 @@
+// S5 — symbolic CSR (the pattern of PAPER.md:449 sparse(), built before any value exists).
+//
+// Node graph of FS-FEM: j is a neighbour of i iff some smoothing domain (face) has both in its
+// field.  The field of face f is nodes(t0) U nodes(t1), so the faces whose field holds i are
+// exactly the faces of the tets containing i, and
+//     nbr(i) = U_{t ni i} ( nodes(t) U { node across each interior face of t } ).
+// Every neighbour pair is a dense 3x3 block (Q13): rows 3i..3i+2 have 3*deg(i) entries each,
+// stored contiguously (row-major) at vals[9*P_i ..], P = exclusive scan of deg.
+// Per own node we also keep F(i) = the ascending list of faces whose field holds i (the
+// summation order of the numeric assembly) and the slot of i inside nbr(i) (the diagonal).
+#include "common.cuh"
+
+namespace fsfem {
+
+namespace {
+
+constexpr int kPatWarps = 4;
+constexpr int kMaxTetsPerNode = 128;                 // UNSUPPORTED beyond (general meshes: ~20-60)
+constexpr int kCandCap = 8 * kMaxTetsPerNode;        // node candidates per node
+constexpr int kSentinel = 0x7fffffff;
+
+__global__ void k_count_node_tets(const int32_t* __restrict__ tets, int64_t nt4, int64_t n_lo, int64_t n_hi,
+                                  int32_t* __restrict__ cnt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nt4; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = tets[k];
+    if (v >= n_lo && v < n_hi) atomicAdd(&cnt[v - n_lo], 1);
+  }
+}
+
+__global__ void k_scatter_node_tets(const int32_t* __restrict__ tets, int64_t nt4, int64_t n_lo, int64_t n_hi,
+                                    const int32_t* __restrict__ ptr, int32_t* __restrict__ cur,
+                                    int32_t* __restrict__ idx) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nt4; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = tets[k];
+    if (v >= n_lo && v < n_hi) idx[ptr[v - n_lo] + atomicAdd(&cur[v - n_lo], 1)] = static_cast<int32_t>(k >> 2);
+  }
+}
+
+// Stable rank sort of n ints in smem (src -> dst), then compaction of distinct values
+// (excluding kSentinel) back into src.  Returns the number of distinct values.  Warp-wide.
+__device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int n, int lane) {
+  for (int i = lane; i < n; i += 32) {
+    const int32_t v = src[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const int32_t u = src[j];
+      r += (u < v || (u == v && j < i)) ? 1 : 0;
+    }
+    dst[r] = v;
+  }
+  __syncwarp();
+  int count = 0;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int i = c0 + lane;
+    const bool keep = i < n && dst[i] != kSentinel && (i == 0 || dst[i - 1] != dst[i]);
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+    if (keep) src[count + __popc(ball & ((1u << lane) - 1u))] = dst[i];
+    count += __popc(ball);
+  }
+  __syncwarp();
+  return count;
+}
+
+// Warp per own node.  Pass 1 (kWrite = false) counts deg(i) and |F(i)|; pass 2 writes the
+// sorted lists at node_ptr / nf_ptr and the diagonal slot.
+template <bool kWrite>
+__global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
+    const int32_t* __restrict__ tets, const int32_t* __restrict__ tet_face, const int32_t* __restrict__ face_tet,
+    const int32_t* __restrict__ face_opp, const int32_t* __restrict__ nt_ptr, const int32_t* __restrict__ nt_idx,
+    int64_t n_lo, int64_t nloc, int32_t* __restrict__ deg, int32_t* __restrict__ nfc,
+    const int64_t* __restrict__ node_ptr, const int64_t* __restrict__ nf_ptr, int32_t* __restrict__ nbr,
+    int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err) {
+  __shared__ int32_t cand[kPatWarps][kCandCap], tmp[kPatWarps][kCandCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t il = blockIdx.x * (int64_t)kPatWarps + w; il < nloc; il += (int64_t)gridDim.x * kPatWarps) {
+    const int32_t b = nt_ptr[il];
+    const int ntet = nt_ptr[il + 1] - b;
+    if (ntet > kMaxTetsPerNode) {
+      if (lane == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, n_lo + il);
+      continue;
+    }
+    // candidates: 4 vertices + 4 across-face nodes per tet
+    for (int k = lane; k < ntet; k += 32) {
+      const int32_t t = nt_idx[b + k];
+      const int4 v = reinterpret_cast<const int4*>(tets)[t];
+      cand[w][8 * k + 0] = v.x;
+      cand[w][8 * k + 1] = v.y;
+      cand[w][8 * k + 2] = v.z;
+      cand[w][8 * k + 3] = v.w;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const int32_t f = tet_face[4 * t + l];
+        const int32_t ta = face_tet[2 * f], tb = face_tet[2 * f + 1];
+        int32_t across = kSentinel;
+        if (tb >= 0) across = (ta == t) ? face_opp[2 * f + 1] : face_opp[2 * f];
+        cand[w][8 * k + 4 + l] = across;
+      }
+    }
+    __syncwarp();
+    const int dn = warp_sort_unique(cand[w], tmp[w], 8 * ntet, lane);
+    if (!kWrite) {
+      if (lane == 0) deg[il] = dn;
+    } else {
+      const int64_t P = node_ptr[il];
+      const int32_t self = static_cast<int32_t>(n_lo + il);
+      for (int k = lane; k < dn; k += 32) {
+        const int32_t j = cand[w][k];
+        nbr[P + k] = j;
+        if (j == self) diag_slot[il] = k;
+      }
+    }
+    __syncwarp();
+    // faces whose field holds i: the 4 faces of every tet containing i (shared ones twice)
+    for (int k = lane; k < ntet; k += 32) {
+      const int32_t t = nt_idx[b + k];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) cand[w][4 * k + l] = tet_face[4 * t + l];
+    }
+    __syncwarp();
+    const int fn = warp_sort_unique(cand[w], tmp[w], 4 * ntet, lane);
+    if (!kWrite) {
+      if (lane == 0) nfc[il] = fn;
+    } else {
+      const int64_t Q = nf_ptr[il];
+      for (int k = lane; k < fn; k += 32) nf_idx[Q + k] = cand[w][k];
+    }
+    __syncwarp();
+  }
+}
+
+// Warp per segment: sort the tets of each node ascending (the atomic scatter left them in
+// arbitrary order).  Values in a segment are distinct.
+__global__ void __launch_bounds__(kPatWarps * 32) k_sort_segments(const int32_t* __restrict__ ptr, int64_t nseg,
+                                                                  int32_t* __restrict__ idx,
+                                                                  unsigned long long* __restrict__ err) {
+  __shared__ int32_t a[kPatWarps][kMaxTetsPerNode], o[kPatWarps][kMaxTetsPerNode];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t s = blockIdx.x * (int64_t)kPatWarps + w; s < nseg; s += (int64_t)gridDim.x * kPatWarps) {
+    const int32_t b = ptr[s];
+    const int n = ptr[s + 1] - b;
+    if (n > kMaxTetsPerNode) {
+      if (lane == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, s);
+      continue;
+    }
+    for (int i = lane; i < n; i += 32) a[w][i] = idx[b + i];
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const int32_t v = a[w][i];
+      int r = 0;
+      for (int j = 0; j < n; ++j) r += a[w][j] < v ? 1 : 0;
+      o[w][r] = v;
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) idx[b + i] = o[w][i];
+    __syncwarp();
+  }
+}
+
+// Expand the node pattern to the public CSR (row_ptr int64, col_idx int32).
+__global__ void k_expand_csr(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, int64_t nloc,
+                             int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t il = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; il < nloc;
+       il += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t P = node_ptr[il];
+    const int deg = static_cast<int>(node_ptr[il + 1] - P);
+    const int m = 3 * deg;
+    if (lane < 3) row_ptr[3 * il + lane] = 9 * P + lane * m;
+    if (il == nloc - 1 && lane == 0) row_ptr[3 * nloc] = 9 * node_ptr[nloc];
+    for (int k = lane; k < m; k += 32) {
+      const int32_t col = 3 * nbr[P + k / 3] + k % 3;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) col_idx[9 * P + a * m + k] = col;
+    }
+  }
+}
+
+}  // namespace
+
+// Host driver of S5 for the own node range [n_lo, n_lo + nloc).
+void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
+                          const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
+                          DevBuf<unsigned char>& scratch, DevBuf<int64_t>& node_ptr, DevBuf<int32_t>& nbr,
+                          DevBuf<int64_t>& nf_ptr, DevBuf<int32_t>& nf_idx, DevBuf<int32_t>& diag_slot,
+                          unsigned long long* h_flags, int64_t* nblk_out, int64_t* nfi_out) {
+  const int sms = num_sms();
+  size_t o = 0;
+  auto carve = [&](size_t bytes) {
+    size_t at = o;
+    o += (bytes + 255) & ~size_t(255);
+    return at;
+  };
+  const size_t o_cnt = carve(sizeof(int32_t) * (nloc + 1));
+  const size_t o_ptr = carve(sizeof(int32_t) * (nloc + 1));
+  const size_t o_cur = carve(sizeof(int32_t) * (nloc + 1));
+  const size_t o_idx = carve(sizeof(int32_t) * 4 * nt);
+  const size_t o_deg = carve(sizeof(int32_t) * (nloc + 1));
+  const size_t o_nfc = carve(sizeof(int32_t) * (nloc + 1));
+  const size_t o_flags = carve(sizeof(unsigned long long) * 2);
+  const size_t o_tmp = carve(scan_tmp_bytes(nloc + 1));
+  unsigned char* base = scratch.ensure(o);
+  int32_t* cnt = reinterpret_cast<int32_t*>(base + o_cnt);
+  int32_t* ptr = reinterpret_cast<int32_t*>(base + o_ptr);
+  int32_t* cur = reinterpret_cast<int32_t*>(base + o_cur);
+  int32_t* idx = reinterpret_cast<int32_t*>(base + o_idx);
+  int32_t* deg = reinterpret_cast<int32_t*>(base + o_deg);
+  int32_t* nfc = reinterpret_cast<int32_t*>(base + o_nfc);
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(base + o_flags);
+  void* tmp = base + o_tmp;
+  const size_t tb = scan_tmp_bytes(nloc + 1);
+
+  FS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nloc + 1), s));
+  FS_CUDA(cudaMemsetAsync(cur, 0, sizeof(int32_t) * (nloc + 1), s));
+  FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
+  const int g4 = static_cast<int>(std::min<int64_t>(ceil_div(4 * nt, 256), 8LL * sms));
+  k_count_node_tets<<<g4, 256, 0, s>>>(d_tets, 4 * nt, n_lo, n_lo + nloc, cnt);
+  FS_LAUNCH_CHECK();
+  exclusive_scan_i32(cnt, ptr, nloc, s, tmp, tb);
+  k_scatter_node_tets<<<g4, 256, 0, s>>>(d_tets, 4 * nt, n_lo, n_lo + nloc, ptr, cur, idx);
+  FS_LAUNCH_CHECK();
+  const int gw = static_cast<int>(std::min<int64_t>(ceil_div(nloc, kPatWarps), 32LL * sms));
+  k_sort_segments<<<gw, kPatWarps * 32, 0, s>>>(ptr, nloc, idx, flags);
+  FS_LAUNCH_CHECK();
+  k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc, deg,
+                                                      nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags);
+  FS_LAUNCH_CHECK();
+  node_ptr.ensure(nloc + 1);
+  nf_ptr.ensure(nloc + 1);
+  exclusive_scan_i32_to_i64(deg, node_ptr.get(), nloc, s, tmp, tb);
+  exclusive_scan_i32_to_i64(nfc, nf_ptr.get(), nloc, s, tmp, tb);
+  int64_t tot[2];
+  FS_CUDA(cudaMemcpyAsync(&tot[0], node_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(&tot[1], nf_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  if (h_flags[0] != kNoError) return;
+  *nblk_out = tot[0];
+  *nfi_out = tot[1];
+  nbr.ensure(tot[0]);
+  nf_idx.ensure(tot[1]);
+  diag_slot.ensure(nloc);
+  k_node_pattern<true><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc,
+                                                     nullptr, nullptr, node_ptr.get(), nf_ptr.get(), nbr.get(),
+                                                     nf_idx.get(), diag_slot.get(), flags);
+  FS_LAUNCH_CHECK();
+  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+}
+
+void expand_csr_device(const int64_t* node_ptr, const int32_t* nbr, int64_t nloc, int64_t* row_ptr, int32_t* col_idx,
+                       cudaStream_t s) {
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
+  k_expand_csr<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nloc, row_ptr, col_idx);
+  FS_LAUNCH_CHECK();
+}
+
+}  // namespace fsfem

@@ -1,0 +1,268 @@
+"""Thin ctypes binding of libfsfem.so (include/fsfem.h): argument marshalling only.
+
+Every step of the path runs in the library's sm_100a kernels.  There is no CPU fallback:
+if the shared library is missing or cannot be loaded, importing/calling raises.
+Arrays may be numpy arrays (host) or torch tensors (host or CUDA); the library detects
+host vs device pointers itself (include/fsfem.h, "Memory").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfsfem.so")
+
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "UNSUPPORTED", 5: "NOT_CONVERGED",
+                6: "BREAKDOWN", 7: "STATE", 8: "CUDA", 9: "NCCL", 10: "OOM"}
+
+# Every symbol include/fsfem.h declares (checked by tests/test_abi.py).
+EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init",
+           "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
+           "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv"]
+
+
+class FsfemReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("rel_residual", ctypes.c_double), ("true_rel_residual", ctypes.c_double),
+                ("t_faces_ms", ctypes.c_double), ("t_symbolic_ms", ctypes.c_double),
+                ("t_numeric_ms", ctypes.c_double), ("t_bc_ms", ctypes.c_double), ("t_pcg_ms", ctypes.c_double),
+                ("t_spmv_ms", ctypes.c_double), ("spmv_launches", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "_pad"}
+
+
+class FsfemError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fsfem {STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS_NAMES.get(code, str(code))
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libfsfem.so (raises OSError if it is missing: build it with paper_2001_08849_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"{path} not found: run `python -m paper_2001_08849_b200.build` (no CPU fallback exists)")
+    L = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+    P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    sig = {
+        "fsfem_status_string": (ctypes.c_char_p, [I]),
+        "fsfem_create": (I, [I, P, ctypes.POINTER(P)]),
+        "fsfem_destroy": (I, [P]),
+        "fsfem_last_error": (ctypes.c_char_p, [P]),
+        "fsfem_comm_init": (I, [P, P, I, I]),
+        "fsfem_nccl_get_unique_id": (I, [P]),
+        "fsfem_build_faces": (I, [P, P, I64, P, I64, P, P]),
+        "fsfem_get_faces": (I, [P, P, P, P]),
+        "fsfem_assemble_csr": (I, [P, D, D, P, P, P]),
+        "fsfem_get_csr": (I, [P, P, P, P]),
+        "fsfem_apply_bc": (I, [P, P, I64, P, I, D]),
+        "fsfem_pcg_solve": (I, [P, P, I, D, I64, ctypes.POINTER(FsfemReport)]),
+        "fsfem_get_report": (I, [P, ctypes.POINTER(FsfemReport)]),
+        "fsfem_spmv": (I, [P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _ptr(a):
+    """Raw pointer of a numpy array or torch tensor (host or device); None -> NULL."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(a.ctypes.data)
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(a.data_ptr())
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _check_dtype(a, np_dtype, name):
+    if a is None:
+        return
+    if isinstance(a, np.ndarray):
+        if a.dtype != np_dtype:
+            raise TypeError(f"{name} must be {np.dtype(np_dtype).name}, got {a.dtype}")
+    else:
+        want = {np.float64: "torch.float64", np.int32: "torch.int32", np.int64: "torch.int64"}[np_dtype]
+        if str(a.dtype) != want:
+            raise TypeError(f"{name} must be {want}, got {a.dtype}")
+
+
+def _nelem(a):
+    return a.size if isinstance(a, np.ndarray) else a.numel()
+
+
+# ------------------------------------------------------------------ C-ABI mirror (same names)
+def fsfem_create(cuda_device: int = 0, cuda_stream: int | None = None):
+    L = load_library()
+    h = ctypes.c_void_p()
+    st = L.fsfem_create(cuda_device, ctypes.c_void_p(cuda_stream) if cuda_stream else None, ctypes.byref(h))
+    if st != 0:
+        raise FsfemError(st, "fsfem_create failed")
+    return h
+
+
+def fsfem_destroy(ctx) -> None:
+    load_library().fsfem_destroy(ctx)
+
+
+def _raise(ctx, st):
+    if st != 0:
+        raise FsfemError(st, load_library().fsfem_last_error(ctx).decode())
+
+
+def fsfem_nccl_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = load_library().fsfem_nccl_get_unique_id(buf)
+    if st != 0:
+        raise FsfemError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def fsfem_comm_init(ctx, unique_id: bytes, rank: int, nranks: int) -> None:
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _raise(ctx, load_library().fsfem_comm_init(ctx, buf, rank, nranks))
+
+
+def fsfem_build_faces(ctx, xyz, tets):
+    _check_dtype(xyz, np.float64, "xyz")
+    _check_dtype(tets, np.int32, "tets")
+    nf, ni = ctypes.c_int64(), ctypes.c_int64()
+    _raise(ctx, load_library().fsfem_build_faces(ctx, _ptr(xyz), _nelem(xyz) // 3, _ptr(tets), _nelem(tets) // 4,
+                                                 ctypes.byref(nf), ctypes.byref(ni)))
+    return nf.value, ni.value
+
+
+def fsfem_get_faces(ctx, face_nodes, face_tet, face_opp) -> None:
+    _raise(ctx, load_library().fsfem_get_faces(ctx, _ptr(face_nodes), _ptr(face_tet), _ptr(face_opp)))
+
+
+def fsfem_assemble_csr(ctx, E: float, nu: float):
+    rb, nr, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _raise(ctx, load_library().fsfem_assemble_csr(ctx, E, nu, ctypes.byref(rb), ctypes.byref(nr), ctypes.byref(nnz)))
+    return rb.value, nr.value, nnz.value
+
+
+def fsfem_get_csr(ctx, row_ptr, col_idx, vals) -> None:
+    _raise(ctx, load_library().fsfem_get_csr(ctx, _ptr(row_ptr), _ptr(col_idx), _ptr(vals)))
+
+
+def fsfem_apply_bc(ctx, dirichlet_nodes, loads, mode: int = 0, penalty_scale: float = 0.0) -> None:
+    _check_dtype(dirichlet_nodes, np.int32, "dirichlet_nodes")
+    _check_dtype(loads, np.float64, "loads")
+    _raise(ctx, load_library().fsfem_apply_bc(ctx, _ptr(dirichlet_nodes), _nelem(dirichlet_nodes), _ptr(loads), mode,
+                                              penalty_scale))
+
+
+def fsfem_pcg_solve(ctx, u, u0_is_zero: bool = True, rel_tol: float = 1e-10, max_iter: int = 0,
+                    allow_not_converged: bool = False) -> dict:
+    _check_dtype(u, np.float64, "u")
+    rep = FsfemReport()
+    st = load_library().fsfem_pcg_solve(ctx, _ptr(u), 1 if u0_is_zero else 0, rel_tol, max_iter, ctypes.byref(rep))
+    d = rep.as_dict()
+    d["status"] = STATUS_NAMES.get(st, st)
+    if st != 0 and not (st == 5 and allow_not_converged):
+        _raise(ctx, st)
+    return d
+
+
+def fsfem_get_report(ctx) -> dict:
+    rep = FsfemReport()
+    _raise(ctx, load_library().fsfem_get_report(ctx, ctypes.byref(rep)))
+    return rep.as_dict()
+
+
+def fsfem_spmv(ctx, p, q) -> None:
+    _raise(ctx, load_library().fsfem_spmv(ctx, _ptr(p), _ptr(q)))
+
+
+# ------------------------------------------------------------------ convenience object
+@dataclass
+class Csr:
+    row_begin: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+
+
+class FsFem:
+    """One context = one mesh on one GPU (one rank).  Host numpy in, host numpy out."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.ctx = fsfem_create(device, stream)
+        self.n_nodes = self.n_faces = self.n_interior = 0
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            fsfem_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int):
+        fsfem_comm_init(self.ctx, unique_id, rank, nranks)
+
+    def build_faces(self, xyz, tets):
+        self.n_nodes = _nelem(xyz) // 3
+        self.n_faces, self.n_interior = fsfem_build_faces(self.ctx, xyz, tets)
+        return self.n_faces, self.n_interior
+
+    def get_faces(self):
+        fn = np.empty((self.n_faces, 3), np.int32)
+        ft = np.empty((self.n_faces, 2), np.int32)
+        fo = np.empty((self.n_faces, 2), np.int32)
+        fsfem_get_faces(self.ctx, fn, ft, fo)
+        return fn, ft, fo
+
+    def assemble_csr(self, E: float, nu: float):
+        self.row_begin, self.n_rows, self.nnz = fsfem_assemble_csr(self.ctx, E, nu)
+        return self.row_begin, self.n_rows, self.nnz
+
+    def get_csr(self, with_pattern: bool = True) -> Csr:
+        rp = np.empty(self.n_rows + 1, np.int64) if with_pattern else None
+        ci = np.empty(self.nnz, np.int32) if with_pattern else None
+        va = np.empty(self.nnz, np.float64)
+        fsfem_get_csr(self.ctx, rp, ci, va)
+        return Csr(self.row_begin, rp, ci, va)
+
+    def apply_bc(self, dirichlet_nodes, loads, mode: int = 0, penalty_scale: float = 0.0):
+        fsfem_apply_bc(self.ctx, dirichlet_nodes, loads, mode, penalty_scale)
+
+    def pcg_solve(self, u0=None, rel_tol: float = 1e-10, max_iter: int = 0, allow_not_converged: bool = False):
+        u = np.zeros(3 * self.n_nodes) if u0 is None else np.ascontiguousarray(u0, np.float64).reshape(-1).copy()
+        rep = fsfem_pcg_solve(self.ctx, u, u0 is None, rel_tol, max_iter, allow_not_converged)
+        return u, rep
+
+    def spmv(self, p):
+        q = np.zeros(3 * self.n_nodes)
+        fsfem_spmv(self.ctx, np.ascontiguousarray(p, np.float64), q)
+        return q
+
+    def report(self) -> dict:
+        return fsfem_get_report(self.ctx)

@@ -1,0 +1,248 @@
+"""GPU (sm_100a, through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): faces / adjacency / row_ptr / col_idx bit-exact;
+CSR values within 1e-12 * max|K|; displacements within 1e-7 relative L2 at PCG residual 1e-10.
+Full-size configs (4, 5) are checked on sampled rows the oracle computes one by one and on
+properties that hold at any size.
+"""
+import numpy as np
+import pytest
+
+from fsfem_inputs import config_mesh, kuhn_beam, kuhn_counts
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+E, NU = 1.0e6, 0.3
+VAL_TOL = 1e-12
+U_TOL = 1e-7
+
+
+@pytest.fixture(scope="module")
+def fs():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2001_08849_b200 import FsFem, load_library
+    load_library()
+    return FsFem
+
+
+def gpu_faces(FsFem, m):
+    g = FsFem()
+    g.build_faces(m.xyz, m.tets)
+    return g, g.get_faces()
+
+
+def check_faces(FsFem, m):
+    o = Oracle(m.xyz, m.tets)
+    ofn, oft, ofo = o.build_faces()
+    g, (fn, ft, fo) = gpu_faces(FsFem, m)
+    assert (g.n_faces, g.n_interior) == (o.n_faces, o.n_interior)
+    assert np.array_equal(fn, ofn) and np.array_equal(ft, oft) and np.array_equal(fo, ofo)
+    return g, o
+
+
+def small_meshes():
+    yield "cfg1", config_mesh(1)
+    yield "cfg2", config_mesh(2)
+    yield "ragged", kuhn_beam(7, 3, 5, L=3.0, jitter=0.2, jitter_seed=17)
+    yield "ragged_perm", kuhn_beam(9, 5, 3, L=4.0, jitter=0.25, jitter_seed=4, node_perm_seed=8, tet_perm_seed=9)
+    yield "cfg3", config_mesh(3)
+
+
+@pytest.mark.parametrize("name,m", list(small_meshes()), ids=[n for n, _ in small_meshes()])
+def test_faces_bit_exact(fs, name, m):
+    check_faces(fs, m)
+
+
+def test_faces_hand_meshes_and_errors(fs):
+    from paper_2001_08849_b200 import FsfemError
+    xyz = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0.2, 0.3, 1.0], [0.3, 0.2, -0.8]], float)
+    g = fs()
+    assert g.build_faces(xyz, np.array([[0, 1, 2, 3]], np.int32)) == (4, 0)
+    assert g.build_faces(xyz, np.array([[0, 1, 2, 3], [0, 1, 2, 4]], np.int32)) == (7, 1)
+    fn, ft, fo = g.get_faces()
+    k = int(np.nonzero(ft[:, 1] >= 0)[0][0])
+    assert list(fn[k]) == [0, 1, 2] and list(ft[k]) == [0, 1] and list(fo[k]) == [3, 4]
+    bad = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, -1], [1, 1, 1]], float)
+    with pytest.raises(FsfemError) as e:
+        g.build_faces(bad, np.array([[0, 1, 2, 3], [0, 1, 2, 4], [0, 1, 2, 5]], np.int32))
+    assert e.value.status == "TOPOLOGY"
+    with pytest.raises(FsfemError) as e:
+        g.build_faces(xyz, np.array([[0, 1, 2, 9]], np.int32))
+    assert e.value.status == "INVALID_ARG"
+    flat = xyz.copy()
+    flat[3] = [0.3, 0.3, 0.0]
+    with pytest.raises(FsfemError) as e:
+        g.build_faces(flat, np.array([[0, 1, 2, 3]], np.int32))
+    assert e.value.status == "DEGENERATE"
+    with pytest.raises(FsfemError) as e:
+        g.assemble_csr(E, NU)  # failed build leaves the context without faces
+    assert e.value.status == "STATE"
+
+
+def check_csr(g, o, node_lo=0, node_hi=None):
+    """Compare GPU CSR rows of nodes [node_lo, node_hi) with the oracle's."""
+    c = g.get_csr()
+    node_hi = g.n_nodes if node_hi is None else node_hi
+    lo, orp, oci, ova = o.assemble_fs(E, NU, node_lo, node_hi)
+    r0, r1 = 3 * node_lo, 3 * node_hi
+    rp = c.row_ptr[r0:r1 + 1] - c.row_ptr[r0]
+    assert np.array_equal(rp, orp)
+    a, b = c.row_ptr[r0], c.row_ptr[r1]
+    assert np.array_equal(c.col_idx[a:b], oci)
+    kmax = np.abs(ova).max()
+    err = np.abs(c.vals[a:b] - ova).max()
+    assert err <= VAL_TOL * kmax, (err, kmax)
+    return c, kmax
+
+
+@pytest.mark.parametrize("name,m", [x for x in small_meshes() if x[0] != "cfg3"],
+                         ids=[n for n, _ in small_meshes() if n != "cfg3"])
+def test_csr_parity_small(fs, name, m):
+    g, o = check_faces(fs, m)
+    g.assemble_csr(E, NU)
+    assert g.nnz == o.assemble_fs(E, NU)[1][-1]
+    check_csr(g, o)
+    if name.startswith("cfg"):
+        assert g.nnz == kuhn_counts(*m.grid)["nnz_fs"]
+
+
+def test_csr_parity_cfg3_rows(fs):
+    m = config_mesh(3)
+    g, o = check_faces(fs, m)
+    g.assemble_csr(E, NU)
+    check_csr(g, o, 0, 3000)          # first tile run (clamped end)
+    check_csr(g, o, 20000, 20777)     # interior, ragged count
+    check_csr(g, o, m.n_nodes - 1500, m.n_nodes)  # tip end
+
+
+def solve_both(fs, m, mode=0):
+    g, o = check_faces(fs, m)
+    g.assemble_csr(E, NU)
+    o.assemble_fs(E, NU)
+    g.apply_bc(m.dirichlet, m.loads.reshape(-1), mode)
+    orp, oci, ova, of = o.apply_bc(m.dirichlet, m.loads, mode)
+    c = g.get_csr()
+    assert np.array_equal(c.row_ptr, orp) and np.array_equal(c.col_idx, oci)
+    assert np.abs(c.vals - ova).max() <= VAL_TOL * np.abs(ova).max()
+    u, rep = g.pcg_solve(rel_tol=1e-10)
+    uo, orep = o.pcg(1e-10)
+    return g, o, u, rep, uo, orep
+
+
+@pytest.mark.parametrize("name,m", [x for x in small_meshes() if x[0] != "cfg3"],
+                         ids=[n for n, _ in small_meshes() if n != "cfg3"])
+def test_solve_parity(fs, name, m):
+    g, o, u, rep, uo, orep = solve_both(fs, m)
+    assert rep["converged"] == 1 and rep["rel_residual"] <= 1e-10
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+    fixed = np.zeros(3 * m.n_nodes, bool)
+    for d in m.dirichlet:
+        fixed[3 * d:3 * d + 3] = True
+    assert np.all(u[fixed] == 0.0)
+    if name == "cfg1":
+        uc = o.cholesky()
+        assert np.linalg.norm(u - uc) <= U_TOL * np.linalg.norm(uc)
+    assert abs(rep["iterations"] - orep["iterations"]) <= max(3, 0.02 * orep["iterations"])
+
+
+def test_penalty_mode(fs):
+    m = config_mesh(1)
+    g, o, u, rep, uo, orep = solve_both(fs, m, mode=1)
+    assert np.linalg.norm(u - uo) <= 1e-6 * np.linalg.norm(uo)
+
+
+def test_determinism_and_warm_start(fs):
+    m = kuhn_beam(9, 5, 3, L=4.0, jitter=0.25, jitter_seed=4, node_perm_seed=8, tet_perm_seed=9)
+    outs = []
+    for _ in range(2):
+        g = fs()
+        g.build_faces(m.xyz, m.tets)
+        g.assemble_csr(E, NU)
+        v1 = g.get_csr().vals.copy()
+        g.assemble_csr(E, NU)  # numeric-only re-assembly
+        v2 = g.get_csr().vals.copy()
+        assert np.array_equal(v1, v2)
+        g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+        u, rep = g.pcg_solve()
+        outs.append((v1, u))
+        u2, rep2 = g.pcg_solve(u0=u)  # warm start from the solution: converges immediately
+        assert rep2["iterations"] <= 2
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_state_machine(fs):
+    from paper_2001_08849_b200 import FsfemError
+    g = fs()
+    for call in (lambda: g.assemble_csr(E, NU), lambda: g.pcg_solve()):
+        with pytest.raises(FsfemError) as e:
+            call()
+        assert e.value.status == "STATE"
+    m = config_mesh(1)
+    g.build_faces(m.xyz, m.tets)
+    with pytest.raises(FsfemError) as e:
+        g.assemble_csr(E, 0.5)
+    assert e.value.status == "INVALID_ARG"
+
+
+def test_device_pointers_accepted(fs):
+    import torch
+    from paper_2001_08849_b200 import fsfem_build_faces, fsfem_get_faces
+    m = config_mesh(2)
+    g = fs()
+    xyz = torch.from_numpy(m.xyz).cuda()
+    tets = torch.from_numpy(m.tets).cuda()
+    nf, ni = fsfem_build_faces(g.ctx, xyz, tets)
+    fn = torch.empty((nf, 3), dtype=torch.int32, device="cuda")
+    fsfem_get_faces(g.ctx, fn, None, None)
+    o = Oracle(m.xyz, m.tets)
+    ofn, _, _ = o.build_faces()
+    assert np.array_equal(fn.cpu().numpy(), ofn)
+
+
+# ---------------------------------------------------------------- full-size configs (bench launch config)
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_faces_and_sampled_rows(fs, cfg):
+    m = config_mesh(cfg)
+    g = fs()
+    nf, ni = g.build_faces(m.xyz, m.tets)
+    c = kuhn_counts(*m.grid)
+    assert (nf, ni) == (c["n_faces"], c["n_interior"])
+    fn, ft, fo = g.get_faces()
+    # properties at any size: strictly ascending keys, owners contain the face, opp is the 4th node
+    key = (fn[:, 0].astype(np.int64) << 42) | (fn[:, 1].astype(np.int64) << 21) | fn[:, 2]
+    assert np.all(np.diff(key) > 0) and np.all(fn[:, 0] < fn[:, 1]) and np.all(fn[:, 1] < fn[:, 2])
+    for k in (0, 1):
+        sel = ft[:, k] >= 0
+        tt = m.tets[ft[sel, k]]
+        for a in range(3):
+            assert np.all(np.any(tt == fn[sel, a:a + 1], axis=1))
+        assert np.all(np.any(tt == fo[sel, k:k + 1], axis=1))
+        assert not np.any(np.any(fn[sel] == fo[sel, k:k + 1], axis=1))
+    assert np.all(ft[ft[:, 1] >= 0, 0] < ft[ft[:, 1] >= 0, 1])
+    g.assemble_csr(E, NU)
+    assert g.nnz == c["nnz_fs"]
+    o = Oracle(m.xyz, m.tets)
+    o.build_faces()
+    rng = np.random.default_rng(cfg)
+    for lo in [0, m.n_nodes - 400, *rng.integers(0, m.n_nodes - 300, 2)]:
+        check_csr(g, o, int(lo), int(lo) + 257)
+
+
+def test_cfg4_solution_properties(fs):
+    """cfg4 at full size: residual, energy identity, Euler-Bernoulli within 3% (north star)."""
+    m = config_mesh(4)
+    g = fs()
+    g.build_faces(m.xyz, m.tets)
+    g.assemble_csr(E, NU)
+    g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+    u, rep = g.pcg_solve(rel_tol=1e-10)
+    assert rep["converged"] == 1
+    assert rep["true_rel_residual"] < 1e-7
+    f = m.loads.reshape(-1).copy()
+    Ku = g.spmv(u)
+    assert np.isclose(u @ Ku, f @ u, rtol=1e-8)
+    tip = -u.reshape(-1, 3)[m.tip, 2].mean()
+    eb = 1.0 * 10.0 ** 3 / (3 * E * (1.0 / 12.0))
+    assert abs(tip - eb) <= 0.03 * eb, (tip, eb)

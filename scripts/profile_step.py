@@ -1,0 +1,42 @@
+#!/usr/bin/env python
+"""One short pass of the hot path for ncu: faces, assembly (symbolic + numeric, then `--reassemble`
+numeric-only repeats), BCs and a PCG bounded to `--pcg-iters` iterations (NOT_CONVERGED is fine).
+
+    python scripts/profile_step.py --config 4 --pcg-iters 64 --reassemble 2
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--pcg-iters", type=int, default=64)
+    ap.add_argument("--reassemble", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+    from fsfem_inputs import config_mesh
+    from paper_2001_08849_b200 import FsFem, fsfem_apply_bc, fsfem_assemble_csr, fsfem_build_faces, fsfem_pcg_solve
+    m = config_mesh(a.config)
+    dev = torch.device("cuda", 0)
+    g = FsFem(device=0, stream=torch.cuda.current_stream().cuda_stream)
+    xyz = torch.from_numpy(m.xyz).to(dev)
+    tets = torch.from_numpy(m.tets).to(dev)
+    dirichlet = torch.from_numpy(m.dirichlet).to(dev)
+    loads = torch.from_numpy(m.loads.reshape(-1).copy()).to(dev)
+    u = torch.zeros(3 * m.n_nodes, dtype=torch.float64, device=dev)
+    fsfem_build_faces(g.ctx, xyz, tets)
+    for _ in range(1 + a.reassemble):
+        fsfem_assemble_csr(g.ctx, 1.0e6, 0.3)
+    fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
+    rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)
+    torch.cuda.synchronize()
+    print({k: rep[k] for k in ("iterations", "status", "t_numeric_ms", "t_pcg_ms", "t_spmv_ms", "spmv_launches")})
+
+
+if __name__ == "__main__":
+    main()

@@ -36,21 +36,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    """Compile every csrc/*.cu into one sm_100a shared library.  `out`/`defines` serve
+    tuning experiments (scripts/); the product library is SO with no extra defines."""
+    if out == SO and not defines and not force and not needs_build():
         return SO
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+    cmd = [NVCC, *[f"-D{d}" for d in defines], "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include(),
-           *sources(), "-o", SO + ".tmp", "-ldl"]
+           *sources(), "-o", out + ".tmp", "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    args = sys.argv[1:]
+    out = SO
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, defines=defs))

@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "nccl.h"
+#include "pattern.cuh"
 #include "pcg.cuh"
 
 namespace fsfem {
@@ -22,10 +23,8 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
                         unsigned long long* h_flags);
 void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
                           const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
-                          DevBuf<unsigned char>& scratch, DevBuf<int64_t>& node_ptr, DevBuf<int32_t>& nbr,
-                          DevBuf<int64_t>& nf_ptr, DevBuf<int32_t>& nf_idx, DevBuf<int32_t>& diag_slot,
-                          unsigned long long* h_flags, int64_t* nblk_out, int64_t* nfi_out);
-void expand_csr_device(const int64_t* node_ptr, const int32_t* nbr, int64_t nloc, int64_t* row_ptr, int32_t* col_idx,
+                          DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags);
+void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr, int32_t* col_idx, double* vals,
                        cudaStream_t s);
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
                    const int32_t* face_opp, int64_t nf, double* face_s, cudaStream_t s);
@@ -107,11 +106,9 @@ struct fsfem_ctx {
   DevBuf<double> xyz;
   DevBuf<int32_t> tets;
   DevBuf<int32_t> face_nodes, face_tet, face_opp, tet_face;
-  // pattern
+  // pattern (symmetric block storage, pattern.cuh)
   bool have_pattern = false;
-  int64_t nblk = 0, nfi = 0;
-  DevBuf<int64_t> node_ptr, nf_ptr;
-  DevBuf<int32_t> nbr, nf_idx, diag_slot;
+  Pattern pat;
   // numeric
   double E = 0, nu = 0;
   DevBuf<double> face_s, vals;
@@ -230,8 +227,7 @@ void pcg_iteration(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
   double* own_x = c->x_full.get() + 3 * c->n_lo;
   const int64_t n = 3 * c->nloc;
   if (e0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
-  launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->p_full.get(), 3 * c->n_lo, c->q.get(), st,
-              c->part.get(), true, c->stream);
+  launch_spmv(c->pat, c->vals.get(), c->p_full.get(), 3 * c->n_lo, c->q.get(), st, c->part.get(), true, c->stream);
   if (e1) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
   if (c->nranks > 1) combine(c, 1);
   launch_update(own_x, c->r.get(), own_p, c->q.get(), c->dinv.get(), n, st, c->part.get(), c->stream);
@@ -395,15 +391,14 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       FS_CUDA(cudaEventRecord(c->ev0, c->stream));
       c->h_flags[0] = kNoError;
       build_pattern_device(c->tets.get(), c->nt, c->tet_face.get(), c->face_tet.get(), c->face_opp.get(), c->n_lo,
-                           c->nloc, c->stream, c->scratch, c->node_ptr, c->nbr, c->nf_ptr, c->nf_idx, c->diag_slot,
-                           c->h_flags, &c->nblk, &c->nfi);
+                           c->nloc, c->stream, c->scratch, c->pat, c->h_flags);
       fsfem_status s = decode_flags(c, c->h_flags[0], "symbolic");
       if (s != FSFEM_OK) return s;
-      if (9 * c->nblk >= (1LL << 31)) return fail(c, FSFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
+      if (9 * c->pat.nblk >= (1LL << 31)) return fail(c, FSFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
       FS_CUDA(cudaEventRecord(c->ev1, c->stream));
       FS_CUDA(cudaEventSynchronize(c->ev1));
       c->rep.t_symbolic_ms = elapsed(c->ev0, c->ev1);
-      c->vals.ensure(9 * c->nblk);
+      c->vals.ensure(9 * c->pat.nsb + 2);  // + slack for the SpMV bulk copies (pattern.cuh)
       c->face_s.ensure(16 * c->nf);
       c->have_pattern = true;
       drop_graph(c);
@@ -413,7 +408,7 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
     face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
                   c->face_s.get(), c->stream);
-    assemble_rows_device(c->node_ptr.get(), c->nbr.get(), c->nf_ptr.get(), c->nf_idx.get(), c->face_nodes.get(),
+    assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->face_nodes.get(),
                          c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(), c->stream);
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     FS_CUDA(cudaEventSynchronize(c->ev1));
@@ -422,7 +417,7 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     c->nu = nu;
     if (row_begin) *row_begin = 3 * c->n_lo;
     if (n_rows) *n_rows = 3 * c->nloc;
-    if (nnz) *nnz = 9 * c->nblk;
+    if (nnz) *nnz = 9 * c->pat.nblk;
     c->stage = kAssembled;
     return FSFEM_OK;
   });
@@ -432,19 +427,21 @@ fsfem_status fsfem_get_csr(const fsfem_ctx* cc, int64_t* row_ptr, int32_t* col_i
   fsfem_ctx* c = const_cast<fsfem_ctx*>(cc);
   return guarded(c, [&]() -> fsfem_status {
     if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
-    const int64_t nnz = 9 * c->nblk, nr = 3 * c->nloc;
-    if (row_ptr || col_idx) {
-      DevBuf<int64_t> rp;
-      DevBuf<int32_t> ci;
-      rp.ensure(nr + 1);
-      ci.ensure(nnz);
-      if (c->nloc > 0) expand_csr_device(c->node_ptr.get(), c->nbr.get(), c->nloc, rp.get(), ci.get(), c->stream);
-      else FS_CUDA(cudaMemsetAsync(rp.get(), 0, sizeof(int64_t), c->stream));
-      from_device(row_ptr, rp.get(), sizeof(int64_t) * (nr + 1), c->stream);
-      from_device(col_idx, ci.get(), sizeof(int32_t) * nnz, c->stream);
-      FS_CUDA(cudaStreamSynchronize(c->stream));
-    }
-    from_device(vals, c->vals.get(), sizeof(double) * nnz, c->stream);
+    const int64_t nnz = 9 * c->pat.nblk, nr = 3 * c->nloc;
+    DevBuf<int64_t> rp;
+    DevBuf<int32_t> ci;
+    DevBuf<double> vo;
+    int64_t* d_rp = nullptr;
+    int32_t* d_ci = nullptr;
+    double* d_vo = nullptr;
+    if (row_ptr) d_rp = is_device_ptr(row_ptr) ? row_ptr : rp.ensure(nr + 1);
+    if (col_idx) d_ci = is_device_ptr(col_idx) ? col_idx : ci.ensure(std::max<int64_t>(nnz, 1));
+    if (vals) d_vo = is_device_ptr(vals) ? vals : vo.ensure(std::max<int64_t>(nnz, 1));
+    if (c->nloc > 0) export_csr_device(c->pat, c->vals.get(), d_rp, d_ci, d_vo, c->stream);
+    else if (d_rp) FS_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), c->stream));
+    if (row_ptr && d_rp != row_ptr) from_device(row_ptr, d_rp, sizeof(int64_t) * (nr + 1), c->stream);
+    if (col_idx && d_ci != col_idx) from_device(col_idx, d_ci, sizeof(int32_t) * nnz, c->stream);
+    if (vals && d_vo != vals) from_device(vals, d_vo, sizeof(double) * nnz, c->stream);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });
@@ -467,7 +464,7 @@ fsfem_status fsfem_apply_bc(fsfem_ctx* c, const int32_t* dirichlet, int64_t n_di
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
     to_device(c->staging.get(), loads, sizeof(double) * 3 * c->nn, c->stream);
     to_device(c->staging_i.get(), dirichlet, sizeof(int32_t) * n_dir, c->stream);
-    apply_bc_device(c->node_ptr.get(), c->nbr.get(), c->diag_slot.get(), c->n_lo, c->nloc, c->nn, c->staging_i.get(),
+    apply_bc_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.sdiag.get(), c->n_lo, c->nloc, c->nn, c->staging_i.get(),
                     n_dir, c->staging.get(), mode, penalty_scale, c->vals.get(), c->f.get(), c->dinv.get(),
                     c->fixed.get(), c->flags.get(), c->stream);
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
@@ -489,8 +486,7 @@ fsfem_status fsfem_spmv(fsfem_ctx* c, const double* p, double* q) {
     c->x_full.ensure(nfull);
     c->q.ensure(std::max<int64_t>(3 * c->nloc, 1));
     to_device(c->x_full.get(), p, sizeof(double) * 3 * c->nn, c->stream);
-    launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->x_full.get(), 0, c->q.get(), nullptr,
-                nullptr, false, c->stream);
+    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
     from_device(q + 3 * c->n_lo, c->q.get(), sizeof(double) * 3 * c->nloc, c->stream);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
@@ -528,8 +524,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     const double* q0 = nullptr;
     if (!u0_is_zero) {
       to_device(c->x_full.get(), u, sizeof(double) * nglob, c->stream);
-      launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->x_full.get(), 0, c->q.get(), nullptr,
-                  nullptr, false, c->stream);
+      launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
       q0 = c->q.get();
     }
     launch_init(c->f.get(), q0, c->dinv.get(), c->r.get(), own_p, n, st, c->part.get(), c->stream);
@@ -578,8 +573,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     // true residual ||f - K x|| / ||f||
     gather_full(c, c->x_full.get());
-    launch_spmv(c->node_ptr.get(), c->nbr.get(), c->vals.get(), c->nloc, c->x_full.get(), 0, c->q.get(), nullptr, nullptr,
-                false, c->stream);
+    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
     launch_resid(c->f.get(), c->q.get(), n, st, c->part.get(), c->stream);
     if (c->nranks > 1) combine(c, 3);
     from_device(u, c->x_full.get(), sizeof(double) * nglob, c->stream);

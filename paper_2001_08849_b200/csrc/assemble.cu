@@ -100,8 +100,9 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
   }
 }
 
-// Warp per own node i; lane = neighbour slot (chunks of 32 slots).  For every face of F(i)
-// in ascending order, lanes whose neighbour j is in the face's field add s_i s_j^T.
+// Warp per own node i; lane = stored block slot (j >= i, or halo j < n_lo; pattern.cuh), in
+// chunks of 32.  For every face of F(i) in ascending order, lanes whose neighbour j is in the
+// face's field add s_i s_j^T.
 __global__ void __launch_bounds__(256) k_assemble_rows(
     const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, const int64_t* __restrict__ nf_ptr,
     const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
@@ -112,9 +113,8 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
     const int32_t self = static_cast<int32_t>(n_lo + il);
     const int64_t P = node_ptr[il];
     const int deg = static_cast<int>(node_ptr[il + 1] - P);
-    const int m = 3 * deg;
     const int64_t f0 = nf_ptr[il], f1 = nf_ptr[il + 1];
-    double* rows = vals + 9 * P;
+    double* blocks = vals + 9 * P;
     for (int s0 = 0; s0 < deg; s0 += 32) {
       const int s = s0 + lane;
       const int32_t j = (s < deg) ? nbr[P + s] : -2;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
           for (int c = 0; c < 3; ++c) {
             double v = fma(lam, M[3 * a + c], mu * M[3 * c + a]);
             if (a == c) v = fma(mu, tr, v);
-            rows[a * m + 3 * s + c] = v;
+            blocks[9 * s + 3 * a + c] = v;
           }
       }
     }

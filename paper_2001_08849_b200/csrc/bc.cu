@@ -19,8 +19,9 @@ __global__ void k_mark_fixed(const int32_t* __restrict__ dir, int64_t nd, int64_
   }
 }
 
-// MODIFY: warp per own node i.  Block (i, j) is zeroed when i or j is clamped, except the
-// diagonal entries of block (i, i).
+// MODIFY: warp per own node i over its stored blocks (pattern.cuh; the transposed half is the
+// same memory).  Block (i, j) is zeroed when i or j is clamped, except the diagonal entries of
+// block (i, i).
 __global__ void k_bc_modify(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, int64_t n_lo,
                             int64_t nloc, const uint8_t* __restrict__ fixed, double* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
@@ -30,8 +31,7 @@ __global__ void k_bc_modify(const int64_t* __restrict__ node_ptr, const int32_t*
     const bool fi = fixed[i] != 0;
     const int64_t P = node_ptr[il];
     const int deg = static_cast<int>(node_ptr[il + 1] - P);
-    const int m = 3 * deg;
-    double* rows = vals + 9 * P;
+    double* blocks = vals + 9 * P;
     for (int s = lane; s < deg; s += 32) {
       const int32_t j = nbr[P + s];
       if (!(fi || fixed[j])) continue;
@@ -39,7 +39,7 @@ __global__ void k_bc_modify(const int64_t* __restrict__ node_ptr, const int32_t*
       for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          if (!(j == i && a == c)) rows[a * m + 3 * s + c] = 0.0;
+          if (!(j == i && a == c)) blocks[9 * s + 3 * a + c] = 0.0;
     }
   }
 }
@@ -55,9 +55,7 @@ __global__ void k_bc_rhs(const double* __restrict__ loads, const uint8_t* __rest
 }
 
 __device__ __forceinline__ int64_t diag_index(const int64_t* node_ptr, const int32_t* diag_slot, int64_t il, int a) {
-  const int64_t P = node_ptr[il];
-  const int64_t m = 3 * (node_ptr[il + 1] - P);
-  return 9 * P + a * m + 3 * diag_slot[il] + a;
+  return 9 * (node_ptr[il] + diag_slot[il]) + 4 * a;
 }
 
 // max_i K_ii over own rows, as the bit pattern of a non-negative double (ordered like integers).

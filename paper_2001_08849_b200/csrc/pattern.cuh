@@ -1,0 +1,48 @@
+// Symbolic structure of the smoothed stiffness for the own node range [n_lo, n_lo + nloc)
+// (S5; DESIGN.md §5 "symmetric block storage").
+//
+// K is symmetric (Eq. 9: K = sum_k V_k B_k^T c B_k with c symmetric), so each own node row i
+// stores only the 3x3 blocks K_ij with j >= i, plus the blocks whose column node j is below the
+// rank's range (j < n_lo, a "halo" block no local row stores).  The remaining blocks of row i
+// (n_lo <= j < i) are read transposed from row j: K_ij = K_ji^T.  Values are block-contiguous:
+// entry (a, c) of stored block b is vals[9*b + 3*a + c].  Arrays the SpMV streams with bulk
+// copies (sptr, tptr, snbr, tlist, vals) carry >= 16 B of slack after their last element.
+#pragma once
+#include "common.cuh"
+
+namespace fsfem {
+
+// SpMV streaming chunk (pcg.cu): own nodes [n0, n1), their stored blocks [Ps0, Ps1) and
+// transposed entries [Pt0, Pt1).  Chunks hold <= kChunkNodes nodes and <= kCapBlocks of each.
+#ifndef FSFEM_CHUNK_NODES
+#define FSFEM_CHUNK_NODES 32
+#endif
+#ifndef FSFEM_CAP_BLOCKS
+#define FSFEM_CAP_BLOCKS 512
+#endif
+constexpr int kChunkNodes = FSFEM_CHUNK_NODES;
+constexpr int kCapBlocks = FSFEM_CAP_BLOCKS;
+struct SpmvChunk {
+  int32_t n0, n1, Ps0, Ps1, Pt0, Pt1, pad0, pad1;
+};
+
+struct Pattern {
+  int64_t n_lo = 0, nloc = 0;
+  int64_t nblk = 0;  // blocks of the full node graph (public CSR nnz = 9 * nblk)
+  int64_t nsb = 0;   // stored blocks
+  int64_t ntb = 0;   // transposed (gathered) blocks
+  int64_t nfi = 0;   // node-face incidences (sum over own nodes of |F(i)|)
+  DevBuf<int64_t> node_ptr;  // [nloc+1] full neighbour list offsets
+  DevBuf<int32_t> nbr;       // [nblk] sorted neighbour node ids of every own node
+  DevBuf<int64_t> sptr;      // [nloc+1] stored block offsets
+  DevBuf<int32_t> snbr;      // [nsb] column node of each stored block (ascending per row)
+  DevBuf<int32_t> sdiag;     // [nloc] slot of the diagonal block inside the stored row
+  DevBuf<int64_t> tptr;      // [nloc+1] transposed block offsets
+  DevBuf<int2> tlist;        // [ntb] (stored block index of K_ji, node j), ascending j
+  int64_t nchunks = 0;
+  DevBuf<SpmvChunk> chunks;  // [nchunks] SpMV streaming chunks
+  DevBuf<int64_t> nf_ptr;    // [nloc+1]
+  DevBuf<int32_t> nf_idx;    // [nfi] faces whose field holds node i, ascending
+};
+
+}  // namespace fsfem

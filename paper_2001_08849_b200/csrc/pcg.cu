@@ -60,51 +60,232 @@ __device__ __forceinline__ bool grid_reduce(const double (&mine)[NV], double* pa
   return true;
 }
 
-// Warp per own node: y[3il + a] = sum_k vals[9P + a*3deg + k] * x[3*nbr[P + k/3] + k%3].
-// Returns (in lane 0) the three row sums.
-__device__ __forceinline__ void node_rows(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr,
-                                          const double* __restrict__ vals, const double* __restrict__ x, int64_t il,
-                                          double& y0, double& y1, double& y2) {
-  const int lane = threadIdx.x & 31;
-  const int64_t P = node_ptr[il];
-  const int m = static_cast<int>(3 * (node_ptr[il + 1] - P));
-  const double* __restrict__ r0 = vals + 9 * P;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  for (int k = lane; k < m; k += 32) {
-    const int jb = k / 3;
-    const double xv = __ldg(x + 3 * static_cast<int64_t>(__ldg(nbr + P + jb)) + (k - 3 * jb));
-    s0 = fma(__ldcs(r0 + k), xv, s0);
-    s1 = fma(__ldcs(r0 + m + k), xv, s1);
-    s2 = fma(__ldcs(r0 + 2 * m + k), xv, s2);
-  }
-  y0 = warp_sum(s0);
-  y1 = warp_sum(s1);
-  y2 = warp_sum(s2);
+// SpMV over the symmetric block storage (pattern.cuh):
+//   y_i = sum_{stored j} K_ij x_j + sum_{n_lo <= j < i} K_ji^T x_j.
+//
+// Streaming design.  The own nodes are cut (once, with the pattern) into chunks of <= 32 nodes
+// whose stored blocks and transposed-list entries fit a shared-memory stage.  A persistent CTA
+// walks chunks c = blockIdx.x + k*gridDim.x; one thread streams everything contiguous that a
+// chunk needs -- node pointers, stored column ids, the transposed list and the stored 3x3 blocks
+// (the bulk of the HBM traffic) -- into a 2-stage shared-memory ring with cp.async.bulk
+// (TMA bulk copies) completing on an mbarrier, two chunks ahead of the compute.  The compute
+// then only gathers x (L1/L2) and the transposed blocks K_ji (L2: row j < i was streamed a
+// moment earlier by the wavefront of CTAs).
+//
+// Compute: warp per node.  A node's blocks are numbered stored first (0..ds-1), then transposed
+// (ds..ds+nt-1); block k gives three lane-items (k, c), each one x value times three values:
+//   stored block, column c:     y[a] += K_ij[a][c] x_j[c]   (values at 9b + c + 3a, a = 0..2)
+//   transposed block, row c:    y[a] += K_ji[c][a] x_j[c]   (values at 9b + 3c + a, a = 0..2)
+// Fixed order: per-lane sums in item order, then a fixed warp tree; no atomics.
+struct StageLayout {  // every region starts 16-B aligned (cp.async.bulk destinations)
+  // byte offsets inside one stage (16-B aligned), sized for the caps plus alignment slack
+  static constexpr int kPtr = 0;                                    // kChunkNodes + 4 int64 (sptr)
+  static constexpr int kTptr = kPtr + (kChunkNodes + 4) * 8;        // kChunkNodes + 4 int64 (tptr)
+  static constexpr int kSnbr = kTptr + (kChunkNodes + 4) * 8;       // kCapBlocks + 4 int32
+  static constexpr int kTl = kSnbr + ((kCapBlocks + 4) * 4 + 15) / 16 * 16;  // kCapBlocks + 2 int2
+  static constexpr int kVals = kTl + (kCapBlocks + 2) * 8;          // 9 kCapBlocks + 2 double
+  static constexpr int kBytes = kVals + (9 * kCapBlocks + 2) * 8;
+};
+static_assert(StageLayout::kTptr % 16 == 0 && StageLayout::kSnbr % 16 == 0 && StageLayout::kTl % 16 == 0 &&
+                  StageLayout::kVals % 16 == 0 && StageLayout::kBytes % 16 == 0,
+              "stage regions must be 16-B aligned");
+#ifndef FSFEM_SPMV_STAGES
+#define FSFEM_SPMV_STAGES 2
+#endif
+#ifndef FSFEM_SPMV_MINB
+#define FSFEM_SPMV_MINB 2
+#endif
+constexpr int kStages = FSFEM_SPMV_STAGES;
+#ifndef FSFEM_SPMV_EXPERIMENT
+#define FSFEM_SPMV_EXPERIMENT 0  // tuning only: 1 = skip the transposed half
+#endif
+#ifndef FSFEM_SPMV_LANE_ITEMS
+#define FSFEM_SPMV_LANE_ITEMS 6
+#endif
+constexpr int kLaneItems = FSFEM_SPMV_LANE_ITEMS;  // items per lane per round (8 lanes per node)
+constexpr int kStreamSmem = 128 + 64 + 32 * kStages + kStages * StageLayout::kBytes;  // + alignment slack
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Copy elements [e0, e1) of a global array (element size `es`) to smem `dst` with 16-B aligned
+// source and size; returns the element offset of e0 inside dst and adds the bytes to `tx`.
+// The global arrays are allocated with >= 16 B of slack, so the rounded-up tail is readable.
+__device__ __forceinline__ int stage_copy(void* dst, const void* base, int64_t e0, int64_t e1, int es, uint64_t* bar,
+                                          uint32_t& tx) {
+  if (e1 <= e0) return 0;
+  const uintptr_t b = reinterpret_cast<uintptr_t>(base);
+  const uintptr_t a0 = (b + e0 * es) & ~uintptr_t(15);
+  const uintptr_t a1 = (b + e1 * es + 15) & ~uintptr_t(15);
+  const uint32_t bytes = static_cast<uint32_t>(a1 - a0);
+  bulk_g2s(dst, reinterpret_cast<const void*>(a0), bytes, bar);
+  tx += bytes;
+  return static_cast<int>((b + e0 * es - a0) / es);
+}
+
+struct StageInfo {  // written by the issuing thread, read after the mbarrier wait
+  int n0, nn, Ps0, Pt0;
+  int dptr, dsn, dtl, dval;  // element offsets of the first needed element in each smem array
+};
+
+__device__ __forceinline__ void issue_chunk(const SpmvChunk& ch, const int64_t* sptr, const int64_t* tptr,
+                                            const int32_t* snbr, const int2* tlist, const double* vals,
+                                            unsigned char* stage, uint64_t* bar, StageInfo* info) {
+  uint32_t tx = 0;
+  // the expected byte count must be armed before any copy can complete: compute it first
+  const int64_t n0 = ch.n0, n1 = ch.n1, Ps0 = ch.Ps0, Ps1 = ch.Ps1, Pt0 = ch.Pt0, Pt1 = ch.Pt1;
+  auto rbytes = [](const void* base, int64_t e0, int64_t e1, int es) -> uint32_t {
+    if (e1 <= e0) return 0;
+    const uintptr_t b = reinterpret_cast<uintptr_t>(base);
+    return static_cast<uint32_t>(((b + e1 * es + 15) & ~uintptr_t(15)) - ((b + e0 * es) & ~uintptr_t(15)));
+  };
+  const uint32_t total = rbytes(sptr, n0, n1 + 1, 8) + rbytes(tptr, n0, n1 + 1, 8) + rbytes(snbr, Ps0, Ps1, 4) +
+                         rbytes(tlist, Pt0, Pt1, 8) + rbytes(vals, 9 * Ps0, 9 * Ps1, 8);
+  mbar_arrive_expect_tx(bar, total);
+  StageInfo in;
+  in.n0 = static_cast<int>(n0);
+  in.nn = static_cast<int>(n1 - n0);
+  in.Ps0 = static_cast<int>(Ps0);
+  in.Pt0 = static_cast<int>(Pt0);
+  in.dptr = stage_copy(stage + StageLayout::kPtr, sptr, n0, n1 + 1, 8, bar, tx);
+  const int dptr_t = stage_copy(stage + StageLayout::kTptr, tptr, n0, n1 + 1, 8, bar, tx);
+  (void)dptr_t;  // same parity as dptr: sptr and tptr are both 16-B aligned allocations
+  in.dsn = stage_copy(stage + StageLayout::kSnbr, snbr, Ps0, Ps1, 4, bar, tx);
+  in.dtl = stage_copy(stage + StageLayout::kTl, tlist, Pt0, Pt1, 8, bar, tx);
+  in.dval = stage_copy(stage + StageLayout::kVals, vals, 9 * Ps0, 9 * Ps1, 8, bar, tx);
+  *info = in;
 }
 
 // q = K p on own rows (+ partial p.q, reduced by the last CTA into alpha).
 template <bool kPcg>
-__global__ void __launch_bounds__(kThreads) k_spmv(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr,
-                                                   const double* __restrict__ vals, int64_t nloc,
-                                                   const double* __restrict__ x_full, int64_t own_off,
-                                                   double* __restrict__ y, PcgState* st, double* part) {
+__global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvChunk* __restrict__ chunks, int nchunks,
+                                                       const int64_t* __restrict__ sptr,
+                                                       const int64_t* __restrict__ tptr,
+                                                       const int32_t* __restrict__ snbr,
+                                                       const int2* __restrict__ tlist, const double* __restrict__ vals,
+                                                       const double* __restrict__ x, int64_t own_off,
+                                                       double* __restrict__ y, PcgState* st, double* part) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // the dynamic window follows the static shared memory of grid_reduce: align it by hand
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                      // [kStages]
+  StageInfo* infos = reinterpret_cast<StageInfo*>(smem + 64);              // [kStages] (32 B each)
+  unsigned char* stages = smem + 64 + 32 * kStages;                         // ring (16-B aligned stages)
   if (kPcg && ld_cg(&st->done_d) != 0.0) return;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) {
+      const int c = blockIdx.x + k * gridDim.x;
+      if (c < nchunks)
+        issue_chunk(chunks[c], sptr, tptr, snbr, tlist, vals, stages + k * StageLayout::kBytes, &bars[k], &infos[k]);
+    }
+  }
   double dot = 0.0;
-  for (int64_t il = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; il < nloc;
-       il += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    double y0, y1, y2;
-    node_rows(node_ptr, nbr, vals, x_full, il, y0, y1, y2);
-    if (lane == 0) {
-      y[3 * il] = y0;
-      y[3 * il + 1] = y1;
-      y[3 * il + 2] = y2;
-      if (kPcg) {
-        const double* xo = x_full + own_off + 3 * il;
-        dot = fma(xo[0], y0, dot);
-        dot = fma(xo[1], y1, dot);
-        dot = fma(xo[2], y2, dot);
+  int it = 0;
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int sg = it % kStages;
+    SpmvChunk nxt;
+    const int cn = c + kStages * gridDim.x;
+    if (threadIdx.x == 0 && cn < nchunks) nxt = chunks[cn];  // prefetched before the compute
+    mbar_wait(&bars[sg], (it / kStages) & 1);
+    const unsigned char* stg = stages + sg * StageLayout::kBytes;
+    const StageInfo in = infos[sg];
+    const int64_t* sp = reinterpret_cast<const int64_t*>(stg + StageLayout::kPtr) + in.dptr;
+    const int64_t* tp = reinterpret_cast<const int64_t*>(stg + StageLayout::kTptr) + in.dptr;
+    const int32_t* sn = reinterpret_cast<const int32_t*>(stg + StageLayout::kSnbr) + in.dsn;
+    const int2* tl = reinterpret_cast<const int2*>(stg + StageLayout::kTl) + in.dtl;
+    const double* sv = reinterpret_cast<const double*>(stg + StageLayout::kVals) + in.dval;
+    // 8-lane group per node: a warp works on 4 nodes at once, a lane on up to kLaneItems
+    // independent items per round (loads issued together), then a 3-level group tree.
+    const int grp = lane >> 3, gl = lane & 7;
+    for (int mb = warp * 4; mb < (FSFEM_SPMV_EXPERIMENT == 3 ? 0 : in.nn); mb += kWarps * 4) {
+      const int m = mb + grp;
+      const bool act = m < in.nn;
+      const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
+      const int ds = act ? static_cast<int>(sp[m + 1] - sp[m]) : 0;
+      const int lt = act ? static_cast<int>(tp[m]) - in.Pt0 : 0;
+      const int nit = act ? 3 * (ds + static_cast<int>(tp[m + 1] - tp[m])) : 0;
+      const int nus = 3 * ds;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int i0 = 0; i0 < nit; i0 += 8 * kLaneItems) {
+        double v0[kLaneItems], v1[kLaneItems], v2[kLaneItems], xv[kLaneItems];
+#pragma unroll
+        for (int u = 0; u < kLaneItems; ++u) {
+          const int k = i0 + gl + 8 * u;
+          v0[u] = v1[u] = v2[u] = xv[u] = 0.0;
+          if (k < nus) {
+            const int b = k / 3, cc = k - 3 * b;
+            const double* pb = sv + 9 * (ls + b) + cc;
+            v0[u] = pb[0];
+            v1[u] = pb[3];
+            v2[u] = pb[6];
+            xv[u] = __ldg(x + 3 * sn[ls + b] + cc);
+          } else if (FSFEM_SPMV_EXPERIMENT == 0 && k < nit) {
+            const int kt = k - nus;
+            const int b = kt / 3, cc = kt - 3 * b;
+            const int2 e = tl[lt + b];
+            const double* pb = vals + 9 * static_cast<int64_t>(e.x) + 3 * cc;
+            v0[u] = __ldg(pb);
+            v1[u] = __ldg(pb + 1);
+            v2[u] = __ldg(pb + 2);
+            xv[u] = __ldg(x + 3 * e.y + cc);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kLaneItems; ++u) {
+          s0 = fma(v0[u], xv[u], s0);
+          s1 = fma(v1[u], xv[u], s1);
+          s2 = fma(v2[u], xv[u], s2);
+        }
       }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (act && gl == 0) {
+        const int64_t il = in.n0 + m;
+        y[3 * il] = s0;
+        y[3 * il + 1] = s1;
+        y[3 * il + 2] = s2;
+        if (kPcg) {
+          const double* xo = x + own_off + 3 * il;
+          dot = fma(xo[0], s0, dot);
+          dot = fma(xo[1], s1, dot);
+          dot = fma(xo[2], s2, dot);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with this stage
+    if (threadIdx.x == 0 && cn < nchunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_chunk(nxt, sptr, tptr, snbr, tlist, vals, stages + sg * StageLayout::kBytes, &bars[sg], &infos[sg]);
     }
   }
   if (!kPcg) return;
@@ -218,12 +399,25 @@ __global__ void k_combine(PcgState* st, const double* __restrict__ all, int stag
 
 int pcg_grid() { return 4 * num_sms(); }
 
-void launch_spmv(const int64_t* node_ptr, const int32_t* nbr, const double* vals, int64_t nloc, const double* x_full,
-                 int64_t own_off, double* y, PcgState* st, double* part, bool pcg, cudaStream_t s) {
+int spmv_grid() { return FSFEM_SPMV_MINB * num_sms(); }
+
+void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
+                 PcgState* st, double* part, bool pcg, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    FS_CUDA(cudaFuncSetAttribute(k_spmv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem));
+    FS_CUDA(cudaFuncSetAttribute(k_spmv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem));
+    attr_set = true;
+  }
+  const int nch = static_cast<int>(pat.nchunks);
   if (pcg)
-    k_spmv<true><<<pcg_grid(), kThreads, 0, s>>>(node_ptr, nbr, vals, nloc, x_full, own_off, y, st, part);
+    k_spmv<true><<<spmv_grid(), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
+                                                            pat.snbr.get(), pat.tlist.get(), vals, x_full, own_off, y,
+                                                            st, part);
   else
-    k_spmv<false><<<pcg_grid(), kThreads, 0, s>>>(node_ptr, nbr, vals, nloc, x_full, own_off, y, st, part);
+    k_spmv<false><<<spmv_grid(), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
+                                                             pat.snbr.get(), pat.tlist.get(), vals, x_full, own_off, y,
+                                                             st, part);
   FS_LAUNCH_CHECK();
 }
 

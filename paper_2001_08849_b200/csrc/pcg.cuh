@@ -1,6 +1,7 @@
 // Device-resident PCG scalars and the scalar steps of the recurrence.
 #pragma once
 #include "common.cuh"
+#include "pattern.cuh"
 
 namespace fsfem {
 
@@ -66,8 +67,8 @@ __device__ __forceinline__ void finish_beta(PcgState* st, double rr, double rz) 
 }
 
 int pcg_grid();
-void launch_spmv(const int64_t* node_ptr, const int32_t* nbr, const double* vals, int64_t nloc, const double* x_full,
-                 int64_t own_off, double* y, PcgState* st, double* part, bool pcg, cudaStream_t s);
+void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
+                 PcgState* st, double* part, bool pcg, cudaStream_t s);
 void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,
                    double* part, cudaStream_t s);
 void launch_direction(double* p, const double* r, const double* dinv, int64_t n, PcgState* st, cudaStream_t s);

@@ -4,11 +4,15 @@
 // field.  The field of face f is nodes(t0) U nodes(t1), so the faces whose field holds i are
 // exactly the faces of the tets containing i, and
 //     nbr(i) = U_{t ni i} ( nodes(t) U { node across each interior face of t } ).
-// Every neighbour pair is a dense 3x3 block (Q13): rows 3i..3i+2 have 3*deg(i) entries each,
-// stored contiguously (row-major) at vals[9*P_i ..], P = exclusive scan of deg.
+// Every neighbour pair is a dense 3x3 block (Q13): public rows 3i..3i+2 have 3*deg(i) entries.
+// Internally only the symmetric half is stored (pattern.cuh): per own node the blocks j >= i
+// (plus halo columns j < n_lo), block-contiguous, and a list locating the transposed blocks.
 // Per own node we also keep F(i) = the ascending list of faces whose field holds i (the
-// summation order of the numeric assembly) and the slot of i inside nbr(i) (the diagonal).
+// summation order of the numeric assembly).
+#include <vector>
+
 #include "common.cuh"
+#include "pattern.cuh"
 
 namespace fsfem {
 
@@ -156,21 +160,104 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_sort_segments(const int32_t*
   }
 }
 
-// Expand the node pattern to the public CSR (row_ptr int64, col_idx int32).
-__global__ void k_expand_csr(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, int64_t nloc,
-                             int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
+// Symmetric split of every own row (pattern.cuh): count stored (j >= i or j < n_lo) and
+// transposed (n_lo <= j < i) blocks.
+__global__ void k_split_count(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, int64_t n_lo,
+                              int64_t nloc, int32_t* __restrict__ cnt_s, int32_t* __restrict__ cnt_t) {
+  for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = n_lo + il;
+    int nt = 0;
+    for (int64_t k = node_ptr[il]; k < node_ptr[il + 1]; ++k) {
+      const int32_t j = nbr[k];
+      nt += (j >= n_lo && j < i) ? 1 : 0;
+    }
+    cnt_t[il] = nt;
+    cnt_s[il] = static_cast<int32_t>(node_ptr[il + 1] - node_ptr[il]) - nt;
+  }
+}
+
+__global__ void k_split_stored(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, int64_t n_lo,
+                               int64_t nloc, const int64_t* __restrict__ sptr, int32_t* __restrict__ snbr,
+                               int32_t* __restrict__ sdiag) {
+  for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = n_lo + il;
+    int64_t o = sptr[il];
+    for (int64_t k = node_ptr[il]; k < node_ptr[il + 1]; ++k) {
+      const int32_t j = nbr[k];
+      if (j >= n_lo && j < i) continue;
+      if (j == i) sdiag[il] = static_cast<int32_t>(o - sptr[il]);
+      snbr[o++] = j;
+    }
+  }
+}
+
+// For n_lo <= j < i, locate block K_ji in row j (binary search of i in the stored list of j).
+__global__ void k_split_trans(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, int64_t n_lo,
+                              int64_t nloc, const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr,
+                              const int64_t* __restrict__ tptr, int2* __restrict__ tlist,
+                              unsigned long long* __restrict__ err) {
+  for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = static_cast<int32_t>(n_lo + il);
+    int64_t o = tptr[il];
+    for (int64_t k = node_ptr[il]; k < node_ptr[il + 1]; ++k) {
+      const int32_t j = nbr[k];
+      if (!(j >= n_lo && j < i)) continue;
+      int64_t lo = sptr[j - n_lo], hi = sptr[j - n_lo + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (snbr[mid] < i) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo >= sptr[j - n_lo + 1] || snbr[lo] != i) report_error(err, FSFEM_ERR_TOPOLOGY, i);  // asymmetric graph
+      tlist[o++] = make_int2(static_cast<int32_t>(lo), j);
+    }
+  }
+}
+
+// Expand the symmetric block storage to the public CSR (row_ptr int64, col_idx int32, vals):
+// row 3i+a lists columns 3j+c for j in nbr(i) ascending.  In nbr order a row is
+// [halo stored (j < n_lo)] [transposed (n_lo <= j < i)] [stored j >= i]; the diagonal is the
+// first non-halo stored block, so the halo count equals sdiag.
+__global__ void k_export_csr(const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr,
+                             const int64_t* __restrict__ sptr, const int32_t* __restrict__ sdiag,
+                             const int64_t* __restrict__ tptr, const int2* __restrict__ tlist,
+                             const double* __restrict__ svals, int64_t nloc, int64_t* __restrict__ row_ptr,
+                             int32_t* __restrict__ col_idx, double* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
   for (int64_t il = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; il < nloc;
        il += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t P = node_ptr[il];
     const int deg = static_cast<int>(node_ptr[il + 1] - P);
     const int m = 3 * deg;
-    if (lane < 3) row_ptr[3 * il + lane] = 9 * P + lane * m;
-    if (il == nloc - 1 && lane == 0) row_ptr[3 * nloc] = 9 * node_ptr[nloc];
-    for (int k = lane; k < m; k += 32) {
-      const int32_t col = 3 * nbr[P + k / 3] + k % 3;
+    const int h = sdiag[il];
+    const int ntr = static_cast<int>(tptr[il + 1] - tptr[il]);
+    if (row_ptr && lane < 3) row_ptr[3 * il + lane] = 9 * P + lane * m;
+    if (row_ptr && il == nloc - 1 && lane == 0) row_ptr[3 * nloc] = 9 * node_ptr[nloc];
+    for (int s = lane; s < deg; s += 32) {
+      const int32_t j = nbr[P + s];
+      if (col_idx) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) col_idx[9 * P + a * m + k] = col;
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) col_idx[9 * P + a * m + 3 * s + c] = 3 * j + c;
+      }
+      if (!vals) continue;
+      double blk[9];
+      if (s >= h && s < h + ntr) {
+        const double* src = svals + 9 * static_cast<int64_t>(tlist[tptr[il] + (s - h)].x);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) blk[3 * a + c] = src[3 * c + a];
+      } else {
+        const double* src = svals + 9 * (sptr[il] + (s < h ? s : s - ntr));
+#pragma unroll
+        for (int q = 0; q < 9; ++q) blk[q] = src[q];
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vals[9 * P + a * m + 3 * s + c] = blk[3 * a + c];
     }
   }
 }
@@ -180,9 +267,14 @@ __global__ void k_expand_csr(const int64_t* __restrict__ node_ptr, const int32_t
 // Host driver of S5 for the own node range [n_lo, n_lo + nloc).
 void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
                           const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
-                          DevBuf<unsigned char>& scratch, DevBuf<int64_t>& node_ptr, DevBuf<int32_t>& nbr,
-                          DevBuf<int64_t>& nf_ptr, DevBuf<int32_t>& nf_idx, DevBuf<int32_t>& diag_slot,
-                          unsigned long long* h_flags, int64_t* nblk_out, int64_t* nfi_out) {
+                          DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags) {
+  DevBuf<int64_t>& node_ptr = pat.node_ptr;
+  DevBuf<int32_t>& nbr = pat.nbr;
+  DevBuf<int64_t>& nf_ptr = pat.nf_ptr;
+  DevBuf<int32_t>& nf_idx = pat.nf_idx;
+  DevBuf<int32_t> diag_slot;
+  pat.n_lo = n_lo;
+  pat.nloc = nloc;
   const int sms = num_sms();
   size_t o = 0;
   auto carve = [&](size_t bytes) {
@@ -234,8 +326,8 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
   if (h_flags[0] != kNoError) return;
-  *nblk_out = tot[0];
-  *nfi_out = tot[1];
+  pat.nblk = tot[0];
+  pat.nfi = tot[1];
   nbr.ensure(tot[0]);
   nf_idx.ensure(tot[1]);
   diag_slot.ensure(nloc);
@@ -243,14 +335,65 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
                                                      nullptr, nullptr, node_ptr.get(), nf_ptr.get(), nbr.get(),
                                                      nf_idx.get(), diag_slot.get(), flags);
   FS_LAUNCH_CHECK();
+  // symmetric split (pattern.cuh): deg and nfc are free again, reuse them as counters
+  const int gt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 8LL * sms)));
+  k_split_count<<<gt, 256, 0, s>>>(node_ptr.get(), nbr.get(), n_lo, nloc, deg, nfc);
+  FS_LAUNCH_CHECK();
+  pat.sptr.ensure(nloc + 3);
+  pat.tptr.ensure(nloc + 3);
+  exclusive_scan_i32_to_i64(deg, pat.sptr.get(), nloc, s, tmp, tb);
+  exclusive_scan_i32_to_i64(nfc, pat.tptr.get(), nloc, s, tmp, tb);
+  FS_CUDA(cudaMemcpyAsync(&tot[0], pat.sptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(&tot[1], pat.tptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  pat.nsb = tot[0];
+  pat.ntb = tot[1];
+  pat.snbr.ensure(pat.nsb + 4);  // + slack for the SpMV bulk copies (pattern.cuh)
+  pat.sdiag.ensure(std::max<int64_t>(nloc, 1));
+  pat.tlist.ensure(pat.ntb + 2);
+  k_split_stored<<<gt, 256, 0, s>>>(node_ptr.get(), nbr.get(), n_lo, nloc, pat.sptr.get(), pat.snbr.get(),
+                                    pat.sdiag.get());
+  FS_LAUNCH_CHECK();
+  k_split_trans<<<gt, 256, 0, s>>>(node_ptr.get(), nbr.get(), n_lo, nloc, pat.sptr.get(), pat.snbr.get(),
+                                   pat.tptr.get(), pat.tlist.get(), flags);
+  FS_LAUNCH_CHECK();
   FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  // SpMV streaming chunks (pattern.cuh): greedy runs of <= kChunkNodes nodes whose stored and
+  // transposed block counts fit kCapBlocks.  Host side, once per pattern.
+  std::vector<int64_t> hs(nloc + 1), ht(nloc + 1);
+  FS_CUDA(cudaMemcpyAsync(hs.data(), pat.sptr.get(), sizeof(int64_t) * (nloc + 1), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(ht.data(), pat.tptr.get(), sizeof(int64_t) * (nloc + 1), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  if (h_flags[0] != kNoError) return;
+  std::vector<SpmvChunk> ch;
+  ch.reserve(nloc / kChunkNodes + 1);
+  for (int64_t n0 = 0; n0 < nloc;) {
+    int64_t n1 = n0;
+    while (n1 < nloc && n1 - n0 < kChunkNodes && hs[n1 + 1] - hs[n0] <= kCapBlocks && ht[n1 + 1] - ht[n0] <= kCapBlocks)
+      ++n1;
+    if (n1 == n0) {  // one node with more than kCapBlocks blocks
+      h_flags[0] = (static_cast<unsigned long long>(FSFEM_ERR_UNSUPPORTED) << 56) | static_cast<unsigned long long>(n_lo + n0);
+      return;
+    }
+    ch.push_back(SpmvChunk{static_cast<int32_t>(n0), static_cast<int32_t>(n1), static_cast<int32_t>(hs[n0]),
+                           static_cast<int32_t>(hs[n1]), static_cast<int32_t>(ht[n0]), static_cast<int32_t>(ht[n1]), 0,
+                           0});
+    n0 = n1;
+  }
+  pat.nchunks = static_cast<int64_t>(ch.size());
+  pat.chunks.ensure(std::max<size_t>(ch.size(), 1));
+  if (!ch.empty())
+    FS_CUDA(cudaMemcpyAsync(pat.chunks.get(), ch.data(), sizeof(SpmvChunk) * ch.size(), cudaMemcpyHostToDevice, s));
   FS_CUDA(cudaStreamSynchronize(s));
 }
 
-void expand_csr_device(const int64_t* node_ptr, const int32_t* nbr, int64_t nloc, int64_t* row_ptr, int32_t* col_idx,
+void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr, int32_t* col_idx, double* vals,
                        cudaStream_t s) {
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
-  k_expand_csr<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nloc, row_ptr, col_idx);
+  if (pat.nloc == 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(pat.nloc * 32, 256), 32LL * num_sms()));
+  k_export_csr<<<std::max(grid, 1), 256, 0, s>>>(pat.node_ptr.get(), pat.nbr.get(), pat.sptr.get(), pat.sdiag.get(),
+                                                  pat.tptr.get(), pat.tlist.get(), svals, pat.nloc, row_ptr, col_idx,
+                                                  vals);
   FS_LAUNCH_CHECK();
 }
 

@@ -15,6 +15,9 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libfsfem.so")
+# Tuning experiments may point at another build of the same sources (scripts/, never the tests).
+if os.environ.get("FSFEM_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["FSFEM_LIB"])
 
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "UNSUPPORTED", 5: "NOT_CONVERGED",
                 6: "BREAKDOWN", 7: "STATE", 8: "CUDA", 9: "NCCL", 10: "OOM"}

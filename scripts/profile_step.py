@@ -33,7 +33,11 @@ def main():
     for _ in range(1 + a.reassemble):
         fsfem_assemble_csr(g.ctx, 1.0e6, 0.3)
     fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
-    rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)
+    try:
+        rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)
+    except Exception as e:  # tuning builds that skip work break PCG: report the timings anyway
+        rep = g.report()
+        rep["status"] = str(e)[:60]
     torch.cuda.synchronize()
     print({k: rep[k] for k in ("iterations", "status", "t_numeric_ms", "t_pcg_ms", "t_spmv_ms", "spmv_launches")})
 

@@ -99,10 +99,25 @@ constexpr int kStages = FSFEM_SPMV_STAGES;
 #ifndef FSFEM_SPMV_EXPERIMENT
 #define FSFEM_SPMV_EXPERIMENT 0  // tuning only: 1 = skip the transposed half
 #endif
+#ifndef FSFEM_SPMV_MAPPING
+#define FSFEM_SPMV_MAPPING 0
+#endif
 #ifndef FSFEM_SPMV_LANE_ITEMS
 #define FSFEM_SPMV_LANE_ITEMS 6
 #endif
-constexpr int kLaneItems = FSFEM_SPMV_LANE_ITEMS;  // items per lane per round (8 lanes per node)
+[[maybe_unused]] constexpr int kLaneItems = FSFEM_SPMV_LANE_ITEMS;  // flat mapping: items per lane per round
+#ifndef FSFEM_SPMV_ITEMS_S
+#define FSFEM_SPMV_ITEMS_S 3
+#endif
+#ifndef FSFEM_SPMV_ITEMS_T
+#define FSFEM_SPMV_ITEMS_T 3
+#endif
+#ifndef FSFEM_SPMV_GROUP
+#define FSFEM_SPMV_GROUP 8
+#endif
+constexpr int kGroupLanes = FSFEM_SPMV_GROUP;  // group mapping: lanes per node
+constexpr int kItemsS = FSFEM_SPMV_ITEMS_S;  // group mapping: stored items per lane per round
+constexpr int kItemsT = FSFEM_SPMV_ITEMS_T;  // group mapping: transposed items per lane per round
 constexpr int kStreamSmem = 128 + 64 + 32 * kStages + kStages * StageLayout::kBytes;  // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -193,6 +208,22 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   unsigned char* stages = smem + 64 + 32 * kStages;                         // ring (16-B aligned stages)
   if (kPcg && ld_cg(&st->done_d) != 0.0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Chunk walk of this CTA: a contiguous range of chunks (x neighbours i+-1, i+-row reuse L1
+  // across consecutive chunks), or grid-strided (FSFEM_SPMV_CONTIG=0, tuning).
+#ifndef FSFEM_SPMV_CONTIG
+#define FSFEM_SPMV_CONTIG 0
+#endif
+  int c_first, c_end, c_step;
+  if (FSFEM_SPMV_CONTIG) {
+    const int per = (nchunks + gridDim.x - 1) / gridDim.x;
+    c_first = min(nchunks, static_cast<int>(blockIdx.x) * per);
+    c_end = min(nchunks, c_first + per);
+    c_step = 1;
+  } else {
+    c_first = blockIdx.x;
+    c_end = nchunks;
+    c_step = gridDim.x;
+  }
   if (threadIdx.x == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -200,19 +231,33 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int k = 0; k < kStages; ++k) {
-      const int c = blockIdx.x + k * gridDim.x;
-      if (c < nchunks)
+      const int c = c_first + k * c_step;
+      if (c < c_end)
         issue_chunk(chunks[c], sptr, tptr, snbr, tlist, vals, stages + k * StageLayout::kBytes, &bars[k], &infos[k]);
     }
   }
   double dot = 0.0;
   int it = 0;
-  for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+#ifndef FSFEM_SPMV_TIMING
+#define FSFEM_SPMV_TIMING 0
+#endif
+#if FSFEM_SPMV_TIMING
+  long long t_wait = 0, t_comp = 0, t_sync = 0;
+  const long long t_start = clock64();
+#endif
+  for (int c = c_first; c < c_end; c += c_step, ++it) {
     const int sg = it % kStages;
     SpmvChunk nxt;
-    const int cn = c + kStages * gridDim.x;
-    if (threadIdx.x == 0 && cn < nchunks) nxt = chunks[cn];  // prefetched before the compute
+    const int cn = c + kStages * c_step;
+    if (threadIdx.x == 0 && cn < c_end) nxt = chunks[cn];  // prefetched before the compute
+#if FSFEM_SPMV_TIMING
+    const long long t0 = clock64();
+#endif
     mbar_wait(&bars[sg], (it / kStages) & 1);
+#if FSFEM_SPMV_TIMING
+    const long long t1 = clock64();
+    t_wait += t1 - t0;
+#endif
     const unsigned char* stg = stages + sg * StageLayout::kBytes;
     const StageInfo in = infos[sg];
     const int64_t* sp = reinterpret_cast<const int64_t*>(stg + StageLayout::kPtr) + in.dptr;
@@ -220,10 +265,78 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
     const int32_t* sn = reinterpret_cast<const int32_t*>(stg + StageLayout::kSnbr) + in.dsn;
     const int2* tl = reinterpret_cast<const int2*>(stg + StageLayout::kTl) + in.dtl;
     const double* sv = reinterpret_cast<const double*>(stg + StageLayout::kVals) + in.dval;
+#if FSFEM_SPMV_MAPPING == 1
+    // Flat value mapping, 16 lanes per node (2 nodes per warp): value v = 9b + e of the node's
+    // block list (stored blocks first, then transposed); consecutive lanes read consecutive
+    // matrix values (shared memory for stored blocks, one coalesced run per transposed block),
+    // and the 3 x values of a block are shared by its 9 lanes.  e = 3r + q:
+    //   stored block:      y[r] += K_ij[r][q] x_j[q]
+    //   transposed block:  y[q] += K_ji[r][q] x_j[r]
+    const int half = lane >> 4, hl = lane & 15;
+    for (int mb = warp * 2; mb < in.nn; mb += kWarps * 2) {
+      const int m = mb + half;
+      const bool act = m < in.nn;
+      const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
+      const int ds = act ? static_cast<int>(sp[m + 1] - sp[m]) : 0;
+      const int lt = act ? static_cast<int>(tp[m]) - in.Pt0 : 0;
+      const int nvs = 9 * ds, nv = act ? 9 * (ds + static_cast<int>(tp[m + 1] - tp[m])) : 0;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      const int nvw = max(nv, __shfl_xor_sync(0xffffffffu, nv, 16));  // uniform trip count
+      for (int v0 = 0; v0 < nvw; v0 += 16 * kLaneItems) {
+        double kv[kLaneItems], xv[kLaneItems];
+        int dst[kLaneItems];
+#pragma unroll
+        for (int u = 0; u < kLaneItems; ++u) {
+          const int v = v0 + hl + 16 * u;
+          const int b = v / 9, e = v - 9 * b;
+          const int r = e / 3, q = e - 3 * r;
+          kv[u] = 0.0;
+          xv[u] = 0.0;
+          dst[u] = 0;
+          if (v < nvs) {
+            kv[u] = sv[9 * ls + v];
+            xv[u] = __ldg(x + 3 * sn[ls + b] + q);
+            dst[u] = r;
+          } else if (v < nv) {
+            const int2 ent = tl[lt + b - ds];
+            kv[u] = __ldg(vals + 9 * static_cast<int64_t>(ent.x) + e);
+            xv[u] = __ldg(x + 3 * ent.y + r);
+            dst[u] = q;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kLaneItems; ++u) {
+          const double t = kv[u] * xv[u];
+          s0 += dst[u] == 0 ? t : 0.0;
+          s1 += dst[u] == 1 ? t : 0.0;
+          s2 += dst[u] == 2 ? t : 0.0;
+        }
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (act && hl == 0) {
+        const int64_t il = in.n0 + m;
+        y[3 * il] = s0;
+        y[3 * il + 1] = s1;
+        y[3 * il + 2] = s2;
+        if (kPcg) {
+          const double* xo = x + own_off + 3 * il;
+          dot = fma(xo[0], s0, dot);
+          dot = fma(xo[1], s1, dot);
+          dot = fma(xo[2], s2, dot);
+        }
+      }
+    }
+#else
     // 8-lane group per node: a warp works on 4 nodes at once, a lane on up to kLaneItems
     // independent items per round (loads issued together), then a 3-level group tree.
-    const int grp = lane >> 3, gl = lane & 7;
-    for (int mb = warp * 4; mb < (FSFEM_SPMV_EXPERIMENT == 3 ? 0 : in.nn); mb += kWarps * 4) {
+    constexpr int G = kGroupLanes, NPW = 32 / kGroupLanes;
+    const int grp = lane / G, gl = lane % G;
+    for (int mb = warp * NPW; mb < (FSFEM_SPMV_EXPERIMENT == 3 ? 0 : in.nn); mb += kWarps * NPW) {
       const int m = mb + grp;
       const bool act = m < in.nn;
       const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
@@ -232,39 +345,60 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
       const int nit = act ? 3 * (ds + static_cast<int>(tp[m + 1] - tp[m])) : 0;
       const int nus = 3 * ds;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      for (int i0 = 0; i0 < nit; i0 += 8 * kLaneItems) {
-        double v0[kLaneItems], v1[kLaneItems], v2[kLaneItems], xv[kLaneItems];
+      // One round covers kItemsS stored and kItemsT transposed items per lane.  All global
+      // gathers of the round (x for stored items; the 3 values of K_ji and x for transposed
+      // items) are issued before anything is consumed, and the stored values are read from
+      // shared memory only afterwards, so a round costs one memory latency.
+      const int nts = nit - nus;
+      int rounds = 0;
+      while (G * kItemsS * rounds < nus || G * kItemsT * rounds < nts) ++rounds;
+#pragma unroll 1
+      for (int o = G; o < 32; o <<= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+      for (int r = 0; r < rounds; ++r) {
+        double xs[kItemsS], tv[kItemsT][3], xt[kItemsT];
 #pragma unroll
-        for (int u = 0; u < kLaneItems; ++u) {
-          const int k = i0 + gl + 8 * u;
-          v0[u] = v1[u] = v2[u] = xv[u] = 0.0;
+        for (int u = 0; u < kItemsS; ++u) {
+          const int k = G * (kItemsS * r + u) + gl;
+          xs[u] = 0.0;
           if (k < nus) {
             const int b = k / 3, cc = k - 3 * b;
-            const double* pb = sv + 9 * (ls + b) + cc;
-            v0[u] = pb[0];
-            v1[u] = pb[3];
-            v2[u] = pb[6];
-            xv[u] = __ldg(x + 3 * sn[ls + b] + cc);
-          } else if (FSFEM_SPMV_EXPERIMENT == 0 && k < nit) {
-            const int kt = k - nus;
-            const int b = kt / 3, cc = kt - 3 * b;
-            const int2 e = tl[lt + b];
-            const double* pb = vals + 9 * static_cast<int64_t>(e.x) + 3 * cc;
-            v0[u] = __ldg(pb);
-            v1[u] = __ldg(pb + 1);
-            v2[u] = __ldg(pb + 2);
-            xv[u] = __ldg(x + 3 * e.y + cc);
+            xs[u] = __ldg(x + 3 * sn[ls + b] + cc);
           }
         }
 #pragma unroll
-        for (int u = 0; u < kLaneItems; ++u) {
-          s0 = fma(v0[u], xv[u], s0);
-          s1 = fma(v1[u], xv[u], s1);
-          s2 = fma(v2[u], xv[u], s2);
+        for (int u = 0; u < kItemsT; ++u) {
+          const int k = G * (kItemsT * r + u) + gl;
+          tv[u][0] = tv[u][1] = tv[u][2] = xt[u] = 0.0;
+          if (FSFEM_SPMV_EXPERIMENT == 0 && k < nts) {
+            const int b = k / 3, cc = k - 3 * b;
+            const int2 e = tl[lt + b];
+            const double* pb = vals + 9 * static_cast<int64_t>(e.x) + 3 * cc;
+            tv[u][0] = __ldg(pb);
+            tv[u][1] = __ldg(pb + 1);
+            tv[u][2] = __ldg(pb + 2);
+            xt[u] = __ldg(x + 3 * e.y + cc);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kItemsS; ++u) {
+          const int k = G * (kItemsS * r + u) + gl;
+          if (k < nus) {
+            const int b = k / 3, cc = k - 3 * b;
+            const double* pb = sv + 9 * (ls + b) + cc;
+            s0 = fma(pb[0], xs[u], s0);
+            s1 = fma(pb[3], xs[u], s1);
+            s2 = fma(pb[6], xs[u], s2);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kItemsT; ++u) {
+          s0 = fma(tv[u][0], xt[u], s0);
+          s1 = fma(tv[u][1], xt[u], s1);
+          s2 = fma(tv[u][2], xt[u], s2);
         }
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
+      for (int o = G / 2; o > 0; o >>= 1) {
         s0 += __shfl_xor_sync(0xffffffffu, s0, o);
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
@@ -282,12 +416,25 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
         }
       }
     }
+#endif
+#if FSFEM_SPMV_TIMING
+    const long long t2 = clock64();
+    t_comp += t2 - t1;
+#endif
     __syncthreads();  // every warp is done with this stage
-    if (threadIdx.x == 0 && cn < nchunks) {
+#if FSFEM_SPMV_TIMING
+    t_sync += clock64() - t2;
+#endif
+    if (threadIdx.x == 0 && cn < c_end) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_chunk(nxt, sptr, tptr, snbr, tlist, vals, stages + sg * StageLayout::kBytes, &bars[sg], &infos[sg]);
     }
   }
+#if FSFEM_SPMV_TIMING
+  if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2))
+    printf("spmv timing blk %d warp %d: chunks %d total %lld wait %lld comp %lld sync %lld\n", blockIdx.x,
+           threadIdx.x >> 5, it, clock64() - t_start, t_wait, t_comp, t_sync);
+#endif
   if (!kPcg) return;
   const double mine[1] = {dot};
   double out[1];

@@ -71,6 +71,15 @@ typedef struct {
   int64_t spmv_launches;     /* number of SpMV launches timed in t_spmv_ms                   */
   int64_t kernel_launches;   /* kernels launched by libfsfem in this process so far (monotonic;
                                 graph replays count their kernels, early-exit ones included) */
+  /* Storage and algorithmic traffic of the assembled operator.  K is stored as
+   * its symmetric half: stored_blocks 3x3 blocks (j >= i, plus halo columns of other ranks) and
+   * transposed_blocks located through a list.                                                 */
+  int64_t stored_blocks;
+  int64_t transposed_blocks;
+  int64_t spmv_bytes;        /* minimum DRAM bytes of one SpMV launch: stored values, column ids,
+                                transposed list, row pointers, x read once, y written once       */
+  int64_t assembly_bytes;    /* minimum DRAM bytes of one numeric assembly: mesh read + stored
+                                values written                                                   */
 } fsfem_report;
 
 /* Human-readable name of a status code (static string). */
@@ -88,7 +97,10 @@ const char* fsfem_last_error(const fsfem_ctx* ctx);
 /* Multi-GPU: join an NCCL communicator of `nranks` processes, one GPU each.
  * `nccl_unique_id` is the 128-byte ncclUniqueId (host memory) created by rank 0 and
  * broadcast by the caller.  Rank r then owns the contiguous node range
- * [r*ceil(N_n/nranks), min(N_n, (r+1)*ceil(N_n/nranks))) and builds only those rows. */
+ * [r*ceil(N_n/nranks), min(N_n, (r+1)*ceil(N_n/nranks))) and builds only those rows.
+ * nccl_unique_id == NULL with nranks > 1 gives a partition-only context: faces, assembly, BCs,
+ * get_csr and spmv of rank r's rows work without any communicator (one GPU can hold every
+ * rank's context, which is how the row partition is tested); pcg_solve returns STATE. */
 fsfem_status fsfem_comm_init(fsfem_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
 /* Rank 0 helper: write a fresh 128-byte ncclUniqueId to out [host].  Needs libnccl.so.2
  * (resolved at run time).  Errors: INVALID_ARG (NULL), NCCL. */

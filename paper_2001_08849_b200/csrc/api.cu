@@ -319,9 +319,9 @@ fsfem_status fsfem_nccl_get_unique_id(void* out) {
 
 fsfem_status fsfem_comm_init(fsfem_ctx* c, const void* uid, int rank, int nranks) {
   return guarded(c, [&]() -> fsfem_status {
-    if (!uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, FSFEM_ERR_INVALID_ARG, "bad rank/nranks/id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, FSFEM_ERR_INVALID_ARG, "bad rank/nranks");
     if (c->stage != kCreated) return fail(c, FSFEM_ERR_STATE, "comm_init must precede build_faces");
-    if (nranks > 1) {
+    if (nranks > 1 && uid) {
       if (!nccl().ok) return fail(c, FSFEM_ERR_NCCL, "libnccl.so.2 not loadable");
       ncclUniqueId id;
       std::memcpy(&id, uid, sizeof(id));
@@ -415,6 +415,11 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     c->rep.t_numeric_ms = elapsed(c->ev0, c->ev1);
     c->E = E;
     c->nu = nu;
+    c->rep.stored_blocks = c->pat.nsb;
+    c->rep.transposed_blocks = c->pat.ntb;
+    c->rep.spmv_bytes = 72 * c->pat.nsb + 4 * c->pat.nsb + 8 * c->pat.ntb + 16 * (c->nloc + 1) + 24 * c->nn +
+                        24 * c->nloc;
+    c->rep.assembly_bytes = 24 * c->nn + 16 * c->nt + 72 * c->pat.nsb;
     if (row_begin) *row_begin = 3 * c->n_lo;
     if (n_rows) *n_rows = 3 * c->nloc;
     if (nnz) *nnz = 9 * c->pat.nblk;
@@ -497,6 +502,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
                              fsfem_report* rep) {
   return guarded(c, [&]() -> fsfem_status {
     if (c->stage < kBc) return fail(c, FSFEM_ERR_STATE, "apply_bc first");
+    if (c->nranks > 1 && !c->comm) return fail(c, FSFEM_ERR_STATE, "partition-only context: no communicator");
     if (!u) return fail(c, FSFEM_ERR_INVALID_ARG, "null u");
     const int64_t n = 3 * c->nloc;
     const int64_t nglob = 3 * c->nn;

@@ -34,7 +34,9 @@ class FsfemReport(ctypes.Structure):
                 ("t_faces_ms", ctypes.c_double), ("t_symbolic_ms", ctypes.c_double),
                 ("t_numeric_ms", ctypes.c_double), ("t_bc_ms", ctypes.c_double), ("t_pcg_ms", ctypes.c_double),
                 ("t_spmv_ms", ctypes.c_double), ("spmv_launches", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("stored_blocks", ctypes.c_int64),
+                ("transposed_blocks", ctypes.c_int64), ("spmv_bytes", ctypes.c_int64),
+                ("assembly_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "_pad"}
@@ -141,8 +143,9 @@ def fsfem_nccl_get_unique_id() -> bytes:
     return buf.raw
 
 
-def fsfem_comm_init(ctx, unique_id: bytes, rank: int, nranks: int) -> None:
-    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+def fsfem_comm_init(ctx, unique_id: bytes | None, rank: int, nranks: int) -> None:
+    """unique_id None: partition-only context (include/fsfem.h)."""
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128) if unique_id is not None else None
     _raise(ctx, load_library().fsfem_comm_init(ctx, buf, rank, nranks))
 
 
@@ -228,7 +231,7 @@ class FsFem:
     def __exit__(self, *a):
         self.close()
 
-    def comm_init(self, unique_id: bytes, rank: int, nranks: int):
+    def comm_init(self, unique_id: bytes | None, rank: int, nranks: int):
         fsfem_comm_init(self.ctx, unique_id, rank, nranks)
 
     def build_faces(self, xyz, tets):

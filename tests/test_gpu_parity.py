@@ -249,3 +249,43 @@ def test_cfg4_solution_properties(fs):
     tip = -u.reshape(-1, 3)[m.tip, 2].mean()
     eb = 1.0 * 10.0 ** 3 / (3 * E * (1.0 / 12.0))
     assert abs(tip - eb) <= 0.03 * eb, (tip, eb)
+
+
+# ---------------------------------------------------------------- row partition (multi-GPU layout)
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_row_partition_contexts(fs, nranks):
+    """Partition-only contexts (include/fsfem.h) hold rank r's rows on one GPU: halo blocks
+    (columns below the rank's range) are stored, the rest of the lower half is read transposed.
+    Each rank's CSR rows, SpMV rows and BC-modified rows must equal the oracle's."""
+    from paper_2001_08849_b200 import FsfemError
+    m = kuhn_beam(9, 5, 3, L=4.0, jitter=0.25, jitter_seed=4, node_perm_seed=8, tet_perm_seed=9)
+    o = Oracle(m.xyz, m.tets)
+    o.build_faces()
+    _, _, _, full_vals = o.assemble_fs(E, NU)
+    kmax = np.abs(full_vals).max()
+    x = np.random.default_rng(nranks).standard_normal(3 * m.n_nodes)
+    q_ref = o.spmv(x)
+    orp_bc, oci_bc, ova_bc, _ = o.apply_bc(m.dirichlet, m.loads, 0)
+    chunk = -(-m.n_nodes // nranks)
+    for r in range(nranks):
+        lo, hi = min(m.n_nodes, r * chunk), min(m.n_nodes, (r + 1) * chunk)
+        g = fs()
+        g.comm_init(None, r, nranks)
+        g.build_faces(m.xyz, m.tets)
+        rb, nr, nnz = g.assemble_csr(E, NU)
+        assert (rb, nr) == (3 * lo, 3 * (hi - lo))
+        c = g.get_csr()
+        _, orp, oci, ova = o.assemble_fs(E, NU, lo, hi)
+        assert np.array_equal(c.row_ptr, orp) and np.array_equal(c.col_idx, oci)
+        assert np.abs(c.vals - ova).max() <= VAL_TOL * kmax
+        q = g.spmv(x)
+        scale = kmax * np.abs(x).max()
+        assert np.abs(q[3 * lo:3 * hi] - q_ref[3 * lo:3 * hi]).max() <= 1e-11 * scale
+        g.apply_bc(m.dirichlet, m.loads.reshape(-1), 0)
+        c = g.get_csr()
+        a, b = orp_bc[3 * lo], orp_bc[3 * hi]
+        assert np.array_equal(c.col_idx, oci_bc[a:b])
+        assert np.abs(c.vals - ova_bc[a:b]).max() <= VAL_TOL * kmax
+        with pytest.raises(FsfemError) as e:
+            g.pcg_solve()
+        assert e.value.status == "STATE"

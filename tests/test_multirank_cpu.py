@@ -1,0 +1,142 @@
+"""World-size-2 (and 3) CPU run of the multi-GPU row partition over `gloo`.
+
+The library's N>1 path (api.cu: fsfem_comm_init, pcg_iteration, combine, gather_full) needs one
+GPU per rank, which this container and the round's GPU box do not have.  This test runs the same
+host-side protocol with torch.distributed/gloo between CPU processes, each rank holding only its
+rows (assembled by the oracle for its node range), and checks it against the single-process
+oracle solve:
+  * partition: rank r owns nodes [r*ceil(N/G), min(N, (r+1)*ceil(N/G))) (include/fsfem.h);
+  * BCs (MODIFY) applied on own rows with the global clamp mask (bc.cu);
+  * per iteration: all_gather of equal padded p slices (ncclAllGather in gather_full), dot
+    partials all_gathered and summed in rank order (combine), the same recurrence as pcg.cuh.
+The GPU side of the partition (halo blocks, transposed lists, per-rank CSR/SpMV/BC rows) is
+covered by tests/test_gpu_parity.py::test_row_partition_contexts.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+E, NU = 1.0e6, 0.3
+
+
+def _mesh():
+    from fsfem_inputs import kuhn_beam
+    return kuhn_beam(9, 3, 3, L=4.0, jitter=0.2, jitter_seed=11, node_perm_seed=12, tet_perm_seed=13)
+
+
+def _partition(nn, nranks, r):
+    chunk = -(-nn // nranks)
+    lo = min(nn, r * chunk)
+    return lo, min(nn, lo + chunk), chunk
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from oracle import Oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = _mesh()
+    nn = m.n_nodes
+    lo, hi, chunk = _partition(nn, world, rank)
+    o = Oracle(m.xyz, m.tets)
+    o.build_faces()
+    _, rp, ci, va = o.assemble_fs(E, NU, lo, hi)  # own rows, global columns
+    va = va.copy()
+    fixed = np.zeros(nn, bool)
+    fixed[m.dirichlet] = True
+    nrow = 3 * (hi - lo)
+    diag = np.zeros(nrow)
+    for k in range(nrow):
+        r = 3 * lo + k
+        for e in range(rp[k], rp[k + 1]):
+            c = ci[e]
+            if (fixed[r // 3] or fixed[c // 3]) and c != r:
+                va[e] = 0.0
+            if c == r:
+                diag[k] = va[e]
+    f = m.loads.reshape(-1)[3 * lo:3 * hi].copy()
+    f[np.repeat(fixed[lo:hi], 3)] = 0.0
+    dinv = 1.0 / diag
+
+    def spmv(p_full):
+        q = np.zeros(nrow)
+        for k in range(nrow):
+            s = 0.0
+            for e in range(rp[k], rp[k + 1]):
+                s += va[e] * p_full[ci[e]]
+            q[k] = s
+        return q
+
+    def gather_full(v_own):
+        buf = torch.zeros(3 * chunk, dtype=torch.float64)
+        buf[:nrow] = torch.from_numpy(v_own)
+        parts = [torch.zeros(3 * chunk, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, buf)
+        return torch.cat(parts).numpy()[:3 * nn]
+
+    def combine(*vals):
+        mine = torch.tensor(vals, dtype=torch.float64)
+        parts = [torch.zeros(len(vals), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        tot = np.zeros(len(vals))
+        for p in parts:  # rank order
+            tot += p.numpy()
+        return tot
+
+    x = np.zeros(nrow)
+    r = f.copy()
+    z = dinv * r
+    p = z.copy()
+    rho, rr, ff = combine(r @ z, r @ r, f @ f)
+    it = 0
+    tol = 1e-10
+    while np.sqrt(rr) > tol * np.sqrt(ff) and it < 5000:
+        q = spmv(gather_full(p))
+        (pq,) = combine(p @ q)
+        alpha = rho / pq
+        x += alpha * p
+        r -= alpha * q
+        z = dinv * r
+        rr, rz = combine(r @ r, r @ z)
+        it += 1
+        if np.sqrt(rr) <= tol * np.sqrt(ff):
+            break
+        beta = rz / rho
+        rho = rz
+        p = z + beta * p
+    u = gather_full(x)
+    np.save(os.path.join(out_dir, f"u{rank}.npy"), u)
+    np.save(os.path.join(out_dir, f"it{rank}.npy"), np.array([it]))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partition_pcg_over_gloo(tmp_path, world):
+    import torch.multiprocessing as mp
+    from oracle import Oracle
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    m = _mesh()
+    o = Oracle(m.xyz, m.tets)
+    o.build_faces()
+    o.assemble_fs(E, NU)
+    o.apply_bc(m.dirichlet, m.loads, 0)
+    u_ref, rep = o.pcg(1e-10)
+    us = [np.load(tmp_path / f"u{r}.npy") for r in range(world)]
+    its = [int(np.load(tmp_path / f"it{r}.npy")[0]) for r in range(world)]
+    for u in us[1:]:
+        assert np.array_equal(u, us[0])  # every rank ends with the same full solution
+    assert len(set(its)) == 1
+    assert np.linalg.norm(us[0] - u_ref) <= 1e-7 * np.linalg.norm(u_ref)
+    assert abs(its[0] - rep["iterations"]) <= max(3, 0.05 * rep["iterations"])
+    fixed = np.repeat(np.isin(np.arange(m.n_nodes), m.dirichlet), 3)
+    assert np.all(us[0][fixed] == 0.0)

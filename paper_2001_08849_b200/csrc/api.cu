@@ -30,7 +30,8 @@ void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_n
                    const int32_t* face_opp, int64_t nf, double* face_s, cudaStream_t s);
 void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
                           const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
-                          int64_t nloc, double lam, double mu, double* vals, cudaStream_t s);
+                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks,
+                          cudaStream_t s);
 void apply_bc_device(const int64_t* node_ptr, const int32_t* nbr, const int32_t* diag_slot, int64_t n_lo, int64_t nloc,
                      int64_t nn, const int32_t* dir, int64_t nd, const double* loads, int mode, double penalty_scale,
                      double* vals, double* f, double* dinv, uint8_t* fixed, unsigned long long* flags, cudaStream_t s);
@@ -409,7 +410,8 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
                   c->face_s.get(), c->stream);
     assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->face_nodes.get(),
-                         c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(), c->stream);
+                         c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(),
+                         c->pat.max_row_blocks, c->stream);
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     FS_CUDA(cudaEventSynchronize(c->ev1));
     c->rep.t_numeric_ms = elapsed(c->ev0, c->ev1);

@@ -32,10 +32,15 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
                                                 const int32_t* __restrict__ face_tet,
                                                 const int32_t* __restrict__ face_opp, int64_t nf,
                                                 double* __restrict__ face_s) {
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
-    int32_t fld[5] = {face_nodes[3 * f], face_nodes[3 * f + 1], face_nodes[3 * f + 2], face_opp[2 * f],
-                      face_opp[2 * f + 1]};
-    const int32_t tt[2] = {face_tet[2 * f], face_tet[2 * f + 1]};
+  __shared__ __align__(16) double stage[256 * kFaceStride];
+  // uniform trip count per block (every thread reaches the __syncthreads)
+  for (int64_t fb0 = blockIdx.x * (int64_t)blockDim.x; fb0 < nf; fb0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = fb0 + threadIdx.x;
+    const bool valid = f < nf;
+    const int64_t fc = valid ? f : fb0;  // inactive threads recompute face fb0 and write nothing extra
+    int32_t fld[5] = {face_nodes[3 * fc], face_nodes[3 * fc + 1], face_nodes[3 * fc + 2], face_opp[2 * fc],
+                      face_opp[2 * fc + 1]};
+    const int32_t tt[2] = {face_tet[2 * fc], face_tet[2 * fc + 1]};
     double g[5][3];
 #pragma unroll
     for (int K = 0; K < 5; ++K) g[K][0] = g[K][1] = g[K][2] = 0.0;
@@ -89,30 +94,41 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
       }
     }
     const double rs = 1.0 / sqrt(Vf);
-    double* out = face_s + kFaceStride * f;
+    // stage the 16 doubles of each face of the block in shared memory, then store coalesced
+    double* st = stage + kFaceStride * threadIdx.x;
 #pragma unroll
     for (int K = 0; K < 5; ++K) {
-      out[3 * K] = g[K][0] * rs;
-      out[3 * K + 1] = g[K][1] * rs;
-      out[3 * K + 2] = g[K][2] * rs;
+      st[3 * K] = g[K][0] * rs;
+      st[3 * K + 1] = g[K][1] * rs;
+      st[3 * K + 2] = g[K][2] * rs;
     }
-    out[15] = Vf;
+    st[15] = Vf;
+    __syncthreads();
+    const int64_t fb = f - threadIdx.x;  // first face of this block-iteration
+    const int nvalid = static_cast<int>(nf - fb < (int64_t)blockDim.x ? nf - fb : (int64_t)blockDim.x);
+    double2* dst = reinterpret_cast<double2*>(face_s + kFaceStride * fb);
+    const double2* src = reinterpret_cast<const double2*>(stage);
+    for (int k = threadIdx.x; k < nvalid * (kFaceStride / 2); k += blockDim.x) __stcs(dst + k, src[k]);
+    __syncthreads();
   }
 }
 
-// Warp per own node i; lane = stored block slot (j >= i, or halo j < n_lo; pattern.cuh), in
-// chunks of 32.  For every face of F(i) in ascending order, lanes whose neighbour j is in the
-// face's field add s_i s_j^T.
+// Generic path (rows with more than 32 stored blocks; none in the Kuhn beams): warp per own
+// node i; lane = stored block slot (j >= i, or halo j < n_lo; pattern.cuh), in chunks of 32.
+// For every face of F(i) in ascending order, lanes whose neighbour j is in the face's field add
+// s_i s_j^T.
 __global__ void __launch_bounds__(256) k_assemble_rows(
     const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, const int64_t* __restrict__ nf_ptr,
     const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
-    const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals) {
+    const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals,
+    int min_deg) {
   const int lane = threadIdx.x & 31;
   for (int64_t il = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; il < nloc;
        il += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int32_t self = static_cast<int32_t>(n_lo + il);
     const int64_t P = node_ptr[il];
     const int deg = static_cast<int>(node_ptr[il + 1] - P);
+    if (deg <= min_deg) continue;  // handled by k_assemble_rows2
     const int64_t f0 = nf_ptr[il], f1 = nf_ptr[il + 1];
     double* blocks = vals + 9 * P;
     for (int s0 = 0; s0 < deg; s0 += 32) {
@@ -161,6 +177,131 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
   }
 }
 
+
+// Fast path, warp per own node i with <= 32 stored blocks (diagonal + j > i + halo j < n_lo).
+// Rounds of 32 faces of F(i) (ascending):
+//   A. lane = face: load the face's field nodes and s vectors (all lanes' loads in flight at
+//      once), add s_i s_i^T to the lane's diagonal partial sum, and for every other field node
+//      that is a stored column of row i record (slot, s_K) and set the face's bit in the slot's
+//      mask (order-independent OR);
+//   B. lane = stored slot: walk the mask bits in ascending face order and add s_i s_K^T.
+// Summation order: off-diagonal blocks in ascending face id (as the generic path); the
+// diagonal block as per-lane sums over faces lane, lane+32, ... then a fixed warp tree.
+constexpr int kRowWarps = 4;
+constexpr int kMaxTargets = 4;  // other field nodes of a face
+
+__global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
+    const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
+    const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
+    const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals) {
+  __shared__ int32_t sh_cols[kRowWarps][32];
+  __shared__ unsigned sh_mask[kRowWarps][32];
+  __shared__ double sh_si[kRowWarps][32][3];
+  __shared__ double sh_sk[kRowWarps][32][kMaxTargets][3];
+  __shared__ int8_t sh_tslot[kRowWarps][32][kMaxTargets];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t il = blockIdx.x * (int64_t)kRowWarps + w; il < nloc; il += (int64_t)gridDim.x * kRowWarps) {
+    const int32_t self = static_cast<int32_t>(n_lo + il);
+    const int64_t P = sptr[il];
+    const int ds = static_cast<int>(sptr[il + 1] - P);
+    if (ds > 32) continue;  // generic path
+    sh_cols[w][lane] = lane < ds ? snbr[P + lane] : 0x7fffffff;
+    sh_mask[w][lane] = 0u;
+    const int64_t f0 = nf_ptr[il];
+    const int nfc = static_cast<int>(nf_ptr[il + 1] - f0);
+    double d[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // diagonal partial: xx yy zz xy xz yz
+    double M[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) M[q] = 0.0;
+    __syncwarp();
+    for (int rb = 0; rb < nfc; rb += 32) {
+      // ---- A: lane = face
+      if (rb + lane < nfc) {
+        const int32_t f = nf_idx[f0 + rb + lane];
+        const int32_t fld[5] = {face_nodes[3 * f], face_nodes[3 * f + 1], face_nodes[3 * f + 2], face_opp[2 * f],
+                                face_opp[2 * f + 1]};
+        const double* sf = face_s + kFaceStride * static_cast<int64_t>(f);
+        int pi = 0;
+#pragma unroll
+        for (int K = 0; K < 5; ++K) pi = (fld[K] == self) ? K : pi;
+        const double s0 = sf[3 * pi], s1 = sf[3 * pi + 1], s2 = sf[3 * pi + 2];
+        sh_si[w][lane][0] = s0;
+        sh_si[w][lane][1] = s1;
+        sh_si[w][lane][2] = s2;
+        d[0] = fma(s0, s0, d[0]);
+        d[1] = fma(s1, s1, d[1]);
+        d[2] = fma(s2, s2, d[2]);
+        d[3] = fma(s0, s1, d[3]);
+        d[4] = fma(s0, s2, d[4]);
+        d[5] = fma(s1, s2, d[5]);
+        int t = 0;
+#pragma unroll
+        for (int K = 0; K < 5; ++K) {
+          const int32_t v = fld[K];
+          if (K == pi || v < 0 || (v < self && v >= n_lo)) continue;
+          // binary search of v in the stored columns (ascending, padded with INT_MAX)
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1)
+            if (sh_cols[w][lo + step - 1] < v) lo += step;
+          sh_tslot[w][lane][t] = static_cast<int8_t>(lo);
+          sh_sk[w][lane][t][0] = sf[3 * K];
+          sh_sk[w][lane][t][1] = sf[3 * K + 1];
+          sh_sk[w][lane][t][2] = sf[3 * K + 2];
+          atomicOr(&sh_mask[w][lo], 1u << lane);
+          ++t;
+        }
+        for (; t < kMaxTargets; ++t) sh_tslot[w][lane][t] = -1;
+      }
+      __syncwarp();
+      // ---- B: lane = stored slot
+      unsigned m = sh_mask[w][lane];
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        int t = 0;
+#pragma unroll
+        for (int q = 1; q < kMaxTargets; ++q) t = (sh_tslot[w][b][q] == lane) ? q : t;
+        const double a0 = sh_si[w][b][0], a1 = sh_si[w][b][1], a2 = sh_si[w][b][2];
+        const double c0 = sh_sk[w][b][t][0], c1 = sh_sk[w][b][t][1], c2 = sh_sk[w][b][t][2];
+        M[0] = fma(a0, c0, M[0]);
+        M[1] = fma(a0, c1, M[1]);
+        M[2] = fma(a0, c2, M[2]);
+        M[3] = fma(a1, c0, M[3]);
+        M[4] = fma(a1, c1, M[4]);
+        M[5] = fma(a1, c2, M[5]);
+        M[6] = fma(a2, c0, M[6]);
+        M[7] = fma(a2, c1, M[7]);
+        M[8] = fma(a2, c2, M[8]);
+      }
+      __syncwarp();
+      sh_mask[w][lane] = 0u;
+      __syncwarp();
+    }
+    // diagonal block: fixed warp tree of the per-lane partial sums
+#pragma unroll
+    for (int q = 0; q < 6; ++q) d[q] = warp_sum(d[q]);
+    double* blocks = vals + 9 * P;
+    const int32_t my_col = sh_cols[w][lane];
+    if (lane < ds && my_col == self) {
+      const double Md[9] = {d[0], d[3], d[4], d[3], d[1], d[5], d[4], d[5], d[2]};
+#pragma unroll
+      for (int q = 0; q < 9; ++q) M[q] = Md[q];
+    }
+    if (lane < ds) {
+      const double tr = M[0] + M[4] + M[8];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double v = fma(lam, M[3 * a + c], mu * M[3 * c + a]);
+          if (a == c) v = fma(mu, tr, v);
+          blocks[9 * lane + 3 * a + c] = v;
+        }
+    }
+    __syncwarp();
+  }
+}
 }  // namespace
 
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
@@ -172,11 +313,18 @@ void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_n
 
 void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
                           const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
-                          int64_t nloc, double lam, double mu, double* vals, cudaStream_t s) {
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
-  k_assemble_rows<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo,
-                                                    nloc, lam, mu, vals);
+                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, cudaStream_t s) {
+  if (nloc == 0) return;
+  const int g2 = static_cast<int>(std::min<int64_t>(ceil_div(nloc, kRowWarps), 64LL * num_sms()));
+  k_assemble_rows2<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp,
+                                                               face_s, n_lo, nloc, lam, mu, vals);
   FS_LAUNCH_CHECK();
+  if (max_row_blocks > 32) {
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
+    k_assemble_rows<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo,
+                                                      nloc, lam, mu, vals, 32);
+    FS_LAUNCH_CHECK();
+  }
 }
 
 }  // namespace fsfem

@@ -32,6 +32,7 @@ struct Pattern {
   int64_t nsb = 0;   // stored blocks
   int64_t ntb = 0;   // transposed (gathered) blocks
   int64_t nfi = 0;   // node-face incidences (sum over own nodes of |F(i)|)
+  int64_t max_row_blocks = 0;  // max stored blocks of one row
   DevBuf<int64_t> node_ptr;  // [nloc+1] full neighbour list offsets
   DevBuf<int32_t> nbr;       // [nblk] sorted neighbour node ids of every own node
   DevBuf<int64_t> sptr;      // [nloc+1] stored block offsets

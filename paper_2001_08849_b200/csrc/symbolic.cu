@@ -365,6 +365,8 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   FS_CUDA(cudaMemcpyAsync(ht.data(), pat.tptr.get(), sizeof(int64_t) * (nloc + 1), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
   if (h_flags[0] != kNoError) return;
+  pat.max_row_blocks = 0;
+  for (int64_t i = 0; i < nloc; ++i) pat.max_row_blocks = std::max<int64_t>(pat.max_row_blocks, hs[i + 1] - hs[i]);
   std::vector<SpmvChunk> ch;
   ch.reserve(nloc / kChunkNodes + 1);
   for (int64_t n0 = 0; n0 < nloc;) {

@@ -297,7 +297,9 @@ def run_gpu(args):
     roof = {"kernel": "k_spmv<true> (PCG SpMV + p.q)", "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(args.config),
             "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms, "launches_timed": spmv_n,
-            "peak_kind": peak_kind, "share_of_step": spmv_ms / args.steps / (ms / args.steps),
+            "peak_kind": peak_kind, "launches_per_step": iters + 1,
+            "share_of_step": spmv_avg_ms * (iters + 1) / (ms / args.steps),
+            "timing": "CUDA events around the first SpMV of every 32-iteration CUDA-graph batch, live in the timed steps",
             "full_csr_equivalent_bytes": 12 * nnz + 32 * 3 * m.n_nodes}
     asm_bytes = int(last["assembly_bytes"])
     line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": args.steps,

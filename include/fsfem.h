@@ -67,8 +67,9 @@ typedef struct {
   double t_numeric_ms;       /* ... of the last numeric assembly (S2-S4, S6)                 */
   double t_bc_ms;            /* ... of the last apply_bc (S7)                                */
   double t_pcg_ms;           /* ... of the last pcg_solve loop (S8-S9)                       */
-  double t_spmv_ms;          /* summed device time of the SpMV launches of that loop         */
-  int64_t spmv_launches;     /* number of SpMV launches timed in t_spmv_ms                   */
+  double t_spmv_ms;          /* summed device time of the sampled SpMV launches of that loop
+                                (the first SpMV of every CUDA-graph batch of iterations)      */
+  int64_t spmv_launches;     /* number of SpMV launches sampled in t_spmv_ms                 */
   int64_t kernel_launches;   /* kernels launched by libfsfem in this process so far (monotonic;
                                 graph replays count their kernels, early-exit ones included) */
   /* Storage and algorithmic traffic of the assembled operator.  K is stored as

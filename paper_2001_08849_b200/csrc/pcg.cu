@@ -19,6 +19,20 @@ constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+// One thread per CTA reads the device-resident PCG scalars (every thread reading the same
+// address through L2 would serialise on one L2 slice); the CTA gets them from shared memory.
+__device__ __forceinline__ bool cta_scalars(const PcgState* st, const double* field, double& value) {
+  __shared__ double sh_s[2];
+  if (threadIdx.x == 0) {
+    sh_s[0] = ld_cg(&st->done_d);
+    sh_s[1] = field ? ld_cg(field) : 0.0;
+  }
+  __syncthreads();
+  value = sh_s[1];
+  const bool done = sh_s[0] != 0.0;
+  return done;
+}
+
 // Deterministic CTA sum of one double per thread (result valid in thread 0).
 __device__ __forceinline__ double block_sum(double v, double* sh /*[kWarps]*/) {
   v = warp_sum(v);
@@ -206,7 +220,10 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                      // [kStages]
   StageInfo* infos = reinterpret_cast<StageInfo*>(smem + 64);              // [kStages] (32 B each)
   unsigned char* stages = smem + 64 + 32 * kStages;                         // ring (16-B aligned stages)
-  if (kPcg && ld_cg(&st->done_d) != 0.0) return;
+  if (kPcg) {
+    double unused;
+    if (cta_scalars(st, nullptr, unused)) return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // Chunk walk of this CTA: a contiguous range of chunks (x neighbours i+-1, i+-row reuse L1
   // across consecutive chunks), or grid-strided (FSFEM_SPMV_CONTIG=0, tuning).
@@ -447,20 +464,44 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   }
 }
 
+// Vector kernels: each thread takes kVec elements per pass at stride gridDim*blockDim (coalesced)
+// and issues all their loads before any arithmetic, so that enough bytes are in flight to
+// stream HBM.  Per-thread partial sums run in element order: the result depends only on the
+// (fixed) launch shape.
+constexpr int kVec = 4;
+
 // x += alpha p; r -= alpha q; partial r.r and r.z with z = dinv r.
 __global__ void __launch_bounds__(kThreads) k_update(double* __restrict__ x, double* __restrict__ r,
                                                      const double* __restrict__ p, const double* __restrict__ q,
                                                      const double* __restrict__ dinv, int64_t n, PcgState* st,
                                                      double* part) {
-  if (ld_cg(&st->done_d) != 0.0) return;
-  const double alpha = ld_cg(&st->alpha);
+  double alpha;
+  if (cta_scalars(st, &st->alpha, alpha)) return;
   double rr = 0.0, rz = 0.0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    x[k] = fma(alpha, p[k], x[k]);
-    const double rk = fma(-alpha, q[k], r[k]);
-    r[k] = rk;
-    rr = fma(rk, rk, rr);
-    rz = fma(rk, dinv[k] * rk, rz);
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+    double xv[kVec], rv[kVec], pv[kVec], qv[kVec], dv[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      const bool ok = k < n;
+      xv[j] = ok ? x[k] : 0.0;
+      rv[j] = ok ? r[k] : 0.0;
+      pv[j] = ok ? p[k] : 0.0;
+      qv[j] = ok ? q[k] : 0.0;
+      dv[j] = ok ? dinv[k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      if (k < n) {
+        x[k] = fma(alpha, pv[j], xv[j]);
+        const double rk = fma(-alpha, qv[j], rv[j]);
+        r[k] = rk;
+        rr = fma(rk, rk, rr);
+        rz = fma(rk, dv[j] * rk, rz);
+      }
+    }
   }
   const double mine[2] = {rr, rz};
   double out[2];
@@ -477,10 +518,130 @@ __global__ void __launch_bounds__(kThreads) k_update(double* __restrict__ x, dou
 // p = dinv r + beta p
 __global__ void __launch_bounds__(kThreads) k_direction(double* __restrict__ p, const double* __restrict__ r,
                                                         const double* __restrict__ dinv, int64_t n, PcgState* st) {
-  if (ld_cg(&st->done_d) != 0.0) return;
-  const double beta = ld_cg(&st->beta);
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-    p[k] = fma(beta, p[k], dinv[k] * r[k]);
+  double beta;
+  if (cta_scalars(st, &st->beta, beta)) return;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+    double pv[kVec], rv[kVec], dv[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      const bool ok = k < n;
+      pv[j] = ok ? p[k] : 0.0;
+      rv[j] = ok ? r[k] : 0.0;
+      dv[j] = ok ? dinv[k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      if (k < n) p[k] = fma(beta, pv[j], dv[j] * rv[j]);
+    }
+  }
+}
+
+// Single-rank fused update + direction (cooperative launch: all CTAs are co-resident).
+//   phase 1: r -= alpha q, per-CTA partials of r.r and r.z (z = dinv r);
+//   grid barrier;
+//   every CTA sums the partials in the same fixed order (so all agree on beta bit for bit);
+//   CTA 0 records the scalars (finish_beta);
+//   phase 2: x += alpha p_old; p = dinv r + beta p_old (r and dinv are L2-warm from phase 1).
+// Same arithmetic as k_update + k_direction, one launch and one DRAM pass less over r and dinv.
+__device__ __forceinline__ void grid_barrier(PcgState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = *reinterpret_cast<volatile unsigned*>(&st->bar_gen);
+    __threadfence();
+    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
+      st->bar_count = 0u;
+      __threadfence();
+      atomicExch(&st->bar_gen, gen + 1u);
+    } else {
+      while (*reinterpret_cast<volatile unsigned*>(&st->bar_gen) == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) k_update_direction(double* __restrict__ x, double* __restrict__ r,
+                                                               double* __restrict__ p, const double* __restrict__ q,
+                                                               const double* __restrict__ dinv, int64_t n,
+                                                               PcgState* st, double* part) {
+  __shared__ double sh[kWarps];
+  __shared__ double sh_sc[4];
+  if (threadIdx.x == 0) {
+    sh_sc[0] = ld_cg(&st->done_d);
+    sh_sc[1] = ld_cg(&st->alpha);
+    sh_sc[2] = ld_cg(&st->rho);
+    sh_sc[3] = ld_cg(&st->ff);
+  }
+  __syncthreads();
+  if (sh_sc[0] != 0.0) return;  // uniform over the grid: done_d is only written between launches
+  const double alpha = sh_sc[1], rho_old = sh_sc[2];
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double rr = 0.0, rz = 0.0;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+    double rv[kVec], qv[kVec], dv[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      const bool ok = k < n;
+      rv[j] = ok ? r[k] : 0.0;
+      qv[j] = ok ? q[k] : 0.0;
+      dv[j] = ok ? dinv[k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      if (k < n) {
+        const double rk = fma(-alpha, qv[j], rv[j]);
+        r[k] = rk;
+        rr = fma(rk, rk, rr);
+        rz = fma(rk, dv[j] * rk, rz);
+      }
+    }
+  }
+  const double trr = block_sum(rr, sh), trz = block_sum(rz, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = trr;
+    part[gridDim.x + blockIdx.x] = trz;
+  }
+  grid_barrier(st);
+  // every CTA: the same fixed-order sums of the partials
+  double a = 0.0, c = 0.0;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += kThreads) {
+    a += ld_cg(part + k);
+    c += ld_cg(part + gridDim.x + k);
+  }
+  const double RR = block_sum(a, sh), RZ = block_sum(c, sh);
+  __shared__ double sh_beta;
+  if (threadIdx.x == 0) {
+    sh_beta = RZ / rho_old;
+    if (blockIdx.x == 0) finish_beta(st, RR, RZ);  // same beta; also sets done / iteration count
+  }
+  __syncthreads();
+  const double beta = sh_beta;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+    double xv[kVec], pv[kVec], rv[kVec], dv[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      const bool ok = k < n;
+      xv[j] = ok ? x[k] : 0.0;
+      pv[j] = ok ? p[k] : 0.0;
+      rv[j] = ok ? r[k] : 0.0;
+      dv[j] = ok ? dinv[k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      if (k < n) {
+        x[k] = fma(alpha, pv[j], xv[j]);
+        p[k] = fma(beta, pv[j], dv[j] * rv[j]);
+      }
+    }
+  }
 }
 
 // r = f - q (q = K x0, or q == nullptr for x0 = 0); z = dinv r; p = z; partial r.z, r.r, f.f.
@@ -577,6 +738,32 @@ void launch_update(double* x, double* r, const double* p, const double* q, const
 void launch_direction(double* p, const double* r, const double* dinv, int64_t n, PcgState* st, cudaStream_t s) {
   k_direction<<<pcg_grid(), kThreads, 0, s>>>(p, r, dinv, n, st);
   FS_LAUNCH_CHECK();
+}
+
+int update_direction_grid() {
+  static int g = 0;
+  if (g == 0) {
+    int per_sm = 0;
+    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_direction, kThreads, 0));
+    g = std::max(1, std::min(4, per_sm)) * num_sms();
+  }
+  return g;
+}
+
+void launch_update_direction(double* x, double* r, double* p, const double* q, const double* dinv, int64_t n,
+                             PcgState* st, double* part, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(update_direction_grid());
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FS_CUDA(cudaLaunchKernelEx(&cfg, k_update_direction, x, r, p, q, dinv, n, st, part));
+  count_launch();
 }
 
 void launch_init(const double* f, const double* q, const double* dinv, double* r, double* p, int64_t n, PcgState* st,

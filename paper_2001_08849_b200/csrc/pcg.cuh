@@ -19,6 +19,7 @@ struct PcgState {
   int status;       // FSFEM_OK, FSFEM_ERR_NOT_CONVERGED or FSFEM_ERR_BREAKDOWN
   int nranks;
   unsigned int ticket[4];
+  unsigned int bar_count, bar_gen;  // grid barrier of the fused update/direction kernel
 };
 
 __device__ __forceinline__ void pcg_stop(PcgState* st, int status) {
@@ -72,6 +73,9 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
 void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,
                    double* part, cudaStream_t s);
 void launch_direction(double* p, const double* r, const double* dinv, int64_t n, PcgState* st, cudaStream_t s);
+// Single-rank: x += alpha p; r -= alpha q; beta; p = dinv r + beta p in one cooperative kernel.
+void launch_update_direction(double* x, double* r, double* p, const double* q, const double* dinv, int64_t n,
+                             PcgState* st, double* part, cudaStream_t s);
 void launch_init(const double* f, const double* q, const double* dinv, double* r, double* p, int64_t n, PcgState* st,
                  double* part, cudaStream_t s);
 void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s);

@@ -289,3 +289,68 @@ def test_row_partition_contexts(fs, nranks):
         with pytest.raises(FsfemError) as e:
             g.pcg_solve()
         assert e.value.status == "STATE"
+
+
+# ---------------------------------------------------------------- full-size displacements vs the oracle
+def _gpu_solve(fs, m):
+    g = fs()
+    g.build_faces(m.xyz, m.tets)
+    g.assemble_csr(E, NU)
+    g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+    u, rep = g.pcg_solve(rel_tol=1e-10)
+    return g, u, rep
+
+
+def _golden(cfg):
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"oracle_cfg{cfg}.json")))
+
+
+def test_cfg3_displacements_match_oracle(fs):
+    """cfg3 (jittered, 134k dofs): the whole u against the oracle's full solve
+    (tests/golden/oracle_cfg3_u.npy, written by scripts/oracle_full_solve.py from oracle/ only)."""
+    import os
+    m = config_mesh(3)
+    g, u, rep = _gpu_solve(fs, m)
+    uo = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_cfg3_u.npy"))
+    gold = _golden(3)
+    assert rep["converged"] == 1 and rep["rel_residual"] <= 1e-10
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
+    f = m.loads.reshape(-1)
+    assert abs(f @ u - gold["f_dot_u"]) <= 1e-8 * abs(gold["f_dot_u"])
+    assert abs(rep["iterations"] - gold["pcg"]["iterations"]) <= 0.05 * gold["pcg"]["iterations"]
+
+
+def test_cfg4_displacements_match_oracle(fs):
+    """cfg4 (bench workload): compliance, tip deflection and 4096 sampled dofs against the
+    oracle's full solve (tests/golden/oracle_cfg4.json)."""
+    m = config_mesh(4)
+    g, u, rep = _gpu_solve(fs, m)
+    gold = _golden(4)
+    assert rep["converged"] == 1
+    f = m.loads.reshape(-1)
+    assert abs(f @ u - gold["f_dot_u"]) <= 1e-8 * abs(gold["f_dot_u"])
+    tip = u.reshape(-1, 3)[m.tip, 2].mean()
+    assert abs(tip - gold["tip_mean_uz"]) <= 1e-7 * abs(gold["tip_mean_uz"])
+    idx = np.asarray(gold["u_sample_idx"])
+    assert np.abs(u[idx] - np.asarray(gold["u_sample"])).max() <= U_TOL * gold["u_norm"]
+    assert abs(np.linalg.norm(u) - gold["u_norm"]) <= U_TOL * gold["u_norm"]
+
+
+def test_cfg5_solution_properties(fs):
+    """cfg5 (9.8M tets, jittered, randomly relabelled; no full oracle solve exists -- SURVEY R4):
+    convergence, true residual, energy identity and the beam deflection between the
+    Euler-Bernoulli value and the Timoshenko one (+3%)."""
+    m = config_mesh(5)
+    g, u, rep = _gpu_solve(fs, m)
+    assert rep["converged"] == 1 and rep["rel_residual"] <= 1e-10
+    assert rep["true_rel_residual"] < 1e-6
+    f = m.loads.reshape(-1)
+    Ku = g.spmv(u)
+    assert np.isclose(u @ Ku, f @ u, rtol=1e-8)
+    tip = -u.reshape(-1, 3)[m.tip, 2].mean()
+    eb = 1.0 * 10.0 ** 3 / (3 * E * (1.0 / 12.0))
+    assert 0.97 * eb <= tip <= 1.03 * 4.031e-3, (tip, eb)
+    fixed = np.repeat(np.isin(np.arange(m.n_nodes), m.dirichlet), 3)
+    assert np.all(u[fixed] == 0.0)

@@ -107,6 +107,14 @@ fsfem_status fsfem_comm_init(fsfem_ctx* ctx, const void* nccl_unique_id, int ran
  * (resolved at run time).  Errors: INVALID_ARG (NULL), NCCL. */
 fsfem_status fsfem_nccl_get_unique_id(void* out);
 
+/* Discretisation of the stiffness (default FSFEM_METHOD_FS).  FSFEM_METHOD_FEM_T4 assembles the
+ * conventional linear-tet stiffness K_e = V_e B^T c B over the tet node graph instead (the paper's
+ * comparison column, PAPER.md:531 and Table 4 at 598-607); faces, BCs, SpMV
+ * and PCG are shared.  Changing the method drops the assembled matrix (stage returns to "faces
+ * built"); the next fsfem_assemble_csr rebuilds the pattern.  Errors: INVALID_ARG. */
+typedef enum { FSFEM_METHOD_FS = 0, FSFEM_METHOD_FEM_T4 = 1 } fsfem_method;
+fsfem_status fsfem_set_method(fsfem_ctx* ctx, int method);
+
 /* S1: extract the unique faces of the mesh.
  *   xyz  [3*n_nodes] double, node coordinates (x, y, z per node)            (Node matrix)
  *   tets [4*n_tets]  int32, 0-based node ids; face l of a tet is the face

@@ -5,6 +5,8 @@ binding.  Method: arxiv 2001.08849 (juSFEM), see DESIGN.md.
 """
 from .fsfem import (  # noqa: F401
     EXPORTS,
+    METHOD_FEM_T4,
+    METHOD_FS,
     LIB_PATH,
     Csr,
     FsFem,
@@ -20,6 +22,7 @@ from .fsfem import (  # noqa: F401
     fsfem_get_report,
     fsfem_nccl_get_unique_id,
     fsfem_pcg_solve,
+    fsfem_set_method,
     fsfem_spmv,
     load_library,
 )

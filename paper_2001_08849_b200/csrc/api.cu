@@ -24,15 +24,16 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
                         unsigned long long* h_flags);
 void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
                           const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
-                          DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags);
+                          DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags, int fem);
 void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr, int32_t* col_idx, double* vals,
                        cudaStream_t s);
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
                    const int32_t* face_opp, int64_t nf, double* face_s, cudaStream_t s);
 void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
                           const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
-                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks,
+                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
                           cudaStream_t s);
+void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, cudaStream_t s);
 void apply_bc_device(const int64_t* node_ptr, const int32_t* nbr, const int32_t* diag_slot, int64_t n_lo, int64_t nloc,
                      int64_t nn, const int32_t* dir, int64_t nd, const double* loads, int mode, double penalty_scale,
                      double* vals, double* f, double* dinv, uint8_t* fixed, unsigned long long* flags, cudaStream_t s);
@@ -112,6 +113,7 @@ struct fsfem_ctx {
   bool have_pattern = false;
   Pattern pat;
   // numeric
+  int method = FSFEM_METHOD_FS;
   double E = 0, nu = 0;
   DevBuf<double> face_s, vals;
   // bc / pcg
@@ -339,6 +341,20 @@ fsfem_status fsfem_comm_init(fsfem_ctx* c, const void* uid, int rank, int nranks
   });
 }
 
+fsfem_status fsfem_set_method(fsfem_ctx* c, int method) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (method != FSFEM_METHOD_FS && method != FSFEM_METHOD_FEM_T4)
+      return fail(c, FSFEM_ERR_INVALID_ARG, "method must be FSFEM_METHOD_FS or FSFEM_METHOD_FEM_T4");
+    if (method != c->method) {
+      c->method = method;
+      c->have_pattern = false;  // different node graph
+      drop_graph(c);
+      if (c->stage > kFaces) c->stage = kFaces;
+    }
+    return FSFEM_OK;
+  });
+}
+
 fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes, const int32_t* tets, int64_t n_tets,
                                int64_t* n_faces, int64_t* n_interior) {
   return guarded(c, [&]() -> fsfem_status {
@@ -397,7 +413,7 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       FS_CUDA(cudaEventRecord(c->ev0, c->stream));
       c->h_flags[0] = kNoError;
       build_pattern_device(c->tets.get(), c->nt, c->tet_face.get(), c->face_tet.get(), c->face_opp.get(), c->n_lo,
-                           c->nloc, c->stream, c->scratch, c->pat, c->h_flags);
+                           c->nloc, c->stream, c->scratch, c->pat, c->h_flags, c->method == FSFEM_METHOD_FEM_T4);
       fsfem_status s = decode_flags(c, c->h_flags[0], "symbolic");
       if (s != FSFEM_OK) return s;
       if (9 * c->pat.nblk >= (1LL << 31)) return fail(c, FSFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
@@ -405,18 +421,25 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       FS_CUDA(cudaEventSynchronize(c->ev1));
       c->rep.t_symbolic_ms = elapsed(c->ev0, c->ev1);
       c->vals.ensure(9 * c->pat.nsb + 2);  // + slack for the SpMV bulk copies (pattern.cuh)
-      c->face_s.ensure(16 * c->nf);
+      c->face_s.ensure(16 * std::max(c->nf, c->nt));
       c->have_pattern = true;
       drop_graph(c);
     }
     const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     const double mu = E / (2.0 * (1.0 + nu));
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
-    face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
-                  c->face_s.get(), c->stream);
-    assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->face_nodes.get(),
-                         c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(),
-                         c->pat.max_row_blocks, c->stream);
+    if (c->method == FSFEM_METHOD_FEM_T4) {
+      tet_s_device(c->xyz.get(), c->tets.get(), c->nt, c->face_s.get(), c->stream);
+      assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(),
+                           c->tets.get(), nullptr, c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(),
+                           c->pat.max_row_blocks, true, c->stream);
+    } else {
+      face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
+                    c->face_s.get(), c->stream);
+      assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(),
+                           c->face_nodes.get(), c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu,
+                           c->vals.get(), c->pat.max_row_blocks, false, c->stream);
+    }
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     FS_CUDA(cudaEventSynchronize(c->ev1));
     c->rep.t_numeric_ms = elapsed(c->ev0, c->ev1);

@@ -113,10 +113,74 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
   }
 }
 
+// Field nodes of assembly record r: FS face r = (a, b, c, opp0, opp1) (opp1 = -1 exterior);
+// FEM-T4 tet r = its 4 nodes and -1.
+template <bool kTet>
+__device__ __forceinline__ void record_field(const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
+                                             int64_t r, int32_t (&fld)[5]) {
+  if (kTet) {
+    const int4 v = reinterpret_cast<const int4*>(rec_a)[r];
+    fld[0] = v.x;
+    fld[1] = v.y;
+    fld[2] = v.z;
+    fld[3] = v.w;
+    fld[4] = -1;
+  } else {
+    fld[0] = rec_a[3 * r];
+    fld[1] = rec_a[3 * r + 1];
+    fld[2] = rec_a[3 * r + 2];
+    fld[3] = rec_b[2 * r];
+    fld[4] = rec_b[2 * r + 1];
+  }
+}
+
+// FEM-T4 (PAPER.md:531 and Table 4's FEM-T4 column): per tet
+// s_I = sqrt(V_e) grad N_I (I = 0..3), so that V_e (B_I^T c B_J) = lam M + mu M^T + mu tr(M) I
+// with M = s_I s_J^T, exactly the M-form of the faces.  Record layout as face_s (stride 16).
+__global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, const int32_t* __restrict__ tets,
+                                               int64_t nt, double* __restrict__ tet_s) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v = reinterpret_cast<const int4*>(tets)[t];
+    double x0, y0, z0, x1, y1, z1, x2, y2, z2, x3, y3, z3;
+    load3(xyz, v.x, x0, y0, z0);
+    load3(xyz, v.y, x1, y1, z1);
+    load3(xyz, v.z, x2, y2, z2);
+    load3(xyz, v.w, x3, y3, z3);
+    const double e1x = x1 - x0, e1y = y1 - y0, e1z = z1 - z0;
+    const double e2x = x2 - x0, e2y = y2 - y0, e2z = z2 - z0;
+    const double e3x = x3 - x0, e3y = y3 - y0, e3z = z3 - z0;
+    double g[4][3];
+    g[1][0] = e2y * e3z - e2z * e3y;
+    g[1][1] = e2z * e3x - e2x * e3z;
+    g[1][2] = e2x * e3y - e2y * e3x;
+    g[2][0] = e3y * e1z - e3z * e1y;
+    g[2][1] = e3z * e1x - e3x * e1z;
+    g[2][2] = e3x * e1y - e3y * e1x;
+    g[3][0] = e1y * e2z - e1z * e2y;
+    g[3][1] = e1z * e2x - e1x * e2z;
+    g[3][2] = e1x * e2y - e1y * e2x;
+    const double det = e1x * g[1][0] + e1y * g[1][1] + e1z * g[1][2];
+    const double V = fabs(det) * (1.0 / 6.0);
+    const double sc = sqrt(V) / det;  // grad N_q = (cross product) / det
+    double* out = tet_s + kFaceStride * t;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const double a = g[1][h] * sc, b = g[2][h] * sc, c = g[3][h] * sc;
+      out[3 * 1 + h] = a;
+      out[3 * 2 + h] = b;
+      out[3 * 3 + h] = c;
+      out[h] = -(a + b + c);
+    }
+    out[12] = V;
+    out[13] = out[14] = out[15] = 0.0;
+  }
+}
+
 // Generic path (rows with more than 32 stored blocks; none in the Kuhn beams): warp per own
 // node i; lane = stored block slot (j >= i, or halo j < n_lo; pattern.cuh), in chunks of 32.
 // For every face of F(i) in ascending order, lanes whose neighbour j is in the face's field add
 // s_i s_j^T.
+template <bool kTet>
 __global__ void __launch_bounds__(256) k_assemble_rows(
     const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, const int64_t* __restrict__ nf_ptr,
     const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
@@ -139,8 +203,8 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
       for (int q = 0; q < 9; ++q) M[q] = 0.0;
       for (int64_t k = f0; k < f1; ++k) {
         const int32_t f = nf_idx[k];
-        const int32_t fld[5] = {face_nodes[3 * f], face_nodes[3 * f + 1], face_nodes[3 * f + 2], face_opp[2 * f],
-                                face_opp[2 * f + 1]};
+        int32_t fld[5];
+        record_field<kTet>(face_nodes, face_opp, f, fld);
         int pi = 0, pj = -1;
 #pragma unroll
         for (int K = 0; K < 5; ++K) {
@@ -190,6 +254,7 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
 constexpr int kRowWarps = 4;
 constexpr int kMaxTargets = 4;  // other field nodes of a face
 
+template <bool kTet>
 __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
     const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
     const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
@@ -218,8 +283,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
       // ---- A: lane = face
       if (rb + lane < nfc) {
         const int32_t f = nf_idx[f0 + rb + lane];
-        const int32_t fld[5] = {face_nodes[3 * f], face_nodes[3 * f + 1], face_nodes[3 * f + 2], face_opp[2 * f],
-                                face_opp[2 * f + 1]};
+        int32_t fld[5];
+        record_field<kTet>(face_nodes, face_opp, f, fld);
         const double* sf = face_s + kFaceStride * static_cast<int64_t>(f);
         int pi = 0;
 #pragma unroll
@@ -311,20 +376,30 @@ void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_n
   FS_LAUNCH_CHECK();
 }
 
+// rec_a/rec_b: FS (kTet = false) face_nodes/face_opp; FEM-T4 (tet = true) tets/unused.
 void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
                           const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
-                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, cudaStream_t s) {
+                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
+                          cudaStream_t s) {
   if (nloc == 0) return;
   const int g2 = static_cast<int>(std::min<int64_t>(ceil_div(nloc, kRowWarps), 64LL * num_sms()));
-  k_assemble_rows2<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp,
-                                                               face_s, n_lo, nloc, lam, mu, vals);
+  auto k2 = tet ? k_assemble_rows2<true> : k_assemble_rows2<false>;
+  k2<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo, nloc,
+                                                lam, mu, vals);
   FS_LAUNCH_CHECK();
   if (max_row_blocks > 32) {
     const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
-    k_assemble_rows<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo,
-                                                      nloc, lam, mu, vals, 32);
+    auto k1 = tet ? k_assemble_rows<true> : k_assemble_rows<false>;
+    k1<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo, nloc, lam,
+                                         mu, vals, 32);
     FS_LAUNCH_CHECK();
   }
+}
+
+void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, cudaStream_t s) {
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nt, 256), 16LL * num_sms()));
+  k_tet_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, nt, tet_s);
+  FS_LAUNCH_CHECK();
 }
 
 }  // namespace fsfem

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
     const int32_t* __restrict__ face_opp, const int32_t* __restrict__ nt_ptr, const int32_t* __restrict__ nt_idx,
     int64_t n_lo, int64_t nloc, int32_t* __restrict__ deg, int32_t* __restrict__ nfc,
     const int64_t* __restrict__ node_ptr, const int64_t* __restrict__ nf_ptr, int32_t* __restrict__ nbr,
-    int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err) {
+    int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err, int fem) {
   __shared__ int32_t cand[kPatWarps][kCandCap], tmp[kPatWarps][kCandCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t il = blockIdx.x * (int64_t)kPatWarps + w; il < nloc; il += (int64_t)gridDim.x * kPatWarps) {
@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
       for (int l = 0; l < 4; ++l) {
         const int32_t f = tet_face[4 * t + l];
         const int32_t ta = face_tet[2 * f], tb = face_tet[2 * f + 1];
-        int32_t across = kSentinel;
-        if (tb >= 0) across = (ta == t) ? face_opp[2 * f + 1] : face_opp[2 * f];
+        int32_t across = kSentinel;  // FEM-T4 couples only the nodes of a tet
+        if (tb >= 0 && !fem) across = (ta == t) ? face_opp[2 * f + 1] : face_opp[2 * f];
         cand[w][8 * k + 4 + l] = across;
       }
     }
@@ -114,14 +114,21 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
       }
     }
     __syncwarp();
-    // faces whose field holds i: the 4 faces of every tet containing i (shared ones twice)
-    for (int k = lane; k < ntet; k += 32) {
-      const int32_t t = nt_idx[b + k];
+    // FS: faces whose field holds i = the 4 faces of every tet containing i (shared ones twice);
+    // FEM-T4: the tets containing i (already ascending).  Either is the assembly order of row i.
+    int fn = ntet;
+    if (fem) {
+      for (int k = lane; k < ntet; k += 32) cand[w][k] = nt_idx[b + k];
+      __syncwarp();
+    } else {
+      for (int k = lane; k < ntet; k += 32) {
+        const int32_t t = nt_idx[b + k];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) cand[w][4 * k + l] = tet_face[4 * t + l];
+        for (int l = 0; l < 4; ++l) cand[w][4 * k + l] = tet_face[4 * t + l];
+      }
+      __syncwarp();
+      fn = warp_sort_unique(cand[w], tmp[w], 4 * ntet, lane);
     }
-    __syncwarp();
-    const int fn = warp_sort_unique(cand[w], tmp[w], 4 * ntet, lane);
     if (!kWrite) {
       if (lane == 0) nfc[il] = fn;
     } else {
@@ -267,7 +274,7 @@ __global__ void k_export_csr(const int64_t* __restrict__ node_ptr, const int32_t
 // Host driver of S5 for the own node range [n_lo, n_lo + nloc).
 void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
                           const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
-                          DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags) {
+                          DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags, int fem) {
   DevBuf<int64_t>& node_ptr = pat.node_ptr;
   DevBuf<int32_t>& nbr = pat.nbr;
   DevBuf<int64_t>& nf_ptr = pat.nf_ptr;
@@ -314,7 +321,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   k_sort_segments<<<gw, kPatWarps * 32, 0, s>>>(ptr, nloc, idx, flags);
   FS_LAUNCH_CHECK();
   k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc, deg,
-                                                      nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags);
+                                                      nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags, fem);
   FS_LAUNCH_CHECK();
   node_ptr.ensure(nloc + 1);
   nf_ptr.ensure(nloc + 1);
@@ -333,7 +340,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   diag_slot.ensure(nloc);
   k_node_pattern<true><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc,
                                                      nullptr, nullptr, node_ptr.get(), nf_ptr.get(), nbr.get(),
-                                                     nf_idx.get(), diag_slot.get(), flags);
+                                                     nf_idx.get(), diag_slot.get(), flags, fem);
   FS_LAUNCH_CHECK();
   // symmetric split (pattern.cuh): deg and nfc are free again, reuse them as counters
   const int gt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 8LL * sms)));

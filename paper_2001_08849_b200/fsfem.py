@@ -23,7 +23,9 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
                 6: "BREAKDOWN", 7: "STATE", 8: "CUDA", 9: "NCCL", 10: "OOM"}
 
 # Every symbol include/fsfem.h declares (checked by tests/test_abi.py).
-EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init",
+METHOD_FS, METHOD_FEM_T4 = 0, 1
+
+EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv"]
 
@@ -67,6 +69,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_destroy": (I, [P]),
         "fsfem_last_error": (ctypes.c_char_p, [P]),
         "fsfem_comm_init": (I, [P, P, I, I]),
+        "fsfem_set_method": (I, [P, I]),
         "fsfem_nccl_get_unique_id": (I, [P]),
         "fsfem_build_faces": (I, [P, P, I64, P, I64, P, P]),
         "fsfem_get_faces": (I, [P, P, P, P]),
@@ -147,6 +150,10 @@ def fsfem_comm_init(ctx, unique_id: bytes | None, rank: int, nranks: int) -> Non
     """unique_id None: partition-only context (include/fsfem.h)."""
     buf = ctypes.create_string_buffer(bytes(unique_id), 128) if unique_id is not None else None
     _raise(ctx, load_library().fsfem_comm_init(ctx, buf, rank, nranks))
+
+
+def fsfem_set_method(ctx, method: int) -> None:
+    _raise(ctx, load_library().fsfem_set_method(ctx, int(method)))
 
 
 def fsfem_build_faces(ctx, xyz, tets):
@@ -233,6 +240,9 @@ class FsFem:
 
     def comm_init(self, unique_id: bytes | None, rank: int, nranks: int):
         fsfem_comm_init(self.ctx, unique_id, rank, nranks)
+
+    def set_method(self, method: int):
+        fsfem_set_method(self.ctx, method)
 
     def build_faces(self, xyz, tets):
         self.n_nodes = _nelem(xyz) // 3

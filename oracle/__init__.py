@@ -61,6 +61,7 @@ def lib():
             "ora_pcg": (I32, [P, D, I64, P, P, P, P]),
             "ora_cholesky": (I32, [P, P]),
             "ora_cholesky_eliminate": (I32, [P, P, I64, P, P]),
+            "ora_recover": (I32, [P, D, D, P, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -190,6 +191,15 @@ class Oracle:
         u = np.empty(3 * self.nn, np.float64)
         self._check(lib().ora_cholesky(self._h, _p(u)))
         return u
+
+    def recover(self, E: float, nu: float, u: np.ndarray):
+        """O9: (face strain [N_f,6], face stress [N_f,6], nodal stress [nn,6], nodal von Mises [nn])."""
+        u = np.ascontiguousarray(u, np.float64).reshape(-1)
+        nf = len(self.build_faces()[0]) if not hasattr(self, "n_faces") else self.n_faces
+        eps, sig = np.empty((nf, 6)), np.empty((nf, 6))
+        ns, vm = np.empty((self.nn, 6)), np.empty(self.nn)
+        self._check(lib().ora_recover(self._h, E, nu, _p(u), _p(eps), _p(sig), _p(ns), _p(vm)))
+        return eps, sig, ns, vm
 
     def cholesky_eliminate(self, dirichlet: np.ndarray, loads: np.ndarray) -> np.ndarray:
         d = np.ascontiguousarray(dirichlet, np.int32)

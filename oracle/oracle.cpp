@@ -723,3 +723,56 @@ int ora_cholesky_eliminate(ora_mesh* m, const int32_t* dirichlet, int64_t n_dir,
 }
 
 }  // extern "C"
+
+// O9 ("first obtain the nodal displacements and then the strain
+// and stress", 457): per smoothing domain k the smoothed strain of Eq. 2 with the B-bar of Eq. 4,
+// eps_k = B_k d_k (Voigt xx, yy, zz, yz, xz, xy, engineering shear), sigma_k = c eps_k; per node
+// the volume-weighted mean over the domains whose field holds the node (averaging rule: reading
+// Q27, the paper does not state one), and the von Mises stress of that mean.
+int ora_recover(ora_mesh* m, double E, double nu, const double* u, double* strain, double* stress,
+                double* node_stress, double* node_vm) {
+  if (!m->faces_built) return fail(m, 6, "faces not built");
+  double c[6][6];
+  material(E, nu, c);
+  const int64_t nf = static_cast<int64_t>(m->face_nodes.size());
+  std::vector<double> acc(6 * static_cast<size_t>(m->nn), 0.0), w(static_cast<size_t>(m->nn), 0.0);
+  for (int64_t f = 0; f < nf; ++f) {
+    int32_t fld[5];
+    double bb[15], Vf;
+    int P;
+    ora_face_domain(m, f, fld, bb, &Vf, &P, nullptr);
+    const int n = (fld[4] >= 0) ? 5 : 4;
+    double eps[6] = {0, 0, 0, 0, 0, 0};
+    for (int I = 0; I < n; ++I) {
+      double blk[6][3];
+      eq4_block(&bb[3 * I], blk);  // Eq. 4 block of node I
+      for (int r = 0; r < 6; ++r)
+        for (int a = 0; a < 3; ++a) eps[r] += blk[r][a] * u[3 * static_cast<int64_t>(fld[I]) + a];
+    }
+    double sig[6];
+    for (int r = 0; r < 6; ++r) {
+      double s = 0.0;
+      for (int k = 0; k < 6; ++k) s += c[r][k] * eps[k];
+      sig[r] = s;
+    }
+    for (int r = 0; r < 6; ++r) {
+      if (strain) strain[6 * f + r] = eps[r];
+      if (stress) stress[6 * f + r] = sig[r];
+    }
+    for (int I = 0; I < n; ++I) {
+      for (int r = 0; r < 6; ++r) acc[6 * static_cast<size_t>(fld[I]) + r] += Vf * sig[r];
+      w[fld[I]] += Vf;
+    }
+  }
+  for (int64_t i = 0; i < m->nn; ++i) {
+    double s[6];
+    for (int r = 0; r < 6; ++r) s[r] = (w[i] > 0.0) ? acc[6 * i + r] / w[i] : 0.0;
+    if (node_stress)
+      for (int r = 0; r < 6; ++r) node_stress[6 * i + r] = s[r];
+    if (node_vm) {
+      const double d01 = s[0] - s[1], d12 = s[1] - s[2], d20 = s[2] - s[0];
+      node_vm[i] = std::sqrt(0.5 * (d01 * d01 + d12 * d12 + d20 * d20) + 3.0 * (s[3] * s[3] + s[4] * s[4] + s[5] * s[5]));
+    }
+  }
+  return 0;
+}

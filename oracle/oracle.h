@@ -73,6 +73,13 @@ int ora_cholesky(ora_mesh* m, double* u);
 int ora_cholesky_eliminate(ora_mesh* m, const int32_t* dirichlet, int64_t n_dir,
                            const double* loads, double* u);
 
+/* O9: smoothed strain eps_k = B_k d (Eq. 2, 4) and stress
+ * sigma_k = c eps_k per face [6*N_f] (Voigt xx,yy,zz,yz,xz,xy, engineering shear), the
+ * volume-weighted nodal mean of sigma over the faces whose field holds the node [6*nn] and its von
+ * Mises value [nn].  Any output may be NULL. */
+int ora_recover(ora_mesh* m, double E, double nu, const double* u, double* strain, double* stress,
+                double* node_stress, double* node_vm);
+
 #ifdef __cplusplus
 }
 #endif

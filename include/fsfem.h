@@ -158,6 +158,18 @@ fsfem_status fsfem_apply_bc(fsfem_ctx* ctx, const int32_t* dirichlet_nodes, int6
 fsfem_status fsfem_pcg_solve(fsfem_ctx* ctx, double* u, int u0_is_zero, double rel_tol,
                              int64_t max_iter, fsfem_report* rep);
 
+/* Strain / stress recovery ("first obtain the nodal displacements and then the
+ * strain and stress", 457).  For the displacements u [3*n_nodes] (full vector),
+ * per smoothing domain k (FS: face, in face order; FEM-T4: tet) the smoothed strain
+ * eps_k = B_k u (Eq. 2 with Eq. 4's B; Voigt xx, yy, zz, yz, xz, xy, engineering shear) ->
+ * strain [6*n_domains], stress = c eps -> stress [6*n_domains]; per own node the volume-weighted
+ * mean of the stress over the domains whose field holds the node -> node_stress [6*n_nodes] and
+ * its von Mises value -> node_vm [n_nodes] (only this rank's nodes are written).  Any output may
+ * be NULL; n_domains [host] receives N_f (FS) or N_t (FEM-T4).  Needs assemble_csr (uses its E,
+ * nu).  Errors: STATE, INVALID_ARG. */
+fsfem_status fsfem_recover_stress(fsfem_ctx* ctx, const double* u, double* strain, double* stress,
+                                  double* node_stress, double* node_vm, int64_t* n_domains);
+
 /* Report of the last calls (timings and last PCG data); rep [host]. */
 fsfem_status fsfem_get_report(const fsfem_ctx* ctx, fsfem_report* rep);
 

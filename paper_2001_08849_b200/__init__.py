@@ -22,6 +22,7 @@ from .fsfem import (  # noqa: F401
     fsfem_get_report,
     fsfem_nccl_get_unique_id,
     fsfem_pcg_solve,
+    fsfem_recover_stress,
     fsfem_set_method,
     fsfem_spmv,
     load_library,

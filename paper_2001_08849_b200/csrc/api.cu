@@ -34,6 +34,9 @@ void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int
                           int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
                           cudaStream_t s);
 void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, cudaStream_t s);
+void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, int64_t nrec,
+                    const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
+                    double* strain, double* stress, double* node_stress, double* node_vm, cudaStream_t s);
 void apply_bc_device(const int64_t* node_ptr, const int32_t* nbr, const int32_t* diag_slot, int64_t n_lo, int64_t nloc,
                      int64_t nn, const int32_t* dir, int64_t nd, const double* loads, int mode, double penalty_scale,
                      double* vals, double* f, double* dinv, uint8_t* fixed, unsigned long long* flags, cudaStream_t s);
@@ -118,6 +121,7 @@ struct fsfem_ctx {
   DevBuf<double> face_s, vals;
   // bc / pcg
   DevBuf<double> f, dinv, x_full, r, p_full, q, part, all;
+  DevBuf<double> rec_u, rec_strain, rec_stress, rec_nodes, rec_vm;  // stress recovery
   DevBuf<uint8_t> fixed;
   DevBuf<PcgState> st;
   DevBuf<unsigned char> scratch;
@@ -632,6 +636,39 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     if (h.status == FSFEM_ERR_BREAKDOWN) return fail(c, FSFEM_ERR_BREAKDOWN, "pcg breakdown (p.q <= 0 or non-finite)");
     if (h.status == FSFEM_ERR_NOT_CONVERGED)
       return fail(c, FSFEM_ERR_NOT_CONVERGED, "pcg reached max_iter=" + std::to_string(max_iter));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_recover_stress(fsfem_ctx* c, const double* u, double* strain, double* stress, double* node_stress,
+                                  double* node_vm, int64_t* n_domains) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
+    if (!u) return fail(c, FSFEM_ERR_INVALID_ARG, "null u");
+    const bool tet = c->method == FSFEM_METHOD_FEM_T4;
+    const int64_t nd = tet ? c->nt : c->nf;
+    if (n_domains) *n_domains = nd;
+    const double lam = c->E * c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
+    const double mu = c->E / (2.0 * (1.0 + c->nu));
+    c->rec_u.ensure(3 * c->nn);
+    to_device(c->rec_u.get(), u, sizeof(double) * 3 * c->nn, c->stream);
+    double* d_stress = (stress && is_device_ptr(stress)) ? stress : c->rec_stress.ensure(6 * nd);
+    double* d_strain = nullptr;
+    if (strain) d_strain = is_device_ptr(strain) ? strain : c->rec_strain.ensure(6 * nd);
+    double* d_nodes = nullptr;
+    if (node_stress)
+      d_nodes = is_device_ptr(node_stress) ? node_stress + 6 * c->n_lo : c->rec_nodes.ensure(std::max<int64_t>(6 * c->nloc, 1));
+    double* d_vm = nullptr;
+    if (node_vm) d_vm = is_device_ptr(node_vm) ? node_vm + c->n_lo : c->rec_vm.ensure(std::max<int64_t>(c->nloc, 1));
+    recover_device(tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet, c->face_s.get(), nd,
+                   c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->nloc, c->rec_u.get(), lam, mu, d_strain, d_stress,
+                   d_nodes, d_vm, c->stream);
+    if (stress && d_stress != stress) from_device(stress, d_stress, sizeof(double) * 6 * nd, c->stream);
+    if (strain && d_strain != strain) from_device(strain, d_strain, sizeof(double) * 6 * nd, c->stream);
+    if (node_stress && !is_device_ptr(node_stress))
+      from_device(node_stress + 6 * c->n_lo, d_nodes, sizeof(double) * 6 * c->nloc, c->stream);
+    if (node_vm && !is_device_ptr(node_vm)) from_device(node_vm + c->n_lo, d_vm, sizeof(double) * c->nloc, c->stream);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });
 }

@@ -27,7 +27,7 @@ METHOD_FS, METHOD_FEM_T4 = 0, 1
 
 EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
-           "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv"]
+           "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress"]
 
 
 class FsfemReport(ctypes.Structure):
@@ -79,6 +79,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_pcg_solve": (I, [P, P, I, D, I64, ctypes.POINTER(FsfemReport)]),
         "fsfem_get_report": (I, [P, ctypes.POINTER(FsfemReport)]),
         "fsfem_spmv": (I, [P, P, P]),
+        "fsfem_recover_stress": (I, [P, P, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -208,6 +209,13 @@ def fsfem_spmv(ctx, p, q) -> None:
     _raise(ctx, load_library().fsfem_spmv(ctx, _ptr(p), _ptr(q)))
 
 
+def fsfem_recover_stress(ctx, u, strain, stress, node_stress, node_vm) -> int:
+    nd = ctypes.c_int64()
+    _raise(ctx, load_library().fsfem_recover_stress(ctx, _ptr(u), _ptr(strain), _ptr(stress), _ptr(node_stress),
+                                                    _ptr(node_vm), ctypes.byref(nd)))
+    return nd.value
+
+
 # ------------------------------------------------------------------ convenience object
 @dataclass
 class Csr:
@@ -279,6 +287,14 @@ class FsFem:
         q = np.zeros(3 * self.n_nodes)
         fsfem_spmv(self.ctx, np.ascontiguousarray(p, np.float64), q)
         return q
+
+    def recover_stress(self, u, n_domains: int):
+        """(domain strain [n,6], domain stress [n,6], nodal stress [nn,6], nodal von Mises [nn])."""
+        u = np.ascontiguousarray(u, np.float64).reshape(-1)
+        eps, sig = np.empty((n_domains, 6)), np.empty((n_domains, 6))
+        ns, vm = np.zeros((self.n_nodes, 6)), np.zeros(self.n_nodes)
+        fsfem_recover_stress(self.ctx, u, eps, sig, ns, vm)
+        return eps, sig, ns, vm
 
     def report(self) -> dict:
         return fsfem_get_report(self.ctx)

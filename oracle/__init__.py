@@ -62,6 +62,7 @@ def lib():
             "ora_cholesky": (I32, [P, P]),
             "ora_cholesky_eliminate": (I32, [P, P, I64, P, P]),
             "ora_recover": (I32, [P, D, D, P, P, P, P, P]),
+            "ora_surface_loads": (I32, [P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -200,6 +201,14 @@ class Oracle:
         ns, vm = np.empty((self.nn, 6)), np.empty(self.nn)
         self._check(lib().ora_recover(self._h, E, nu, _p(u), _p(eps), _p(sig), _p(ns), _p(vm)))
         return eps, sig, ns, vm
+
+    def surface_loads(self, node_flag: np.ndarray, traction) -> np.ndarray:
+        """O10: nodal loads [nn, 3] of a uniform traction on the flagged exterior faces."""
+        fl = np.ascontiguousarray(node_flag, np.uint8)
+        t = np.ascontiguousarray(traction, np.float64)
+        out = np.empty((self.nn, 3))
+        self._check(lib().ora_surface_loads(self._h, _p(fl), _p(t), _p(out)))
+        return out
 
     def cholesky_eliminate(self, dirichlet: np.ndarray, loads: np.ndarray) -> np.ndarray:
         d = np.ascontiguousarray(dirichlet, np.int32)

@@ -776,3 +776,22 @@ int ora_recover(ora_mesh* m, double E, double nu, const double* u, double* strai
   }
   return 0;
 }
+
+// O10 ("the nodal load is calculated"; 496-499 §4.1: uniform pressure on the upper
+// face): a uniform traction t on the exterior faces whose three nodes are all
+// flagged gives each of those nodes t * A / 3 (A from Eq. 11), accumulated in face order.
+int ora_surface_loads(ora_mesh* m, const uint8_t* node_flag, const double* traction, double* loads) {
+  if (!m->faces_built) return fail(m, 6, "faces not built");
+  for (int64_t i = 0; i < 3 * m->nn; ++i) loads[i] = 0.0;
+  const int64_t nf = static_cast<int64_t>(m->face_nodes.size());
+  for (int64_t f = 0; f < nf; ++f) {
+    if (m->face_tet[f][1] >= 0) continue;  // interior face
+    const int32_t* v = m->face_nodes[f].data();
+    if (!node_flag[v[0]] || !node_flag[v[1]] || !node_flag[v[2]]) continue;
+    const V3 a = node(m, v[0]), b = node(m, v[1]), c = node(m, v[2]);
+    const double area = 0.5 * norm(cross(sub(b, a), sub(c, a)));  // Eq. 11
+    for (int k = 0; k < 3; ++k)
+      for (int h = 0; h < 3; ++h) loads[3 * static_cast<int64_t>(v[k]) + h] += traction[h] * area / 3.0;
+  }
+  return 0;
+}

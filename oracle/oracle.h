@@ -80,6 +80,10 @@ int ora_cholesky_eliminate(ora_mesh* m, const int32_t* dirichlet, int64_t n_dir,
 int ora_recover(ora_mesh* m, double E, double nu, const double* u, double* strain, double* stress,
                 double* node_stress, double* node_vm);
 
+/* O10: nodal loads [3*nn] of a uniform traction[3] (N/m^2) on the exterior
+ * faces whose 3 nodes all have node_flag[] != 0: each such node gets traction * A_face / 3. */
+int ora_surface_loads(ora_mesh* m, const uint8_t* node_flag, const double* traction, double* loads);
+
 #ifdef __cplusplus
 }
 #endif

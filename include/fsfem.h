@@ -170,6 +170,14 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* ctx, double* u, int u0_is_zero, double r
 fsfem_status fsfem_recover_stress(fsfem_ctx* ctx, const double* u, double* strain, double* stress,
                                   double* node_stress, double* node_vm, int64_t* n_domains);
 
+/* Nodal loads of a surface traction ("the nodal load is calculated"; 496-499: the
+ * §4.1 beam's uniform pressure on its upper face).  node_flag [n_nodes] (bytes,
+ * nonzero = on the loaded surface), traction [3, host] in N/m^2: every exterior face whose three
+ * nodes are flagged gives each of them traction * area / 3.  loads [3*n_nodes] receives this rank's
+ * node rows (others untouched).  Needs assemble_csr (uses its node lists).  The fixed mask of a
+ * previous apply_bc is overwritten (apply_bc rebuilds it).  Errors: STATE, INVALID_ARG. */
+fsfem_status fsfem_surface_loads(fsfem_ctx* ctx, const uint8_t* node_flag, const double* traction, double* loads);
+
 /* Report of the last calls (timings and last PCG data); rep [host]. */
 fsfem_status fsfem_get_report(const fsfem_ctx* ctx, fsfem_report* rep);
 

@@ -25,5 +25,6 @@ from .fsfem import (  # noqa: F401
     fsfem_recover_stress,
     fsfem_set_method,
     fsfem_spmv,
+    fsfem_surface_loads,
     load_library,
 )

@@ -37,6 +37,9 @@ void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* te
 void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, int64_t nrec,
                     const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
                     double* strain, double* stress, double* node_stress, double* node_vm, cudaStream_t s);
+void surface_loads_device(const int64_t* nd_ptr, const int32_t* nd_idx, bool tet, const int32_t* tet_face,
+                          const int32_t* face_nodes, const int32_t* face_tet, const uint8_t* flag, const double* xyz,
+                          int64_t n_lo, int64_t nloc, const double* t, double* loads, cudaStream_t s);
 void apply_bc_device(const int64_t* node_ptr, const int32_t* nbr, const int32_t* diag_slot, int64_t n_lo, int64_t nloc,
                      int64_t nn, const int32_t* dir, int64_t nd, const double* loads, int mode, double penalty_scale,
                      double* vals, double* f, double* dinv, uint8_t* fixed, unsigned long long* flags, cudaStream_t s);
@@ -668,6 +671,22 @@ fsfem_status fsfem_recover_stress(fsfem_ctx* c, const double* u, double* strain,
     if (node_stress && !is_device_ptr(node_stress))
       from_device(node_stress + 6 * c->n_lo, d_nodes, sizeof(double) * 6 * c->nloc, c->stream);
     if (node_vm && !is_device_ptr(node_vm)) from_device(node_vm + c->n_lo, d_vm, sizeof(double) * c->nloc, c->stream);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_surface_loads(fsfem_ctx* c, const uint8_t* node_flag, const double* traction, double* loads) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first (uses its node lists)");
+    if (!node_flag || !traction || !loads) return fail(c, FSFEM_ERR_INVALID_ARG, "null argument");
+    c->fixed.ensure(c->nn);
+    to_device(c->fixed.get(), node_flag, c->nn, c->stream);
+    double* d_loads = is_device_ptr(loads) ? loads + 3 * c->n_lo : c->rec_u.ensure(std::max<int64_t>(3 * c->nloc, 1));
+    surface_loads_device(c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->method == FSFEM_METHOD_FEM_T4, c->tet_face.get(),
+                         c->face_nodes.get(), c->face_tet.get(), c->fixed.get(), c->xyz.get(), c->n_lo, c->nloc,
+                         traction, d_loads, c->stream);
+    if (!is_device_ptr(loads)) from_device(loads + 3 * c->n_lo, d_loads, sizeof(double) * 3 * c->nloc, c->stream);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });

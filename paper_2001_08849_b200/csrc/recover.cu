@@ -112,3 +112,63 @@ void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const 
 }
 
 }  // namespace fsfem
+
+// ---------------------------------------------------------------------------------------------
+// Surface loads ("the nodal load is calculated"; 496-499: uniform pressure on the
+// upper face): each exterior face whose three nodes are flagged gives each of
+// them traction * A / 3.  Thread per own node, over its assembly list in ascending order
+// (FS: the faces holding the node; FEM-T4: its tets, whose exterior faces are found through
+// tet_face -- an exterior face has exactly one tet): deterministic, no atomics.
+namespace fsfem {
+namespace {
+
+__device__ __forceinline__ double tri_area(const double* __restrict__ xyz, int32_t a, int32_t b, int32_t c) {
+  const double ax = xyz[3 * a], ay = xyz[3 * a + 1], az = xyz[3 * a + 2];
+  const double ux = xyz[3 * b] - ax, uy = xyz[3 * b + 1] - ay, uz = xyz[3 * b + 2] - az;
+  const double vx = xyz[3 * c] - ax, vy = xyz[3 * c + 1] - ay, vz = xyz[3 * c + 2] - az;
+  const double cx = uy * vz - uz * vy, cy = uz * vx - ux * vz, cz = ux * vy - uy * vx;
+  return 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+}
+
+__global__ void __launch_bounds__(256) k_surface_loads(const int64_t* __restrict__ nd_ptr,
+                                                       const int32_t* __restrict__ nd_idx, bool tet,
+                                                       const int32_t* __restrict__ tet_face,
+                                                       const int32_t* __restrict__ face_nodes,
+                                                       const int32_t* __restrict__ face_tet,
+                                                       const uint8_t* __restrict__ flag,
+                                                       const double* __restrict__ xyz, int64_t n_lo, int64_t nloc,
+                                                       double tx, double ty, double tz, double* __restrict__ loads) {
+  for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = static_cast<int32_t>(n_lo + il);
+    double A = 0.0;
+    for (int64_t k = nd_ptr[il]; k < nd_ptr[il + 1]; ++k) {
+      const int32_t r = nd_idx[k];
+      const int nl = tet ? 4 : 1;
+      for (int l = 0; l < nl; ++l) {
+        const int32_t f = tet ? tet_face[4 * r + l] : r;
+        if (face_tet[2 * f + 1] >= 0) continue;  // interior face
+        const int32_t a = face_nodes[3 * f], b = face_nodes[3 * f + 1], c = face_nodes[3 * f + 2];
+        if (a != i && b != i && c != i) continue;
+        if (!flag[a] || !flag[b] || !flag[c]) continue;
+        A += tri_area(xyz, a, b, c) * (1.0 / 3.0);
+      }
+    }
+    loads[3 * il] = tx * A;
+    loads[3 * il + 1] = ty * A;
+    loads[3 * il + 2] = tz * A;
+  }
+}
+
+}  // namespace
+
+void surface_loads_device(const int64_t* nd_ptr, const int32_t* nd_idx, bool tet, const int32_t* tet_face,
+                          const int32_t* face_nodes, const int32_t* face_tet, const uint8_t* flag, const double* xyz,
+                          int64_t n_lo, int64_t nloc, const double* t, double* loads, cudaStream_t s) {
+  if (nloc == 0) return;
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 16LL * num_sms())));
+  k_surface_loads<<<g, 256, 0, s>>>(nd_ptr, nd_idx, tet, tet_face, face_nodes, face_tet, flag, xyz, n_lo, nloc, t[0],
+                                    t[1], t[2], loads);
+  FS_LAUNCH_CHECK();
+}
+
+}  // namespace fsfem

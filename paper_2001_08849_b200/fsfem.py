@@ -27,7 +27,8 @@ METHOD_FS, METHOD_FEM_T4 = 0, 1
 
 EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
-           "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress"]
+           "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
+           "fsfem_surface_loads"]
 
 
 class FsfemReport(ctypes.Structure):
@@ -80,6 +81,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_get_report": (I, [P, ctypes.POINTER(FsfemReport)]),
         "fsfem_spmv": (I, [P, P, P]),
         "fsfem_recover_stress": (I, [P, P, P, P, P, P, P]),
+        "fsfem_surface_loads": (I, [P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -216,6 +218,11 @@ def fsfem_recover_stress(ctx, u, strain, stress, node_stress, node_vm) -> int:
     return nd.value
 
 
+def fsfem_surface_loads(ctx, node_flag, traction, loads) -> None:
+    t = np.ascontiguousarray(traction, np.float64)
+    _raise(ctx, load_library().fsfem_surface_loads(ctx, _ptr(node_flag), _ptr(t), _ptr(loads)))
+
+
 # ------------------------------------------------------------------ convenience object
 @dataclass
 class Csr:
@@ -295,6 +302,12 @@ class FsFem:
         ns, vm = np.zeros((self.n_nodes, 6)), np.zeros(self.n_nodes)
         fsfem_recover_stress(self.ctx, u, eps, sig, ns, vm)
         return eps, sig, ns, vm
+
+    def surface_loads(self, node_flag, traction):
+        """Nodal loads [n_nodes, 3] of a uniform traction on the flagged exterior faces."""
+        loads = np.zeros((self.n_nodes, 3))
+        fsfem_surface_loads(self.ctx, np.ascontiguousarray(node_flag, np.uint8), traction, loads)
+        return loads
 
     def report(self) -> dict:
         return fsfem_get_report(self.ctx)

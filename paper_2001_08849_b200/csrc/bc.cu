@@ -54,8 +54,10 @@ __global__ void k_bc_rhs(const double* __restrict__ loads, const uint8_t* __rest
   }
 }
 
+// Index of diagonal entry a of own node il, or -1 when the node has no diagonal block (in no tet).
 __device__ __forceinline__ int64_t diag_index(const int64_t* node_ptr, const int32_t* diag_slot, int64_t il, int a) {
-  return 9 * (node_ptr[il] + diag_slot[il]) + 4 * a;
+  const int32_t d = diag_slot[il];
+  return d < 0 ? -1 : 9 * (node_ptr[il] + d) + 4 * a;
 }
 
 // max_i K_ii over own rows, as the bit pattern of a non-negative double (ordered like integers).
@@ -63,7 +65,10 @@ __global__ void k_diag_max(const int64_t* __restrict__ node_ptr, const int32_t* 
                            const double* __restrict__ vals, int64_t nloc, unsigned long long* __restrict__ out) {
   double mx = 0.0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3 * nloc; k += (int64_t)gridDim.x * blockDim.x)
-    mx = fmax(mx, vals[diag_index(node_ptr, diag_slot, k / 3, static_cast<int>(k % 3))]);
+  {
+    const int64_t di = diag_index(node_ptr, diag_slot, k / 3, static_cast<int>(k % 3));
+    if (di >= 0) mx = fmax(mx, vals[di]);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(mx)));
@@ -74,7 +79,8 @@ __global__ void k_bc_penalty(const int64_t* __restrict__ node_ptr, const int32_t
                              double scale, double* __restrict__ vals) {
   const double alpha = scale * __longlong_as_double(static_cast<long long>(*dmax));
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3 * nloc; k += (int64_t)gridDim.x * blockDim.x) {
-    if (fixed[n_lo + k / 3]) vals[diag_index(node_ptr, diag_slot, k / 3, static_cast<int>(k % 3))] += alpha;
+    const int64_t di = diag_index(node_ptr, diag_slot, k / 3, static_cast<int>(k % 3));
+    if (fixed[n_lo + k / 3] && di >= 0) vals[di] += alpha;
   }
 }
 
@@ -82,7 +88,8 @@ __global__ void k_dinv(const int64_t* __restrict__ node_ptr, const int32_t* __re
                        const double* __restrict__ vals, int64_t n_lo, int64_t nloc, double* __restrict__ dinv,
                        unsigned long long* __restrict__ err) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 3 * nloc; k += (int64_t)gridDim.x * blockDim.x) {
-    const double d = vals[diag_index(node_ptr, diag_slot, k / 3, static_cast<int>(k % 3))];
+    const int64_t di = diag_index(node_ptr, diag_slot, k / 3, static_cast<int>(k % 3));
+    const double d = di >= 0 ? vals[di] : 0.0;
     if (!(d > 0.0) || !isfinite(d)) report_error(err, FSFEM_ERR_BREAKDOWN, 3 * n_lo + k);
     dinv[k] = 1.0 / d;
   }

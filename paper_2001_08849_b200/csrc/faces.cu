@@ -63,11 +63,32 @@ __global__ void k_bbox_partial(const double* __restrict__ xyz, int64_t nn, doubl
   }
 }
 
-__global__ void k_bbox_final(const double* __restrict__ part, int nparts, double* __restrict__ bbox) {
+// One block of 256 threads: strided partial reductions, then warp trees (min/max are exact and
+// order-independent).
+__global__ void __launch_bounds__(256) k_bbox_final(const double* __restrict__ part, int nparts,
+                                                    double* __restrict__ bbox) {
+  double r[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+#pragma unroll
+    for (int a = 0; a < 6; ++a) r[a] = a < 3 ? fmin(r[a], part[6 * b + a]) : fmax(r[a], part[6 * b + a]);
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v = __shfl_xor_sync(0xffffffffu, r[a], o);
+      r[a] = a < 3 ? fmin(r[a], v) : fmax(r[a], v);
+    }
+  __shared__ double s[8][6];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int a = 0; a < 6; ++a) s[wid][a] = r[a];
+  __syncthreads();
   if (threadIdx.x < 6) {
-    double r = part[threadIdx.x];
-    for (int b = 1; b < nparts; ++b) r = threadIdx.x < 3 ? fmin(r, part[6 * b + threadIdx.x]) : fmax(r, part[6 * b + threadIdx.x]);
-    bbox[threadIdx.x] = r;
+    double v = s[0][threadIdx.x];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      v = threadIdx.x < 3 ? fmin(v, s[w][threadIdx.x]) : fmax(v, s[w][threadIdx.x]);
+    bbox[threadIdx.x] = v;
   }
 }
 
@@ -335,7 +356,7 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   const int nbb = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(1, ceil_div(nn, 256))));
   k_bbox_partial<<<nbb, 256, 0, s>>>(d_xyz, nn, bbp);
   FS_LAUNCH_CHECK();
-  k_bbox_final<<<1, 32, 0, s>>>(bbp, nbb, bb);
+  k_bbox_final<<<1, 256, 0, s>>>(bbp, nbb, bb);
   FS_LAUNCH_CHECK();
   const int grid_t = static_cast<int>(std::min<int64_t>(ceil_div(nt, 256), 8LL * sms));
   k_face_count<<<grid_t, 256, 0, s>>>(reinterpret_cast<const int4*>(d_tets), nt, nn, d_xyz, bb, cnt, flags);

@@ -189,6 +189,7 @@ __global__ void k_split_stored(const int64_t* __restrict__ node_ptr, const int32
   for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = n_lo + il;
     int64_t o = sptr[il];
+    sdiag[il] = -1;  // a node in no tet has no blocks at all (BCs then report BREAKDOWN)
     for (int64_t k = node_ptr[il]; k < node_ptr[il + 1]; ++k) {
       const int32_t j = nbr[k];
       if (j >= n_lo && j < i) continue;

@@ -354,3 +354,84 @@ def test_cfg5_solution_properties(fs):
     assert 0.97 * eb <= tip <= 1.03 * 4.031e-3, (tip, eb)
     fixed = np.repeat(np.isin(np.arange(m.n_nodes), m.dirichlet), 3)
     assert np.all(u[fixed] == 0.0)
+
+
+# ---------------------------------------------------------------- error paths and edge cases
+def test_not_converged_reports_and_writes_u(fs):
+    from paper_2001_08849_b200 import fsfem_pcg_solve
+    m = config_mesh(2)
+    g = fs()
+    g.build_faces(m.xyz, m.tets)
+    g.assemble_csr(E, NU)
+    g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+    u = np.zeros(3 * m.n_nodes)
+    rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, 7, allow_not_converged=True)
+    assert rep["status"] == "NOT_CONVERGED" and rep["iterations"] == 7 and rep["converged"] == 0
+    assert np.linalg.norm(u) > 0 and rep["rel_residual"] > 1e-10
+    # the same 7 iterations as the start of a full solve: deterministic prefix
+    g2 = fs()
+    g2.build_faces(m.xyz, m.tets)
+    g2.assemble_csr(E, NU)
+    g2.apply_bc(m.dirichlet, m.loads.reshape(-1))
+    u2 = np.zeros(3 * m.n_nodes)
+    fsfem_pcg_solve(g2.ctx, u2, True, 1e-10, 7, allow_not_converged=True)
+    assert np.array_equal(u, u2)
+
+
+def test_invalid_arguments(fs):
+    from paper_2001_08849_b200 import FsfemError
+    m = config_mesh(1)
+    g = fs()
+    with pytest.raises(FsfemError) as e:
+        g.build_faces(m.xyz, m.tets[:0])
+    assert e.value.status == "INVALID_ARG"
+    g.build_faces(m.xyz, m.tets)
+    for bad in ((0.0, 0.3), (-1.0, 0.3), (E, 0.5), (E, -1.0)):
+        with pytest.raises(FsfemError) as e:
+            g.assemble_csr(*bad)
+        assert e.value.status == "INVALID_ARG"
+    g.assemble_csr(E, NU)
+    with pytest.raises(FsfemError) as e:
+        g.apply_bc(np.array([0, m.n_nodes], np.int32), m.loads.reshape(-1))
+    assert e.value.status == "INVALID_ARG"
+    with pytest.raises(FsfemError) as e:
+        g.apply_bc(m.dirichlet, m.loads.reshape(-1), 7)
+    assert e.value.status == "INVALID_ARG"
+
+
+def test_outputs_to_device_buffers(fs):
+    """get_csr / pcg_solve with CUDA tensors as outputs (no host round trip) equal the host path."""
+    import torch
+    from paper_2001_08849_b200 import fsfem_get_csr, fsfem_pcg_solve
+    m = config_mesh(2)
+    g = fs()
+    g.build_faces(m.xyz, m.tets)
+    g.assemble_csr(E, NU)
+    c = g.get_csr()
+    rp = torch.empty(g.n_rows + 1, dtype=torch.int64, device="cuda")
+    ci = torch.empty(g.nnz, dtype=torch.int32, device="cuda")
+    va = torch.empty(g.nnz, dtype=torch.float64, device="cuda")
+    fsfem_get_csr(g.ctx, rp, ci, va)
+    assert np.array_equal(rp.cpu().numpy(), c.row_ptr) and np.array_equal(ci.cpu().numpy(), c.col_idx)
+    assert np.array_equal(va.cpu().numpy(), c.vals)
+    g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+    u_h, _ = g.pcg_solve()
+    u_d = torch.zeros(3 * m.n_nodes, dtype=torch.float64, device="cuda")
+    fsfem_pcg_solve(g.ctx, u_d, True, 1e-10, 0)
+    assert np.array_equal(u_d.cpu().numpy(), u_h)
+
+
+def test_unreferenced_node_is_rejected_by_bcs(fs):
+    """A node in no tet has an empty row: the Jacobi preconditioner cannot be formed (BREAKDOWN
+    from apply_bc), unless the node is clamped."""
+    from paper_2001_08849_b200 import FsfemError
+    m = config_mesh(1)
+    xyz = np.vstack([m.xyz, [[20.0, 0.0, 0.0]]])
+    g = fs()
+    g.build_faces(xyz, m.tets)
+    g.assemble_csr(E, NU)
+    loads = np.zeros(3 * (m.n_nodes + 1))
+    loads[:3 * m.n_nodes] = m.loads.reshape(-1)
+    with pytest.raises(FsfemError) as e:
+        g.apply_bc(m.dirichlet, loads)
+    assert e.value.status == "BREAKDOWN"

@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
 //      that is a stored column of row i record (slot, s_K) and set the face's bit in the slot's
 //      mask (order-independent OR);
 //   B. lane = stored slot: walk the mask bits in ascending face order and add s_i s_K^T.
-// Summation order: off-diagonal blocks in ascending face id (as the generic path); the
-// diagonal block as per-lane sums over faces lane, lane+32, ... then a fixed warp tree.
+// Summation order (fixed, independent of timing): off-diagonal blocks in ascending face id, or
+// for rows with <= 16 stored blocks (the common case) ascending over the even then the odd
+// positions of each 32-face round; the diagonal block as per-lane sums over faces lane,
+// lane+32, ... then a fixed warp tree.
 constexpr int kRowWarps = 4;
 constexpr int kMaxTargets = 4;  // other field nodes of a face
 
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
     const int64_t P = sptr[il];
     const int ds = static_cast<int>(sptr[il + 1] - P);
     if (ds > 32) continue;  // generic path
+    const bool split = ds <= 16;
     sh_cols[w][lane] = lane < ds ? snbr[P + lane] : 0x7fffffff;
     sh_mask[w][lane] = 0u;
     const int64_t f0 = nf_ptr[il];
@@ -319,14 +322,17 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
         for (; t < kMaxTargets; ++t) sh_tslot[w][lane][t] = -1;
       }
       __syncwarp();
-      // ---- B: lane = stored slot
-      unsigned m = sh_mask[w][lane];
+      // ---- B: lane = stored slot; rows with <= 16 stored blocks give every slot 2 lanes, one for
+      // the even and one for the odd record positions (combined at the end in that order)
+      const int slot = split ? (lane & 15) : lane;
+      unsigned m = sh_mask[w][slot];
+      if (split) m &= (lane < 16) ? 0x55555555u : 0xAAAAAAAAu;
       while (m) {
         const int b = __ffs(m) - 1;
         m &= m - 1;
         int t = 0;
 #pragma unroll
-        for (int q = 1; q < kMaxTargets; ++q) t = (sh_tslot[w][b][q] == lane) ? q : t;
+        for (int q = 1; q < kMaxTargets; ++q) t = (sh_tslot[w][b][q] == slot) ? q : t;
         const double a0 = sh_si[w][b][0], a1 = sh_si[w][b][1], a2 = sh_si[w][b][2];
         const double c0 = sh_sk[w][b][t][0], c1 = sh_sk[w][b][t][1], c2 = sh_sk[w][b][t][2];
         M[0] = fma(a0, c0, M[0]);
@@ -342,6 +348,10 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
       __syncwarp();
       sh_mask[w][lane] = 0u;
       __syncwarp();
+    }
+    if (split) {  // slot s = (even records) + (odd records): lane s adds lane s+16's partial
+#pragma unroll
+      for (int q = 0; q < 9; ++q) M[q] += __shfl_down_sync(0xffffffffu, M[q], 16);
     }
     // diagonal block: fixed warp tree of the per-lane partial sums
 #pragma unroll

@@ -40,27 +40,44 @@ __global__ void k_scatter_node_tets(const int32_t* __restrict__ tets, int64_t nt
   }
 }
 
-// Stable rank sort of n ints in smem (src -> dst), then compaction of distinct values
-// (excluding kSentinel) back into src.  Returns the number of distinct values.  Warp-wide.
+// Distinct values of src[0..n) (kSentinel entries ignored), ascending, written back to the front
+// of src; returns their number.  Warp-wide.  The duplicates are removed first with an open-
+// addressing hash set in dst (the order of insertion does not matter: only set membership is
+// used), then the few distinct values are ranked (all distinct, so ranks are unique).
+// dst is scratch of capacity kCandCap.
 __device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int n, int lane) {
+  int H = 64;
+  while (H < 2 * n && H < kCandCap) H <<= 1;
+  for (int i = lane; i < H; i += 32) dst[i] = kSentinel;
+  __syncwarp();
   for (int i = lane; i < n; i += 32) {
     const int32_t v = src[i];
-    int r = 0;
-    for (int j = 0; j < n; ++j) {
-      const int32_t u = src[j];
-      r += (u < v || (u == v && j < i)) ? 1 : 0;
+    if (v == kSentinel) continue;
+    unsigned h = (static_cast<unsigned>(v) * 2654435761u) & (H - 1);
+    while (true) {
+      const int32_t old = atomicCAS(&dst[h], kSentinel, v);
+      if (old == kSentinel || old == v) break;
+      h = (h + 1) & (H - 1);
     }
-    dst[r] = v;
   }
   __syncwarp();
   int count = 0;
-  for (int c0 = 0; c0 < n; c0 += 32) {
-    const int i = c0 + lane;
-    const bool keep = i < n && dst[i] != kSentinel && (i == 0 || dst[i - 1] != dst[i]);
+  for (int c0 = 0; c0 < H; c0 += 32) {
+    const int32_t v = dst[c0 + lane];
+    const bool keep = v != kSentinel;
     const unsigned ball = __ballot_sync(0xffffffffu, keep);
-    if (keep) src[count + __popc(ball & ((1u << lane) - 1u))] = dst[i];
+    if (keep) src[count + __popc(ball & ((1u << lane) - 1u))] = v;
     count += __popc(ball);
   }
+  __syncwarp();
+  for (int i = lane; i < count; i += 32) {
+    const int32_t v = src[i];
+    int r = 0;
+    for (int j = 0; j < count; ++j) r += src[j] < v ? 1 : 0;
+    dst[r] = v;
+  }
+  __syncwarp();
+  for (int i = lane; i < count; i += 32) src[i] = dst[i];
   __syncwarp();
   return count;
 }

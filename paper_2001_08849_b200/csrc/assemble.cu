@@ -392,8 +392,15 @@ void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int
                           int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
                           cudaStream_t s) {
   if (nloc == 0) return;
-  const int g2 = static_cast<int>(std::min<int64_t>(ceil_div(nloc, kRowWarps), 64LL * num_sms()));
+  // Persistent grid of exactly the resident CTAs: warp w takes nodes w, w + W, ... so the nodes in
+  // flight form one contiguous window that slides forward; the field nodes of a face (which span
+  // less than two windows in a banded numbering) are then assembled close together in time and
+  // the face's record is re-read from L2, not DRAM.
   auto k2 = tet ? k_assemble_rows2<true> : k_assemble_rows2<false>;
+  static int per_sm[2] = {0, 0};
+  if (per_sm[tet] == 0) FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[tet], k2, kRowWarps * 32, 0));
+  const int g2 = static_cast<int>(
+      std::min<int64_t>(ceil_div(nloc, kRowWarps), static_cast<int64_t>(std::max(1, per_sm[tet])) * num_sms()));
   k2<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo, nloc,
                                                 lam, mu, vals);
   FS_LAUNCH_CHECK();

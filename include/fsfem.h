@@ -59,7 +59,7 @@ typedef struct fsfem_ctx fsfem_ctx; /* opaque */
 typedef struct {
   int64_t iterations;        /* PCG iterations performed (SpMVs inside the loop)            */
   int32_t converged;         /* 1 if ||r||_2 <= rel_tol * ||f||_2 was reached               */
-  int32_t _pad;
+  int32_t reordered;         /* 1 if the last build_faces renumbered the nodes internally     */
   double rel_residual;       /* recurrence residual ||r|| / ||f|| at exit                    */
   double true_rel_residual;  /* ||f - K u|| / ||f|| recomputed at exit                       */
   double t_faces_ms;         /* device time (CUDA events) of the last build_faces (S1)       */
@@ -114,6 +114,15 @@ fsfem_status fsfem_nccl_get_unique_id(void* out);
  * built"); the next fsfem_assemble_csr rebuilds the pattern.  Errors: INVALID_ARG. */
 typedef enum { FSFEM_METHOD_FS = 0, FSFEM_METHOD_FEM_T4 = 1 } fsfem_method;
 fsfem_status fsfem_set_method(fsfem_ctx* ctx, int method);
+
+/* Internal node order.  The SpMV and the assembly gather through L1/L2 and need a
+ * banded numbering; mode 0 (default, auto) renumbers the nodes internally in Morton order of their
+ * coordinates when the mean tet id span exceeds 16 N^(2/3), mode 1 always, mode 2 never.  Every
+ * input and output of the API stays in the caller's numbering (faces, CSR rows and columns, loads,
+ * Dirichlet ids, u, nodal stresses); only the internal storage order changes.  Single rank only
+ * (with several ranks the row partition is in the caller's numbering).  Takes effect at the next
+ * fsfem_build_faces.  Errors: INVALID_ARG. */
+fsfem_status fsfem_set_reorder(fsfem_ctx* ctx, int mode);
 
 /* S1: extract the unique faces of the mesh.
  *   xyz  [3*n_nodes] double, node coordinates (x, y, z per node)            (Node matrix)

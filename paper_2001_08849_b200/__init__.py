@@ -24,6 +24,7 @@ from .fsfem import (  # noqa: F401
     fsfem_pcg_solve,
     fsfem_recover_stress,
     fsfem_set_method,
+    fsfem_set_reorder,
     fsfem_spmv,
     fsfem_surface_loads,
     load_library,

@@ -2,6 +2,7 @@
 // host/device pointer handling, stage timing, PCG batching in CUDA graphs, NCCL row partition.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cmath>
@@ -37,6 +38,18 @@ void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* te
 void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, int64_t nrec,
                     const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
                     double* strain, double* stress, double* node_stress, double* node_vm, cudaStream_t s);
+double mean_tet_span_device(const int32_t* tets, int64_t nt, unsigned long long* d_tmp, cudaStream_t s);
+void morton_order_host(const double* d_xyz, int64_t nn, std::vector<int32_t>& iperm, cudaStream_t s);
+void perm_ids_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);
+void perm_ids_valid_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, int64_t nn,
+                           cudaStream_t s);
+void permute_rows_device(const int32_t* iperm, const double* in, double* out, int64_t nn, int w, bool to_internal,
+                         cudaStream_t s);
+void permute_rows_u8_device(const int32_t* iperm, const uint8_t* in, uint8_t* out, int64_t nn, bool to_internal,
+                            cudaStream_t s);
+void export_csr_user_device(const int32_t* perm, const int32_t* iperm, const Pattern& pat, const double* svals,
+                            int64_t* uptr, int64_t* udeg, void* scan_tmp, size_t scan_tmp_b, int64_t* row_ptr,
+                            int32_t* col_idx, double* vals, cudaStream_t s);
 void surface_loads_device(const int64_t* nd_ptr, const int32_t* nd_idx, bool tet, const int32_t* tet_face,
                           const int32_t* face_nodes, const int32_t* face_tet, const uint8_t* flag, const double* xyz,
                           int64_t n_lo, int64_t nloc, const double* t, double* loads, cudaStream_t s);
@@ -122,6 +135,15 @@ struct fsfem_ctx {
   int method = FSFEM_METHOD_FS;
   double E = 0, nu = 0;
   DevBuf<double> face_s, vals;
+  // internal node order (reorder.cu): perm user -> internal, iperm internal -> user
+  int reorder_mode = 0;  // 0 auto, 1 always, 2 never
+  bool reordered = false;
+  double mean_span = 0.0;
+  DevBuf<int32_t> perm, iperm, tmp_i;
+  DevBuf<double> tmp_d;
+  DevBuf<uint8_t> tmp_u8;
+  DevBuf<int64_t> exp_tmp;
+  DevBuf<unsigned long long> span_tmp;
   // bc / pcg
   DevBuf<double> f, dinv, x_full, r, p_full, q, part, all;
   DevBuf<double> rec_u, rec_strain, rec_stress, rec_nodes, rec_vm;  // stress recovery
@@ -167,6 +189,18 @@ void from_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   FS_CUDA(cudaMemcpyAsync(dst, src, bytes, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
 }
 
+template <typename T>
+void swap_buf(DevBuf<T>& a, DevBuf<T>& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.n, b.n);
+}
+
+// Node-indexed input (nn rows of w doubles, caller's numbering, host or device) -> device, internal
+// numbering.  Uses c->staging (must hold w*nn) when a permutation is needed.
+const double* node_in(fsfem_ctx* c, const double* user, int w, double* dst);
+// Device internal-numbered rows -> caller's array (host or device), caller's numbering.
+void node_out(fsfem_ctx* c, double* user, const double* internal, int64_t row0, int64_t nrows, int w);
+
 fsfem_status fail(fsfem_ctx* c, fsfem_status code, const std::string& msg) {
   if (c) c->err = msg;
   return code;
@@ -207,6 +241,28 @@ fsfem_status decode_flags(fsfem_ctx* c, unsigned long long v, const char* what) 
   c->err = std::string(what) + ": " + fsfem_status_string(static_cast<fsfem_status>(code)) + " at " + item + " " +
            std::to_string(idx);
   return static_cast<fsfem_status>(code);
+}
+
+const double* node_in(fsfem_ctx* c, const double* user, int w, double* dst) {
+  if (!c->reordered) {
+    to_device(dst, user, sizeof(double) * w * c->nn, c->stream);
+    return dst;
+  }
+  double* tmp = c->tmp_d.ensure(static_cast<size_t>(w) * c->nn);
+  to_device(tmp, user, sizeof(double) * w * c->nn, c->stream);
+  permute_rows_device(c->iperm.get(), tmp, dst, c->nn, w, true, c->stream);
+  return dst;
+}
+
+void node_out(fsfem_ctx* c, double* user, const double* internal, int64_t row0, int64_t nrows, int w) {
+  if (!user || nrows <= 0) return;
+  if (!c->reordered) {
+    from_device(user + static_cast<int64_t>(w) * row0, internal, sizeof(double) * w * nrows, c->stream);
+    return;
+  }
+  double* tmp = c->tmp_d.ensure(static_cast<size_t>(w) * c->nn);  // single rank: row0 = 0, nrows = nn
+  permute_rows_device(c->iperm.get(), internal, tmp, c->nn, w, false, c->stream);
+  from_device(user, tmp, sizeof(double) * w * c->nn, c->stream);
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -362,6 +418,14 @@ fsfem_status fsfem_set_method(fsfem_ctx* c, int method) {
   });
 }
 
+fsfem_status fsfem_set_reorder(fsfem_ctx* c, int mode) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (mode < 0 || mode > 2) return fail(c, FSFEM_ERR_INVALID_ARG, "reorder mode must be 0 (auto), 1 (always) or 2 (never)");
+    c->reorder_mode = mode;  // takes effect at the next fsfem_build_faces
+    return FSFEM_OK;
+  });
+}
+
 fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes, const int32_t* tets, int64_t n_tets,
                                int64_t* n_faces, int64_t* n_interior) {
   return guarded(c, [&]() -> fsfem_status {
@@ -387,6 +451,44 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
                        c->face_opp, c->tet_face, &nf, &ni, c->h_flags);
     fsfem_status s = decode_flags(c, c->h_flags[0], "build_faces");
     if (s != FSFEM_OK) return s;
+    // Internal node order (reorder.cu): renumber in Morton order when the caller's numbering is
+    // not banded (mean tet id span > 16 N^(2/3)), never with several ranks (the documented row
+    // partition is in the caller's numbering).
+    c->span_tmp.ensure(1);
+    c->mean_span = mean_tet_span_device(c->tets.get(), n_tets, c->span_tmp.get(), c->stream);
+    const bool want = c->nranks == 1 &&
+                      (c->reorder_mode == 1 ||
+                       (c->reorder_mode == 0 && c->mean_span > 16.0 * std::pow(static_cast<double>(n_nodes), 2.0 / 3.0)));
+    c->reordered = false;
+    if (want) {
+      std::vector<int32_t> hi_perm, h_perm(n_nodes);
+      morton_order_host(c->xyz.get(), n_nodes, hi_perm, c->stream);
+      for (int64_t k = 0; k < n_nodes; ++k) h_perm[hi_perm[k]] = static_cast<int32_t>(k);
+      c->iperm.ensure(n_nodes);
+      c->perm.ensure(n_nodes);
+      FS_CUDA(cudaMemcpyAsync(c->iperm.get(), hi_perm.data(), sizeof(int32_t) * n_nodes, cudaMemcpyHostToDevice,
+                              c->stream));
+      FS_CUDA(cudaMemcpyAsync(c->perm.get(), h_perm.data(), sizeof(int32_t) * n_nodes, cudaMemcpyHostToDevice,
+                              c->stream));
+      // the matrix path works on the renumbered mesh; faces keep their ids and order
+      DevBuf<double> xyz_i;
+      xyz_i.ensure(3 * n_nodes);
+      permute_rows_device(c->iperm.get(), c->xyz.get(), xyz_i.get(), n_nodes, 3, true, c->stream);
+      DevBuf<int32_t> tets_i, fn_i, fo_i;
+      tets_i.ensure(4 * n_tets);
+      fn_i.ensure(3 * nf);
+      fo_i.ensure(2 * nf);
+      perm_ids_device(c->perm.get(), c->tets.get(), tets_i.get(), 4 * n_tets, c->stream);
+      perm_ids_device(c->perm.get(), c->face_nodes.get(), fn_i.get(), 3 * nf, c->stream);
+      perm_ids_device(c->perm.get(), c->face_opp.get(), fo_i.get(), 2 * nf, c->stream);
+      FS_CUDA(cudaStreamSynchronize(c->stream));
+      swap_buf(c->xyz, xyz_i);
+      swap_buf(c->tets, tets_i);
+      swap_buf(c->face_nodes, fn_i);
+      swap_buf(c->face_opp, fo_i);
+      c->reordered = true;
+    }
+    c->rep.reordered = c->reordered ? 1 : 0;
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     FS_CUDA(cudaEventSynchronize(c->ev1));
     c->rep.t_faces_ms = elapsed(c->ev0, c->ev1);
@@ -403,9 +505,18 @@ fsfem_status fsfem_get_faces(const fsfem_ctx* cc, int32_t* face_nodes, int32_t* 
   fsfem_ctx* c = const_cast<fsfem_ctx*>(cc);
   return guarded(c, [&]() -> fsfem_status {
     if (c->stage < kFaces) return fail(c, FSFEM_ERR_STATE, "build_faces first");
-    from_device(face_nodes, c->face_nodes.get(), sizeof(int32_t) * 3 * c->nf, c->stream);
+    const int32_t* fn = c->face_nodes.get();
+    const int32_t* fo = c->face_opp.get();
+    if (c->reordered) {  // back to the caller's node ids (the sorted triples are restored exactly)
+      int32_t* t = c->tmp_i.ensure(5 * c->nf);
+      perm_ids_device(c->iperm.get(), fn, t, 3 * c->nf, c->stream);
+      perm_ids_device(c->iperm.get(), fo, t + 3 * c->nf, 2 * c->nf, c->stream);
+      fn = t;
+      fo = t + 3 * c->nf;
+    }
+    from_device(face_nodes, fn, sizeof(int32_t) * 3 * c->nf, c->stream);
     from_device(face_tet, c->face_tet.get(), sizeof(int32_t) * 2 * c->nf, c->stream);
-    from_device(face_opp, c->face_opp.get(), sizeof(int32_t) * 2 * c->nf, c->stream);
+    from_device(face_opp, fo, sizeof(int32_t) * 2 * c->nf, c->stream);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });
@@ -479,7 +590,17 @@ fsfem_status fsfem_get_csr(const fsfem_ctx* cc, int64_t* row_ptr, int32_t* col_i
     if (row_ptr) d_rp = is_device_ptr(row_ptr) ? row_ptr : rp.ensure(nr + 1);
     if (col_idx) d_ci = is_device_ptr(col_idx) ? col_idx : ci.ensure(std::max<int64_t>(nnz, 1));
     if (vals) d_vo = is_device_ptr(vals) ? vals : vo.ensure(std::max<int64_t>(nnz, 1));
-    if (c->nloc > 0) export_csr_device(c->pat, c->vals.get(), d_rp, d_ci, d_vo, c->stream);
+    if (c->nloc > 0 && c->reordered) {
+      int64_t* t = c->exp_tmp.ensure(2 * (c->nn + 1));
+      DevBuf<unsigned char> sc;
+      const size_t tb = scan_tmp_bytes(c->nn + 1);
+      sc.ensure(tb);
+      export_csr_user_device(c->perm.get(), c->iperm.get(), c->pat, c->vals.get(), t, t + c->nn + 1, sc.get(), tb, d_rp,
+                             d_ci, d_vo, c->stream);
+      FS_CUDA(cudaStreamSynchronize(c->stream));
+    } else if (c->nloc > 0) {
+      export_csr_device(c->pat, c->vals.get(), d_rp, d_ci, d_vo, c->stream);
+    }
     else if (d_rp) FS_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), c->stream));
     if (row_ptr && d_rp != row_ptr) from_device(row_ptr, d_rp, sizeof(int64_t) * (nr + 1), c->stream);
     if (col_idx && d_ci != col_idx) from_device(col_idx, d_ci, sizeof(int32_t) * nnz, c->stream);
@@ -504,8 +625,13 @@ fsfem_status fsfem_apply_bc(fsfem_ctx* c, const int32_t* dirichlet, int64_t n_di
     c->staging.ensure(3 * c->nn);
     c->staging_i.ensure(std::max<int64_t>(n_dir, 1));
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
-    to_device(c->staging.get(), loads, sizeof(double) * 3 * c->nn, c->stream);
+    node_in(c, loads, 3, c->staging.get());
     to_device(c->staging_i.get(), dirichlet, sizeof(int32_t) * n_dir, c->stream);
+    if (c->reordered && n_dir > 0) {  // ids out of range are left for apply_bc to report
+      int32_t* t = c->tmp_i.ensure(n_dir);
+      FS_CUDA(cudaMemcpyAsync(t, c->staging_i.get(), sizeof(int32_t) * n_dir, cudaMemcpyDeviceToDevice, c->stream));
+      perm_ids_valid_device(c->perm.get(), t, c->staging_i.get(), n_dir, c->nn, c->stream);
+    }
     apply_bc_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.sdiag.get(), c->n_lo, c->nloc, c->nn, c->staging_i.get(),
                     n_dir, c->staging.get(), mode, penalty_scale, c->vals.get(), c->f.get(), c->dinv.get(),
                     c->fixed.get(), c->flags.get(), c->stream);
@@ -527,9 +653,9 @@ fsfem_status fsfem_spmv(fsfem_ctx* c, const double* p, double* q) {
     const int64_t nfull = 3 * c->chunk * c->nranks;
     c->x_full.ensure(nfull);
     c->q.ensure(std::max<int64_t>(3 * c->nloc, 1));
-    to_device(c->x_full.get(), p, sizeof(double) * 3 * c->nn, c->stream);
+    node_in(c, p, 3, c->x_full.get());
     launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
-    from_device(q + 3 * c->n_lo, c->q.get(), sizeof(double) * 3 * c->nloc, c->stream);
+    node_out(c, q, c->q.get(), c->n_lo, c->nloc, 3);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });
@@ -566,7 +692,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     double* own_p = c->p_full.get() + 3 * c->n_lo;
     const double* q0 = nullptr;
     if (!u0_is_zero) {
-      to_device(c->x_full.get(), u, sizeof(double) * nglob, c->stream);
+      node_in(c, u, 3, c->x_full.get());
       launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
       q0 = c->q.get();
     }
@@ -622,7 +748,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
     launch_resid(c->f.get(), c->q.get(), n, st, c->part.get(), c->stream);
     if (c->nranks > 1) combine(c, 3);
-    from_device(u, c->x_full.get(), sizeof(double) * nglob, c->stream);
+    node_out(c, u, c->x_full.get(), 0, c->nn, 3);
     FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
     FS_CUDA(cudaStreamSynchronize(c->stream));
     (void)own_x;
@@ -654,23 +780,21 @@ fsfem_status fsfem_recover_stress(fsfem_ctx* c, const double* u, double* strain,
     const double lam = c->E * c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
     const double mu = c->E / (2.0 * (1.0 + c->nu));
     c->rec_u.ensure(3 * c->nn);
-    to_device(c->rec_u.get(), u, sizeof(double) * 3 * c->nn, c->stream);
+    node_in(c, u, 3, c->rec_u.get());
     double* d_stress = (stress && is_device_ptr(stress)) ? stress : c->rec_stress.ensure(6 * nd);
     double* d_strain = nullptr;
     if (strain) d_strain = is_device_ptr(strain) ? strain : c->rec_strain.ensure(6 * nd);
     double* d_nodes = nullptr;
-    if (node_stress)
-      d_nodes = is_device_ptr(node_stress) ? node_stress + 6 * c->n_lo : c->rec_nodes.ensure(std::max<int64_t>(6 * c->nloc, 1));
+    if (node_stress) d_nodes = c->rec_nodes.ensure(std::max<int64_t>(6 * c->nloc, 1));
     double* d_vm = nullptr;
-    if (node_vm) d_vm = is_device_ptr(node_vm) ? node_vm + c->n_lo : c->rec_vm.ensure(std::max<int64_t>(c->nloc, 1));
+    if (node_vm) d_vm = c->rec_vm.ensure(std::max<int64_t>(c->nloc, 1));
     recover_device(tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet, c->face_s.get(), nd,
                    c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->nloc, c->rec_u.get(), lam, mu, d_strain, d_stress,
                    d_nodes, d_vm, c->stream);
     if (stress && d_stress != stress) from_device(stress, d_stress, sizeof(double) * 6 * nd, c->stream);
     if (strain && d_strain != strain) from_device(strain, d_strain, sizeof(double) * 6 * nd, c->stream);
-    if (node_stress && !is_device_ptr(node_stress))
-      from_device(node_stress + 6 * c->n_lo, d_nodes, sizeof(double) * 6 * c->nloc, c->stream);
-    if (node_vm && !is_device_ptr(node_vm)) from_device(node_vm + c->n_lo, d_vm, sizeof(double) * c->nloc, c->stream);
+    if (node_stress) node_out(c, node_stress, d_nodes, c->n_lo, c->nloc, 6);
+    if (node_vm) node_out(c, node_vm, d_vm, c->n_lo, c->nloc, 1);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });
@@ -681,12 +805,18 @@ fsfem_status fsfem_surface_loads(fsfem_ctx* c, const uint8_t* node_flag, const d
     if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first (uses its node lists)");
     if (!node_flag || !traction || !loads) return fail(c, FSFEM_ERR_INVALID_ARG, "null argument");
     c->fixed.ensure(c->nn);
-    to_device(c->fixed.get(), node_flag, c->nn, c->stream);
-    double* d_loads = is_device_ptr(loads) ? loads + 3 * c->n_lo : c->rec_u.ensure(std::max<int64_t>(3 * c->nloc, 1));
+    if (c->reordered) {
+      uint8_t* t = c->tmp_u8.ensure(c->nn);
+      to_device(t, node_flag, c->nn, c->stream);
+      permute_rows_u8_device(c->iperm.get(), t, c->fixed.get(), c->nn, true, c->stream);
+    } else {
+      to_device(c->fixed.get(), node_flag, c->nn, c->stream);
+    }
+    double* d_loads = c->rec_u.ensure(std::max<int64_t>(3 * c->nn, 1));
     surface_loads_device(c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->method == FSFEM_METHOD_FEM_T4, c->tet_face.get(),
                          c->face_nodes.get(), c->face_tet.get(), c->fixed.get(), c->xyz.get(), c->n_lo, c->nloc,
                          traction, d_loads, c->stream);
-    if (!is_device_ptr(loads)) from_device(loads + 3 * c->n_lo, d_loads, sizeof(double) * 3 * c->nloc, c->stream);
+    node_out(c, loads, d_loads, c->n_lo, c->nloc, 3);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });

@@ -1,0 +1,225 @@
+// Internal node renumbering for locality (DESIGN.md §5 "node order").
+//
+// The SpMV and the assembly gather x and face records through L1/L2, so they rely on the node
+// numbering being banded (neighbours have nearby ids).  A mesh whose numbering is not (e.g. a
+// random relabelling, BASELINE configs[4]) is renumbered internally in Morton order of its node
+// coordinates; every API output stays in the caller's numbering.  perm: user -> internal,
+// iperm: internal -> user.  Nothing here changes what is computed, only where it is stored.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "pattern.cuh"
+
+namespace fsfem {
+
+namespace {
+
+// Sum over tets of (max id - min id): the numbering's bandwidth (integer sum: exact).
+__global__ void k_tet_span(const int4* __restrict__ tets, int64_t nt, unsigned long long* __restrict__ out) {
+  unsigned long long s = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v = tets[t];
+    const int lo = min(min(v.x, v.y), min(v.z, v.w)), hi = max(max(v.x, v.y), max(v.z, v.w));
+    s += static_cast<unsigned long long>(hi - lo);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+__global__ void k_perm_ids(const int32_t* __restrict__ perm, const int32_t* __restrict__ in, int32_t* __restrict__ out,
+                           int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = in[k];
+    out[k] = v < 0 ? v : perm[v];
+  }
+}
+
+__global__ void k_perm_ids_valid(const int32_t* __restrict__ perm, const int32_t* __restrict__ in,
+                                 int32_t* __restrict__ out, int64_t n, int64_t nn) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = in[k];
+    out[k] = (v >= 0 && v < nn) ? perm[v] : v;  // invalid ids stay invalid (reported downstream)
+  }
+}
+
+// out[w*i + a] = in[w*iperm[i] + a] (to_internal) or out[w*iperm[i] + a] = in[w*i + a].
+template <typename T>
+__global__ void k_permute_rows(const int32_t* __restrict__ iperm, const T* __restrict__ in, T* __restrict__ out,
+                               int64_t nn, int w, bool to_internal) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nn * w; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / w, a = k - i * w;
+    const int64_t u = iperm[i];
+    if (to_internal) out[k] = in[w * u + a];
+    else out[w * u + a] = in[k];
+  }
+}
+
+// Public CSR in the caller's numbering from the (internally numbered) symmetric storage.
+// Warp per user node I: its internal row i = perm[I]; the neighbours are mapped to user ids and
+// ranked (ascending user column order), then each lane emits its blocks like k_export_csr.
+constexpr int kExpWarps = 4;
+constexpr int kExpCap = 1024;
+__global__ void __launch_bounds__(kExpWarps * 32) k_export_csr_user(
+    const int32_t* __restrict__ perm, const int32_t* __restrict__ iperm, const int64_t* __restrict__ node_ptr,
+    const int32_t* __restrict__ nbr, const int64_t* __restrict__ sptr, const int32_t* __restrict__ sdiag,
+    const int64_t* __restrict__ tptr, const int2* __restrict__ tlist, const double* __restrict__ svals,
+    const int64_t* __restrict__ uptr /* user-order node offsets */, int64_t nn, int64_t* __restrict__ row_ptr,
+    int32_t* __restrict__ col_idx, double* __restrict__ vals) {
+  __shared__ int32_t ucol[kExpWarps][kExpCap];
+  __shared__ int32_t order[kExpWarps][kExpCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t I = blockIdx.x * (int64_t)kExpWarps + w; I < nn; I += (int64_t)gridDim.x * kExpWarps) {
+    const int64_t i = perm[I];
+    const int64_t P = node_ptr[i];
+    const int deg = static_cast<int>(node_ptr[i + 1] - P);
+    const int m = 3 * deg;
+    const int64_t PU = uptr[I];
+    if (row_ptr && lane < 3) row_ptr[3 * I + lane] = 9 * PU + lane * m;
+    if (row_ptr && I == nn - 1 && lane == 0) row_ptr[3 * nn] = 9 * uptr[nn];
+    for (int s = lane; s < deg; s += 32) ucol[w][s] = iperm[nbr[P + s]];
+    __syncwarp();
+    for (int s = lane; s < deg; s += 32) {  // rank of each neighbour among the user ids (distinct)
+      const int32_t v = ucol[w][s];
+      int r = 0;
+      for (int t = 0; t < deg; ++t) r += ucol[w][t] < v ? 1 : 0;
+      order[w][r] = s;
+    }
+    __syncwarp();
+    const int h = sdiag[i];
+    const int ntr = static_cast<int>(tptr[i + 1] - tptr[i]);
+    for (int r = lane; r < deg; r += 32) {
+      const int s = order[w][r];  // internal slot of the r-th user column
+      const int32_t j = ucol[w][s];
+      if (col_idx) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) col_idx[9 * PU + a * m + 3 * r + c] = 3 * j + c;
+      }
+      if (!vals) continue;
+      double blk[9];
+      if (s >= h && s < h + ntr) {
+        const double* src = svals + 9 * static_cast<int64_t>(tlist[tptr[i] + (s - h)].x);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) blk[3 * a + c] = src[3 * c + a];
+      } else {
+        const double* src = svals + 9 * (sptr[i] + (s < h ? s : s - ntr));
+#pragma unroll
+        for (int q = 0; q < 9; ++q) blk[q] = src[q];
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vals[9 * PU + a * m + 3 * r + c] = blk[3 * a + c];
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_user_degrees(const int32_t* __restrict__ perm, const int64_t* __restrict__ node_ptr, int64_t nn,
+                               int64_t* __restrict__ deg) {
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < nn; I += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = perm[I];
+    deg[I] = node_ptr[i + 1] - node_ptr[i];
+  }
+}
+
+int grid_for(int64_t n) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 16LL * num_sms())));
+}
+
+uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
+  v &= 0x1fffffULL;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+}  // namespace
+
+// Mean tet id span (user numbering), exact.
+double mean_tet_span_device(const int32_t* tets, int64_t nt, unsigned long long* d_tmp, cudaStream_t s) {
+  FS_CUDA(cudaMemsetAsync(d_tmp, 0, sizeof(unsigned long long), s));
+  k_tet_span<<<grid_for(nt), 256, 0, s>>>(reinterpret_cast<const int4*>(tets), nt, d_tmp);
+  FS_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  FS_CUDA(cudaMemcpyAsync(&h, d_tmp, sizeof(h), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  return static_cast<double>(h) / static_cast<double>(std::max<int64_t>(nt, 1));
+}
+
+// Morton order of the nodes (host; once per mesh): iperm[k] = user id of the k-th node.
+void morton_order_host(const double* d_xyz, int64_t nn, std::vector<int32_t>& iperm, cudaStream_t s) {
+  std::vector<double> x(3 * nn);
+  FS_CUDA(cudaMemcpyAsync(x.data(), d_xyz, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  double lo[3] = {x[0], x[1], x[2]}, hi[3] = {x[0], x[1], x[2]};
+  for (int64_t i = 0; i < nn; ++i)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], x[3 * i + a]);
+      hi[a] = std::max(hi[a], x[3 * i + a]);
+    }
+  // one common cell size (the beam is long and thin: per-axis scaling would distort the curve)
+  const double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+  const double sc = ext > 0 ? 2097151.0 / ext : 0.0;
+  std::vector<std::pair<uint64_t, int32_t>> key(nn);
+  for (int64_t i = 0; i < nn; ++i) {
+    uint64_t k = 0;
+    for (int a = 0; a < 3; ++a) k |= spread3(static_cast<uint64_t>((x[3 * i + a] - lo[a]) * sc)) << a;
+    key[i] = {k, static_cast<int32_t>(i)};
+  }
+  std::sort(key.begin(), key.end());
+  iperm.resize(nn);
+  for (int64_t k = 0; k < nn; ++k) iperm[k] = key[k].second;
+}
+
+void perm_ids_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_perm_ids<<<grid_for(n), 256, 0, s>>>(perm, in, out, n);
+  FS_LAUNCH_CHECK();
+}
+
+void perm_ids_valid_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, int64_t nn,
+                           cudaStream_t s) {
+  if (n <= 0) return;
+  k_perm_ids_valid<<<grid_for(n), 256, 0, s>>>(perm, in, out, n, nn);
+  FS_LAUNCH_CHECK();
+}
+
+void permute_rows_device(const int32_t* iperm, const double* in, double* out, int64_t nn, int w, bool to_internal,
+                         cudaStream_t s) {
+  if (nn <= 0) return;
+  k_permute_rows<double><<<grid_for(nn * w), 256, 0, s>>>(iperm, in, out, nn, w, to_internal);
+  FS_LAUNCH_CHECK();
+}
+
+void permute_rows_u8_device(const int32_t* iperm, const uint8_t* in, uint8_t* out, int64_t nn, bool to_internal,
+                            cudaStream_t s) {
+  if (nn <= 0) return;
+  k_permute_rows<uint8_t><<<grid_for(nn), 256, 0, s>>>(iperm, in, out, nn, 1, to_internal);
+  FS_LAUNCH_CHECK();
+}
+
+void export_csr_user_device(const int32_t* perm, const int32_t* iperm, const Pattern& pat, const double* svals,
+                            int64_t* uptr /*[nn+1] scratch*/, int64_t* udeg /*[nn+1] scratch*/, void* scan_tmp,
+                            size_t scan_tmp_b, int64_t* row_ptr, int32_t* col_idx, double* vals, cudaStream_t s) {
+  const int64_t nn = pat.nloc;
+  k_user_degrees<<<grid_for(nn), 256, 0, s>>>(perm, pat.node_ptr.get(), nn, udeg);
+  FS_LAUNCH_CHECK();
+  exclusive_scan_i64(udeg, uptr, nn, s, scan_tmp, scan_tmp_b);
+  const int g = static_cast<int>(std::min<int64_t>(ceil_div(nn, kExpWarps), 32LL * num_sms()));
+  k_export_csr_user<<<std::max(g, 1), kExpWarps * 32, 0, s>>>(perm, iperm, pat.node_ptr.get(), pat.nbr.get(),
+                                                              pat.sptr.get(), pat.sdiag.get(), pat.tptr.get(),
+                                                              pat.tlist.get(), svals, uptr, nn, row_ptr, col_idx,
+                                                              vals);
+  FS_LAUNCH_CHECK();
+}
+
+}  // namespace fsfem

@@ -25,14 +25,14 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
 # Every symbol include/fsfem.h declares (checked by tests/test_abi.py).
 METHOD_FS, METHOD_FEM_T4 = 0, 1
 
-EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method",
+EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method", "fsfem_set_reorder",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
            "fsfem_surface_loads"]
 
 
 class FsfemReport(ctypes.Structure):
-    _fields_ = [("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("_pad", ctypes.c_int32),
+    _fields_ = [("iterations", ctypes.c_int64), ("converged", ctypes.c_int32), ("reordered", ctypes.c_int32),
                 ("rel_residual", ctypes.c_double), ("true_rel_residual", ctypes.c_double),
                 ("t_faces_ms", ctypes.c_double), ("t_symbolic_ms", ctypes.c_double),
                 ("t_numeric_ms", ctypes.c_double), ("t_bc_ms", ctypes.c_double), ("t_pcg_ms", ctypes.c_double),
@@ -42,7 +42,7 @@ class FsfemReport(ctypes.Structure):
                 ("assembly_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "_pad"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class FsfemError(RuntimeError):
@@ -71,6 +71,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_last_error": (ctypes.c_char_p, [P]),
         "fsfem_comm_init": (I, [P, P, I, I]),
         "fsfem_set_method": (I, [P, I]),
+        "fsfem_set_reorder": (I, [P, I]),
         "fsfem_nccl_get_unique_id": (I, [P]),
         "fsfem_build_faces": (I, [P, P, I64, P, I64, P, P]),
         "fsfem_get_faces": (I, [P, P, P, P]),
@@ -157,6 +158,11 @@ def fsfem_comm_init(ctx, unique_id: bytes | None, rank: int, nranks: int) -> Non
 
 def fsfem_set_method(ctx, method: int) -> None:
     _raise(ctx, load_library().fsfem_set_method(ctx, int(method)))
+
+
+def fsfem_set_reorder(ctx, mode: int) -> None:
+    """0 auto (default), 1 always, 2 never (include/fsfem.h)."""
+    _raise(ctx, load_library().fsfem_set_reorder(ctx, int(mode)))
 
 
 def fsfem_build_faces(ctx, xyz, tets):
@@ -255,6 +261,9 @@ class FsFem:
 
     def comm_init(self, unique_id: bytes | None, rank: int, nranks: int):
         fsfem_comm_init(self.ctx, unique_id, rank, nranks)
+
+    def set_reorder(self, mode: int):
+        fsfem_set_reorder(self.ctx, mode)
 
     def set_method(self, method: int):
         fsfem_set_method(self.ctx, method)

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--pcg-iters", type=int, default=64)
     ap.add_argument("--reassemble", type=int, default=2)
+    ap.add_argument("--reorder", type=int, default=0, help="0 auto, 1 always, 2 never")
     a = ap.parse_args()
     import torch
     from fsfem_inputs import config_mesh
@@ -24,6 +25,7 @@ def main():
     m = config_mesh(a.config)
     dev = torch.device("cuda", 0)
     g = FsFem(device=0, stream=torch.cuda.current_stream().cuda_stream)
+    g.set_reorder(a.reorder)
     xyz = torch.from_numpy(m.xyz).to(dev)
     tets = torch.from_numpy(m.tets).to(dev)
     dirichlet = torch.from_numpy(m.dirichlet).to(dev)
@@ -39,7 +41,8 @@ def main():
         rep = g.report()
         rep["status"] = str(e)[:60]
     torch.cuda.synchronize()
-    print({k: rep[k] for k in ("iterations", "status", "t_numeric_ms", "t_pcg_ms", "t_spmv_ms", "spmv_launches")})
+    print({k: rep[k] for k in ("iterations", "status", "t_numeric_ms", "t_pcg_ms", "t_spmv_ms", "spmv_launches",
+                               "reordered", "t_faces_ms", "t_symbolic_ms")})
 
 
 if __name__ == "__main__":

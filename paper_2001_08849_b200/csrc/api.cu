@@ -29,13 +29,14 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
 void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr, int32_t* col_idx, double* vals,
                        cudaStream_t s);
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
-                   const int32_t* face_opp, int64_t nf, double* face_s, cudaStream_t s);
+                   const int32_t* face_opp, int64_t nf, double* face_s, double* face_V, cudaStream_t s);
 void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
                           const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
                           int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
                           cudaStream_t s);
-void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, cudaStream_t s);
-void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, int64_t nrec,
+void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s);
+void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, const double* rec_V,
+                    int64_t nrec,
                     const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
                     double* strain, double* stress, double* node_stress, double* node_vm, cudaStream_t s);
 double mean_tet_span_device(const int32_t* tets, int64_t nt, unsigned long long* d_tmp, cudaStream_t s);
@@ -134,7 +135,7 @@ struct fsfem_ctx {
   // numeric
   int method = FSFEM_METHOD_FS;
   double E = 0, nu = 0;
-  DevBuf<double> face_s, vals;
+  DevBuf<double> face_s, face_V, vals;  // assembly records (144 B per face / tet) and volumes
   // internal node order (reorder.cu): perm user -> internal, iperm internal -> user
   int reorder_mode = 0;  // 0 auto, 1 always, 2 never
   bool reordered = false;
@@ -539,7 +540,8 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       FS_CUDA(cudaEventSynchronize(c->ev1));
       c->rep.t_symbolic_ms = elapsed(c->ev0, c->ev1);
       c->vals.ensure(9 * c->pat.nsb + 2);  // + slack for the SpMV bulk copies (pattern.cuh)
-      c->face_s.ensure(16 * std::max(c->nf, c->nt));
+      c->face_s.ensure(18 * std::max(c->nf, c->nt));
+      c->face_V.ensure(std::max(c->nf, c->nt));
       c->have_pattern = true;
       drop_graph(c);
     }
@@ -547,13 +549,13 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     const double mu = E / (2.0 * (1.0 + nu));
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
     if (c->method == FSFEM_METHOD_FEM_T4) {
-      tet_s_device(c->xyz.get(), c->tets.get(), c->nt, c->face_s.get(), c->stream);
+      tet_s_device(c->xyz.get(), c->tets.get(), c->nt, c->face_s.get(), c->face_V.get(), c->stream);
       assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(),
                            c->tets.get(), nullptr, c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(),
                            c->pat.max_row_blocks, true, c->stream);
     } else {
       face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
-                    c->face_s.get(), c->stream);
+                    c->face_s.get(), c->face_V.get(), c->stream);
       assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(),
                            c->face_nodes.get(), c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu,
                            c->vals.get(), c->pat.max_row_blocks, false, c->stream);
@@ -788,7 +790,8 @@ fsfem_status fsfem_recover_stress(fsfem_ctx* c, const double* u, double* strain,
     if (node_stress) d_nodes = c->rec_nodes.ensure(std::max<int64_t>(6 * c->nloc, 1));
     double* d_vm = nullptr;
     if (node_vm) d_vm = c->rec_vm.ensure(std::max<int64_t>(c->nloc, 1));
-    recover_device(tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet, c->face_s.get(), nd,
+    recover_device(tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet, c->face_s.get(),
+                   c->face_V.get(), nd,
                    c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->nloc, c->rec_u.get(), lam, mu, d_strain, d_stress,
                    d_nodes, d_vm, c->stream);
     if (stress && d_stress != stress) from_device(stress, d_stress, sizeof(double) * 6 * nd, c->stream);

@@ -18,7 +18,14 @@ namespace fsfem {
 
 namespace {
 
-constexpr int kFaceStride = 16;  // doubles per face: 5 field nodes x 3 + V_f
+// Assembly record of a face (FS) or tet (FEM-T4), 144 bytes = 9 x 16 B:
+//   doubles [0, 15): s_K for the 5 field nodes K (tets: 4; the 5th zero);
+//   bytes [120, 140): int32 field node ids (a, b, c, opp0, opp1) (tets: 4 nodes, -1); 4 B pad.
+// The domain volumes V_k live in a separate array (strain recovery).
+constexpr int kRec = 18;  // doubles per record
+__device__ __forceinline__ const int32_t* rec_field(const double* rec) {
+  return reinterpret_cast<const int32_t*>(rec + 15);
+}
 
 __device__ __forceinline__ void load3(const double* __restrict__ xyz, int32_t v, double& x, double& y, double& z) {
   x = xyz[3 * v];
@@ -31,8 +38,8 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
                                                 const int32_t* __restrict__ face_nodes,
                                                 const int32_t* __restrict__ face_tet,
                                                 const int32_t* __restrict__ face_opp, int64_t nf,
-                                                double* __restrict__ face_s) {
-  __shared__ __align__(16) double stage[256 * kFaceStride];
+                                                double* __restrict__ face_s, double* __restrict__ face_V) {
+  __shared__ __align__(16) double stage[256 * kRec];
   // uniform trip count per block (every thread reaches the __syncthreads)
   for (int64_t fb0 = blockIdx.x * (int64_t)blockDim.x; fb0 < nf; fb0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = fb0 + threadIdx.x;
@@ -94,51 +101,34 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
       }
     }
     const double rs = 1.0 / sqrt(Vf);
-    // stage the 16 doubles of each face of the block in shared memory, then store coalesced
-    double* st = stage + kFaceStride * threadIdx.x;
+    // stage the record of each face of the block in shared memory, then store coalesced
+    double* st = stage + kRec * threadIdx.x;
 #pragma unroll
     for (int K = 0; K < 5; ++K) {
       st[3 * K] = g[K][0] * rs;
       st[3 * K + 1] = g[K][1] * rs;
       st[3 * K + 2] = g[K][2] * rs;
     }
-    st[15] = Vf;
+    int32_t* sfld = reinterpret_cast<int32_t*>(st + 15);
+#pragma unroll
+    for (int K = 0; K < 5; ++K) sfld[K] = fld[K];
+    sfld[5] = 0;
+    if (valid) face_V[f] = Vf;
     __syncthreads();
     const int64_t fb = f - threadIdx.x;  // first face of this block-iteration
     const int nvalid = static_cast<int>(nf - fb < (int64_t)blockDim.x ? nf - fb : (int64_t)blockDim.x);
-    double2* dst = reinterpret_cast<double2*>(face_s + kFaceStride * fb);
+    double2* dst = reinterpret_cast<double2*>(face_s + kRec * fb);
     const double2* src = reinterpret_cast<const double2*>(stage);
-    for (int k = threadIdx.x; k < nvalid * (kFaceStride / 2); k += blockDim.x) __stcs(dst + k, src[k]);
+    for (int k = threadIdx.x; k < nvalid * (kRec / 2); k += blockDim.x) dst[k] = src[k];
     __syncthreads();
-  }
-}
-
-// Field nodes of assembly record r: FS face r = (a, b, c, opp0, opp1) (opp1 = -1 exterior);
-// FEM-T4 tet r = its 4 nodes and -1.
-template <bool kTet>
-__device__ __forceinline__ void record_field(const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
-                                             int64_t r, int32_t (&fld)[5]) {
-  if (kTet) {
-    const int4 v = reinterpret_cast<const int4*>(rec_a)[r];
-    fld[0] = v.x;
-    fld[1] = v.y;
-    fld[2] = v.z;
-    fld[3] = v.w;
-    fld[4] = -1;
-  } else {
-    fld[0] = rec_a[3 * r];
-    fld[1] = rec_a[3 * r + 1];
-    fld[2] = rec_a[3 * r + 2];
-    fld[3] = rec_b[2 * r];
-    fld[4] = rec_b[2 * r + 1];
   }
 }
 
 // FEM-T4 (PAPER.md:531 and Table 4's FEM-T4 column): per tet
 // s_I = sqrt(V_e) grad N_I (I = 0..3), so that V_e (B_I^T c B_J) = lam M + mu M^T + mu tr(M) I
-// with M = s_I s_J^T, exactly the M-form of the faces.  Record layout as face_s (stride 16).
+// with M = s_I s_J^T, exactly the M-form of the faces.  Same 144-byte record as the faces.
 __global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, const int32_t* __restrict__ tets,
-                                               int64_t nt, double* __restrict__ tet_s) {
+                                               int64_t nt, double* __restrict__ tet_s, double* __restrict__ tet_V) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
     const int4 v = reinterpret_cast<const int4*>(tets)[t];
     double x0, y0, z0, x1, y1, z1, x2, y2, z2, x3, y3, z3;
@@ -162,7 +152,7 @@ __global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, c
     const double det = e1x * g[1][0] + e1y * g[1][1] + e1z * g[1][2];
     const double V = fabs(det) * (1.0 / 6.0);
     const double sc = sqrt(V) / det;  // grad N_q = (cross product) / det
-    double* out = tet_s + kFaceStride * t;
+    double* out = tet_s + kRec * t;
 #pragma unroll
     for (int h = 0; h < 3; ++h) {
       const double a = g[1][h] * sc, b = g[2][h] * sc, c = g[3][h] * sc;
@@ -171,8 +161,15 @@ __global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, c
       out[3 * 3 + h] = c;
       out[h] = -(a + b + c);
     }
-    out[12] = V;
-    out[13] = out[14] = out[15] = 0.0;
+    out[12] = out[13] = out[14] = 0.0;
+    int32_t* ofld = reinterpret_cast<int32_t*>(out + 15);
+    ofld[0] = v.x;
+    ofld[1] = v.y;
+    ofld[2] = v.z;
+    ofld[3] = v.w;
+    ofld[4] = -1;
+    ofld[5] = 0;
+    tet_V[t] = V;
   }
 }
 
@@ -203,8 +200,9 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
       for (int q = 0; q < 9; ++q) M[q] = 0.0;
       for (int64_t k = f0; k < f1; ++k) {
         const int32_t f = nf_idx[k];
-        int32_t fld[5];
-        record_field<kTet>(face_nodes, face_opp, f, fld);
+        const double* sf = face_s + kRec * static_cast<int64_t>(f);
+        const int32_t* rf = rec_field(sf);
+        const int32_t fld[5] = {rf[0], rf[1], rf[2], rf[3], rf[4]};
         int pi = 0, pj = -1;
 #pragma unroll
         for (int K = 0; K < 5; ++K) {
@@ -212,7 +210,6 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
           pj = (fld[K] == j) ? K : pj;
         }
         if (pj >= 0) {
-          const double* sf = face_s + kFaceStride * f;
           const double si0 = sf[3 * pi], si1 = sf[3 * pi + 1], si2 = sf[3 * pi + 2];
           const double sj0 = sf[3 * pj], sj1 = sf[3 * pj + 1], sj2 = sf[3 * pj + 2];
           M[0] = fma(si0, sj0, M[0]);
@@ -243,9 +240,11 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
 
 
 // Fast path, warp per own node i with <= 32 stored blocks (diagonal + j > i + halo j < n_lo).
-// Rounds of 32 faces of F(i) (ascending):
-//   A. lane = face: load the face's field nodes and s vectors (all lanes' loads in flight at
-//      once), add s_i s_i^T to the lane's diagonal partial sum, and for every other field node
+// Rounds of 32 records (faces of F(i), or tets for FEM-T4; ascending):
+//   load: the warp copies the round's 32 records (144 B each) into shared memory with
+//      coalesced 16-byte loads (9 warp instructions, each covering ~4 records), instead of
+//      each lane gathering its own record piece by piece (the L1 wavefront bound);
+//   A. lane = face: add s_i s_i^T to the lane's diagonal partial sum, and for every other field node
 //      that is a stored column of row i record (slot, s_K) and set the face's bit in the slot's
 //      mask (order-independent OR);
 //   B. lane = stored slot: walk the mask bits in ascending face order and add s_i s_K^T.
@@ -261,11 +260,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
     const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
     const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
     const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals) {
+  __shared__ __align__(16) double sh_rec[kRowWarps][32][kRec];
   __shared__ int32_t sh_cols[kRowWarps][32];
   __shared__ unsigned sh_mask[kRowWarps][32];
-  __shared__ double sh_si[kRowWarps][32][3];
-  __shared__ double sh_sk[kRowWarps][32][kMaxTargets][3];
+  __shared__ int8_t sh_pi[kRowWarps][32];
   __shared__ int8_t sh_tslot[kRowWarps][32][kMaxTargets];
+  __shared__ int8_t sh_tk[kRowWarps][32][kMaxTargets];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t il = blockIdx.x * (int64_t)kRowWarps + w; il < nloc; il += (int64_t)gridDim.x * kRowWarps) {
     const int32_t self = static_cast<int32_t>(n_lo + il);
@@ -283,19 +283,35 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
     for (int q = 0; q < 9; ++q) M[q] = 0.0;
     __syncwarp();
     for (int rb = 0; rb < nfc; rb += 32) {
+      // ---- load the round's records: chunk c = 16-byte piece (c % 9) of record (c / 9)
+      const int nact = min(32, nfc - rb);
+      const int32_t myr = lane < nact ? nf_idx[f0 + rb + lane] : 0;
+      // 16-byte cp.async (LDGSTS): global -> shared without registers, all 9 in flight
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const int c = lane + 32 * q;
+        const int k = c / 9, part = c - 9 * k;
+        const int32_t r = __shfl_sync(0xffffffffu, myr, k);
+        if (k < nact) {
+          const double2* src = reinterpret_cast<const double2*>(face_s + kRec * static_cast<int64_t>(r)) + part;
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&sh_rec[w][0][0])) + 16u * c;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
       // ---- A: lane = face
-      if (rb + lane < nfc) {
-        const int32_t f = nf_idx[f0 + rb + lane];
+      if (lane < nact) {
+        const double* sf = sh_rec[w][lane];
+        const int32_t* rf = rec_field(sf);
         int32_t fld[5];
-        record_field<kTet>(face_nodes, face_opp, f, fld);
-        const double* sf = face_s + kFaceStride * static_cast<int64_t>(f);
+#pragma unroll
+        for (int K = 0; K < 5; ++K) fld[K] = rf[K];
         int pi = 0;
 #pragma unroll
         for (int K = 0; K < 5; ++K) pi = (fld[K] == self) ? K : pi;
         const double s0 = sf[3 * pi], s1 = sf[3 * pi + 1], s2 = sf[3 * pi + 2];
-        sh_si[w][lane][0] = s0;
-        sh_si[w][lane][1] = s1;
-        sh_si[w][lane][2] = s2;
+        sh_pi[w][lane] = static_cast<int8_t>(pi);
         d[0] = fma(s0, s0, d[0]);
         d[1] = fma(s1, s1, d[1]);
         d[2] = fma(s2, s2, d[2]);
@@ -313,9 +329,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
           for (int step = 16; step > 0; step >>= 1)
             if (sh_cols[w][lo + step - 1] < v) lo += step;
           sh_tslot[w][lane][t] = static_cast<int8_t>(lo);
-          sh_sk[w][lane][t][0] = sf[3 * K];
-          sh_sk[w][lane][t][1] = sf[3 * K + 1];
-          sh_sk[w][lane][t][2] = sf[3 * K + 2];
+          sh_tk[w][lane][t] = static_cast<int8_t>(K);
           atomicOr(&sh_mask[w][lo], 1u << lane);
           ++t;
         }
@@ -333,8 +347,10 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
         int t = 0;
 #pragma unroll
         for (int q = 1; q < kMaxTargets; ++q) t = (sh_tslot[w][b][q] == slot) ? q : t;
-        const double a0 = sh_si[w][b][0], a1 = sh_si[w][b][1], a2 = sh_si[w][b][2];
-        const double c0 = sh_sk[w][b][t][0], c1 = sh_sk[w][b][t][1], c2 = sh_sk[w][b][t][2];
+        const double* rb_ = sh_rec[w][b];
+        const int pb = sh_pi[w][b], K = sh_tk[w][b][t];
+        const double a0 = rb_[3 * pb], a1 = rb_[3 * pb + 1], a2 = rb_[3 * pb + 2];
+        const double c0 = rb_[3 * K], c1 = rb_[3 * K + 1], c2 = rb_[3 * K + 2];
         M[0] = fma(a0, c0, M[0]);
         M[1] = fma(a0, c1, M[1]);
         M[2] = fma(a0, c2, M[2]);
@@ -380,9 +396,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
 }  // namespace
 
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
-                   const int32_t* face_opp, int64_t nf, double* face_s, cudaStream_t s) {
+                   const int32_t* face_opp, int64_t nf, double* face_s, double* face_V, cudaStream_t s) {
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nf, 256), 16LL * num_sms()));
-  k_face_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, face_nodes, face_tet, face_opp, nf, face_s);
+  k_face_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, face_nodes, face_tet, face_opp, nf, face_s, face_V);
   FS_LAUNCH_CHECK();
 }
 
@@ -413,9 +429,9 @@ void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int
   }
 }
 
-void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, cudaStream_t s) {
+void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s) {
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nt, 256), 16LL * num_sms()));
-  k_tet_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, nt, tet_s);
+  k_tet_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, nt, tet_s, tet_V);
   FS_LAUNCH_CHECK();
 }
 

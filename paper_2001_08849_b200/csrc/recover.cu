@@ -13,7 +13,7 @@ namespace fsfem {
 
 namespace {
 
-constexpr int kRecStride = 16;  // doubles per assembly record (assemble.cu)
+constexpr int kRecStride = 18;  // doubles per assembly record (assemble.cu): s_K at 3K
 
 __device__ __forceinline__ void domain_field(const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
                                              bool tet, int64_t r, int32_t (&fld)[5]) {
@@ -35,14 +35,15 @@ __device__ __forceinline__ void domain_field(const int32_t* __restrict__ rec_a, 
 
 __global__ void __launch_bounds__(256) k_domain_stress(const int32_t* __restrict__ rec_a,
                                                        const int32_t* __restrict__ rec_b, bool tet,
-                                                       const double* __restrict__ rec_s, int64_t nrec,
+                                                       const double* __restrict__ rec_s,
+                                                       const double* __restrict__ rec_V, int64_t nrec,
                                                        const double* __restrict__ u, double lam, double mu,
                                                        double* __restrict__ strain, double* __restrict__ stress) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
     int32_t fld[5];
     domain_field(rec_a, rec_b, tet, r, fld);
     const double* sr = rec_s + kRecStride * r;
-    const double V = tet ? sr[12] : sr[15];
+    const double V = rec_V[r];
     const double inv = 1.0 / sqrt(V);
     double e[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -71,14 +72,14 @@ __global__ void __launch_bounds__(256) k_domain_stress(const int32_t* __restrict
 
 // Thread per own node: sum over its domain list in ascending order (fixed order).
 __global__ void __launch_bounds__(256) k_node_stress(const int64_t* __restrict__ nd_ptr,
-                                                     const int32_t* __restrict__ nd_idx, const double* __restrict__ rec_s,
-                                                     bool tet, const double* __restrict__ stress, int64_t nloc,
+                                                     const int32_t* __restrict__ nd_idx, const double* __restrict__ rec_V,
+                                                     const double* __restrict__ stress, int64_t nloc,
                                                      double* __restrict__ node_stress, double* __restrict__ node_vm) {
   for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
     double a[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, w = 0.0;
     for (int64_t k = nd_ptr[il]; k < nd_ptr[il + 1]; ++k) {
       const int64_t r = nd_idx[k];
-      const double V = rec_s[kRecStride * r + (tet ? 12 : 15)];
+      const double V = rec_V[r];
 #pragma unroll
       for (int q = 0; q < 6; ++q) a[q] = fma(V, stress[6 * r + q], a[q]);
       w += V;
@@ -98,15 +99,16 @@ __global__ void __launch_bounds__(256) k_node_stress(const int64_t* __restrict__
 
 }  // namespace
 
-void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, int64_t nrec,
+void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, const double* rec_V,
+                    int64_t nrec,
                     const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
                     double* strain, double* stress, double* node_stress, double* node_vm, cudaStream_t s) {
   const int g1 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrec, 256), 16LL * num_sms())));
-  k_domain_stress<<<g1, 256, 0, s>>>(rec_a, rec_b, tet, rec_s, nrec, u, lam, mu, strain, stress);
+  k_domain_stress<<<g1, 256, 0, s>>>(rec_a, rec_b, tet, rec_s, rec_V, nrec, u, lam, mu, strain, stress);
   FS_LAUNCH_CHECK();
   if (nloc > 0 && (node_stress || node_vm)) {
     const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 16LL * num_sms())));
-    k_node_stress<<<g2, 256, 0, s>>>(nd_ptr, nd_idx, rec_s, tet, stress, nloc, node_stress, node_vm);
+    k_node_stress<<<g2, 256, 0, s>>>(nd_ptr, nd_idx, rec_V, stress, nloc, node_stress, node_vm);
     FS_LAUNCH_CHECK();
   }
 }

@@ -253,10 +253,13 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
 // positions of each 32-face round; the diagonal block as per-lane sums over faces lane,
 // lane+32, ... then a fixed warp tree.
 constexpr int kRowWarps = 4;
+#ifndef FSFEM_ASM_MINB
+#define FSFEM_ASM_MINB 6
+#endif
 constexpr int kMaxTargets = 4;  // other field nodes of a face
 
 template <bool kTet>
-__global__ void __launch_bounds__(kRowWarps * 32) k_assemble_rows2(
+__global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_rows2(
     const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
     const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
     const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals) {

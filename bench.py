@@ -312,6 +312,7 @@ def run_gpu(args):
                            "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,
                            "pcg_it_per_s": iters / (t_pcg / 1e3), "pcg_iterations": iters, "pcg_ms": t_pcg,
                            "faces_ms": agg("t_faces_ms"), "symbolic_ms": agg("t_symbolic_ms"), "bc_ms": agg("t_bc_ms"),
+                           "cold_faces_per_s": nf / ((agg("t_faces_ms") + agg("t_symbolic_ms") + t_num) / 1e3),
                            "true_rel_residual": reps[-1][2]["true_rel_residual"]},
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
     if world == 1 and not args.no_cpu_baseline:

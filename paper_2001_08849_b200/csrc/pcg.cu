@@ -110,16 +110,6 @@ static_assert(StageLayout::kTptr % 16 == 0 && StageLayout::kSnbr % 16 == 0 && St
 #define FSFEM_SPMV_MINB 2
 #endif
 constexpr int kStages = FSFEM_SPMV_STAGES;
-#ifndef FSFEM_SPMV_EXPERIMENT
-#define FSFEM_SPMV_EXPERIMENT 0  // tuning only: 1 = skip the transposed half
-#endif
-#ifndef FSFEM_SPMV_MAPPING
-#define FSFEM_SPMV_MAPPING 0
-#endif
-#ifndef FSFEM_SPMV_LANE_ITEMS
-#define FSFEM_SPMV_LANE_ITEMS 6
-#endif
-[[maybe_unused]] constexpr int kLaneItems = FSFEM_SPMV_LANE_ITEMS;  // flat mapping: items per lane per round
 #ifndef FSFEM_SPMV_ITEMS_S
 #define FSFEM_SPMV_ITEMS_S 3
 #endif
@@ -282,78 +272,11 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
     const int32_t* sn = reinterpret_cast<const int32_t*>(stg + StageLayout::kSnbr) + in.dsn;
     const int2* tl = reinterpret_cast<const int2*>(stg + StageLayout::kTl) + in.dtl;
     const double* sv = reinterpret_cast<const double*>(stg + StageLayout::kVals) + in.dval;
-#if FSFEM_SPMV_MAPPING == 1
-    // Flat value mapping, 16 lanes per node (2 nodes per warp): value v = 9b + e of the node's
-    // block list (stored blocks first, then transposed); consecutive lanes read consecutive
-    // matrix values (shared memory for stored blocks, one coalesced run per transposed block),
-    // and the 3 x values of a block are shared by its 9 lanes.  e = 3r + q:
-    //   stored block:      y[r] += K_ij[r][q] x_j[q]
-    //   transposed block:  y[q] += K_ji[r][q] x_j[r]
-    const int half = lane >> 4, hl = lane & 15;
-    for (int mb = warp * 2; mb < in.nn; mb += kWarps * 2) {
-      const int m = mb + half;
-      const bool act = m < in.nn;
-      const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
-      const int ds = act ? static_cast<int>(sp[m + 1] - sp[m]) : 0;
-      const int lt = act ? static_cast<int>(tp[m]) - in.Pt0 : 0;
-      const int nvs = 9 * ds, nv = act ? 9 * (ds + static_cast<int>(tp[m + 1] - tp[m])) : 0;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      const int nvw = max(nv, __shfl_xor_sync(0xffffffffu, nv, 16));  // uniform trip count
-      for (int v0 = 0; v0 < nvw; v0 += 16 * kLaneItems) {
-        double kv[kLaneItems], xv[kLaneItems];
-        int dst[kLaneItems];
-#pragma unroll
-        for (int u = 0; u < kLaneItems; ++u) {
-          const int v = v0 + hl + 16 * u;
-          const int b = v / 9, e = v - 9 * b;
-          const int r = e / 3, q = e - 3 * r;
-          kv[u] = 0.0;
-          xv[u] = 0.0;
-          dst[u] = 0;
-          if (v < nvs) {
-            kv[u] = sv[9 * ls + v];
-            xv[u] = __ldg(x + 3 * sn[ls + b] + q);
-            dst[u] = r;
-          } else if (v < nv) {
-            const int2 ent = tl[lt + b - ds];
-            kv[u] = __ldg(vals + 9 * static_cast<int64_t>(ent.x) + e);
-            xv[u] = __ldg(x + 3 * ent.y + r);
-            dst[u] = q;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kLaneItems; ++u) {
-          const double t = kv[u] * xv[u];
-          s0 += dst[u] == 0 ? t : 0.0;
-          s1 += dst[u] == 1 ? t : 0.0;
-          s2 += dst[u] == 2 ? t : 0.0;
-        }
-      }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      }
-      if (act && hl == 0) {
-        const int64_t il = in.n0 + m;
-        y[3 * il] = s0;
-        y[3 * il + 1] = s1;
-        y[3 * il + 2] = s2;
-        if (kPcg) {
-          const double* xo = x + own_off + 3 * il;
-          dot = fma(xo[0], s0, dot);
-          dot = fma(xo[1], s1, dot);
-          dot = fma(xo[2], s2, dot);
-        }
-      }
-    }
-#else
-    // 8-lane group per node: a warp works on 4 nodes at once, a lane on up to kLaneItems
+    // 8-lane group per node: a warp works on 4 nodes at once, a lane on up to kItemsS + kItemsT
     // independent items per round (loads issued together), then a 3-level group tree.
     constexpr int G = kGroupLanes, NPW = 32 / kGroupLanes;
     const int grp = lane / G, gl = lane % G;
-    for (int mb = warp * NPW; mb < (FSFEM_SPMV_EXPERIMENT == 3 ? 0 : in.nn); mb += kWarps * NPW) {
+    for (int mb = warp * NPW; mb < in.nn; mb += kWarps * NPW) {
       const int m = mb + grp;
       const bool act = m < in.nn;
       const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
@@ -386,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
         for (int u = 0; u < kItemsT; ++u) {
           const int k = G * (kItemsT * r + u) + gl;
           tv[u][0] = tv[u][1] = tv[u][2] = xt[u] = 0.0;
-          if (FSFEM_SPMV_EXPERIMENT == 0 && k < nts) {
+          if (k < nts) {
             const int b = k / 3, cc = k - 3 * b;
             const int2 e = tl[lt + b];
             const double* pb = vals + 9 * static_cast<int64_t>(e.x) + 3 * cc;
@@ -433,7 +356,6 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
         }
       }
     }
-#endif
 #if FSFEM_SPMV_TIMING
     const long long t2 = clock64();
     t_comp += t2 - t1;

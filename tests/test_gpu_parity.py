@@ -435,3 +435,20 @@ def test_unreferenced_node_is_rejected_by_bcs(fs):
     with pytest.raises(FsfemError) as e:
         g.apply_bc(m.dirichlet, loads)
     assert e.value.status == "BREAKDOWN"
+
+
+def test_full_pipeline_bitwise_reproducible_cfg3(fs):
+    """Two complete runs (faces, pattern, assembly, BCs, PCG) on cfg3 give byte-identical CSR values
+    and displacements: every reduction has a fixed order (Q26), no atomics on values."""
+    m = config_mesh(3)
+    outs = []
+    for _ in range(2):
+        g = fs()
+        g.build_faces(m.xyz, m.tets)
+        g.assemble_csr(E, NU)
+        v = g.get_csr(with_pattern=False).vals.copy()
+        g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+        u, rep = g.pcg_solve()
+        outs.append((v, u, rep["iterations"]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1]) and outs[0][2] == outs[1][2]

@@ -628,8 +628,15 @@ __global__ void k_combine(PcgState* st, const double* __restrict__ all, int stag
 }  // namespace
 
 int pcg_grid() { return 4 * num_sms(); }
+// Small problems: fewer CTAs (less launch, barrier and last-CTA reduction work per iteration).
+// The grid only depends on the problem size, so reductions keep a fixed order for a given mesh.
+int vec_grid(int64_t n) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pcg_grid(), ceil_div(n, kThreads * kVec))));
+}
 
-int spmv_grid() { return FSFEM_SPMV_MINB * num_sms(); }
+int spmv_grid(int64_t nchunks) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(FSFEM_SPMV_MINB * num_sms(), nchunks)));
+}
 
 void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
                  PcgState* st, double* part, bool pcg, cudaStream_t s) {
@@ -641,11 +648,11 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
   }
   const int nch = static_cast<int>(pat.nchunks);
   if (pcg)
-    k_spmv<true><<<spmv_grid(), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
+    k_spmv<true><<<spmv_grid(nch), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
                                                             pat.snbr.get(), pat.tlist.get(), vals, x_full, own_off, y,
                                                             st, part);
   else
-    k_spmv<false><<<spmv_grid(), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
+    k_spmv<false><<<spmv_grid(nch), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
                                                              pat.snbr.get(), pat.tlist.get(), vals, x_full, own_off, y,
                                                              st, part);
   FS_LAUNCH_CHECK();
@@ -653,12 +660,12 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
 
 void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,
                    double* part, cudaStream_t s) {
-  k_update<<<pcg_grid(), kThreads, 0, s>>>(x, r, p, q, dinv, n, st, part);
+  k_update<<<vec_grid(n), kThreads, 0, s>>>(x, r, p, q, dinv, n, st, part);
   FS_LAUNCH_CHECK();
 }
 
 void launch_direction(double* p, const double* r, const double* dinv, int64_t n, PcgState* st, cudaStream_t s) {
-  k_direction<<<pcg_grid(), kThreads, 0, s>>>(p, r, dinv, n, st);
+  k_direction<<<vec_grid(n), kThreads, 0, s>>>(p, r, dinv, n, st);
   FS_LAUNCH_CHECK();
 }
 
@@ -675,7 +682,7 @@ int update_direction_grid() {
 void launch_update_direction(double* x, double* r, double* p, const double* q, const double* dinv, int64_t n,
                              PcgState* st, double* part, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(update_direction_grid());
+  cfg.gridDim = dim3(std::min(update_direction_grid(), vec_grid(n)));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
@@ -690,12 +697,12 @@ void launch_update_direction(double* x, double* r, double* p, const double* q, c
 
 void launch_init(const double* f, const double* q, const double* dinv, double* r, double* p, int64_t n, PcgState* st,
                  double* part, cudaStream_t s) {
-  k_init<<<pcg_grid(), kThreads, 0, s>>>(f, q, dinv, r, p, n, st, part);
+  k_init<<<vec_grid(n), kThreads, 0, s>>>(f, q, dinv, r, p, n, st, part);
   FS_LAUNCH_CHECK();
 }
 
 void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s) {
-  k_resid<<<pcg_grid(), kThreads, 0, s>>>(f, q, n, st, part);
+  k_resid<<<vec_grid(n), kThreads, 0, s>>>(f, q, n, st, part);
   FS_LAUNCH_CHECK();
 }
 

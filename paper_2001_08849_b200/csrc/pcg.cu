@@ -386,6 +386,80 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   }
 }
 
+// Small meshes (fewer chunks than SMs: the configurations whose PCG is launch-latency bound):
+// a plain warp-per-node kernel without the TMA pipeline -- no mbarrier set-up, no staging, one
+// node per warp with all its loads issued directly.  Same items and fixed warp-tree order as
+// the group mapping (the choice depends only on the mesh, so results stay reproducible).
+template <bool kPcg>
+__global__ void __launch_bounds__(kThreads) k_spmv_small(const int64_t* __restrict__ sptr,
+                                                         const int32_t* __restrict__ snbr,
+                                                         const int64_t* __restrict__ tptr,
+                                                         const int2* __restrict__ tlist,
+                                                         const double* __restrict__ vals, int64_t nloc,
+                                                         const double* __restrict__ x, int64_t own_off,
+                                                         double* __restrict__ y, PcgState* st, double* part) {
+  if (kPcg) {
+    double unused;
+    if (cta_scalars(st, nullptr, unused)) return;
+  }
+  const int lane = threadIdx.x & 31;
+  double dot = 0.0;
+  for (int64_t il = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; il < nloc;
+       il += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t Ps = sptr[il], Pt = tptr[il];
+    const int nus = static_cast<int>(3 * (sptr[il + 1] - Ps));
+    const int ntot = nus + static_cast<int>(3 * (tptr[il + 1] - Pt));
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int k = lane; k < ntot; k += 32) {
+      double v0, v1, v2, xv;
+      if (k < nus) {
+        const int b = k / 3, cc = k - 3 * b;
+        const double* pb = vals + 9 * (Ps + b) + cc;
+        v0 = __ldg(pb);
+        v1 = __ldg(pb + 3);
+        v2 = __ldg(pb + 6);
+        xv = __ldg(x + 3 * static_cast<int64_t>(__ldg(snbr + Ps + b)) + cc);
+      } else {
+        const int kt = k - nus;
+        const int b = kt / 3, cc = kt - 3 * b;
+        const int2 e = __ldg(tlist + Pt + b);
+        const double* pb = vals + 9 * static_cast<int64_t>(e.x) + 3 * cc;
+        v0 = __ldg(pb);
+        v1 = __ldg(pb + 1);
+        v2 = __ldg(pb + 2);
+        xv = __ldg(x + 3 * static_cast<int64_t>(e.y) + cc);
+      }
+      s0 = fma(v0, xv, s0);
+      s1 = fma(v1, xv, s1);
+      s2 = fma(v2, xv, s2);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      y[3 * il] = s0;
+      y[3 * il + 1] = s1;
+      y[3 * il + 2] = s2;
+      if (kPcg) {
+        const double* xo = x + own_off + 3 * il;
+        dot = fma(xo[0], s0, dot);
+        dot = fma(xo[1], s1, dot);
+        dot = fma(xo[2], s2, dot);
+      }
+    }
+  }
+  if (!kPcg) return;
+  const double mine[1] = {dot};
+  double out[1];
+  if (grid_reduce<1>(mine, part, &st->ticket[0], out) && threadIdx.x == 0) {
+    if (st->nranks > 1) {
+      st->local[0] = out[0];
+    } else {
+      finish_alpha(st, out[0]);
+    }
+  }
+}
+
 // Vector kernels: each thread takes kVec elements per pass at stride gridDim*blockDim (coalesced)
 // and issues all their loads before any arithmetic, so that enough bytes are in flight to
 // stream HBM.  Per-thread partial sums run in element order: the result depends only on the
@@ -647,6 +721,14 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     attr_set = true;
   }
   const int nch = static_cast<int>(pat.nchunks);
+  if (nch < num_sms()) {  // small mesh: plain warp-per-node kernel
+    const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pcg_grid(), ceil_div(pat.nloc, kWarps))));
+    auto kern = pcg ? k_spmv_small<true> : k_spmv_small<false>;
+    kern<<<g, kThreads, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.tptr.get(), pat.tlist.get(), vals, pat.nloc, x_full,
+                                own_off, y, st, part);
+    FS_LAUNCH_CHECK();
+    return;
+  }
   if (pcg)
     k_spmv<true><<<spmv_grid(nch), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
                                                             pat.snbr.get(), pat.tlist.get(), vals, x_full, own_off, y,

@@ -187,11 +187,18 @@ def load_peaks() -> tuple[float, str]:
     return 6650.0, "fallback"
 
 
-def traffic_from_profile(cfg: int):
+SPMV_KERNELS = {0: "k_spmv_small<true> (warp per node, PCG SpMV + p.q)",
+                1: "k_spmv<true> (gather, PCG SpMV + p.q)",
+                2: "k_spmv_df<true> (dataflow push, PCG SpMV + p.q)"}
+
+
+def traffic_from_profile(cfg: int, kernel: int):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the kernel from
+    the committed ncu capture (profiles/spmv_dram_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "spmv_dram_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get(f"cfg{cfg}")
+        return d.get(f"cfg{cfg}_kernel{kernel}")
     return None
 
 
@@ -294,8 +301,9 @@ def run_gpu(args):
     # algorithmic bytes as the library counts them for its symmetric block storage
     spmv_bytes = int(last["spmv_bytes"])
     achieved = spmv_bytes / (spmv_avg_ms / 1e3) / 1e9
-    roof = {"kernel": "k_spmv<true> (PCG SpMV + p.q)", "bound": "hbm", "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(args.config),
+    kind = int(last["spmv_kernel"])
+    roof = {"kernel": SPMV_KERNELS.get(kind, str(kind)), "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(args.config, kind),
             "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms, "launches_timed": spmv_n,
             "peak_kind": peak_kind, "launches_per_step": iters + 1,
             "share_of_step": spmv_avg_ms * (iters + 1) / (ms / args.steps),

@@ -81,6 +81,9 @@ typedef struct {
                                 transposed list, row pointers, x read once, y written once       */
   int64_t assembly_bytes;    /* minimum DRAM bytes of one numeric assembly: mesh read + stored
                                 values written                                                   */
+  int64_t spmv_kernel;       /* SpMV kernel of this pattern: 0 warp per node (small meshes),
+                                1 gather (transposed blocks read from their rows), 2 dataflow push
+                                                                                   */
 } fsfem_report;
 
 /* Human-readable name of a status code (static string). */

@@ -22,6 +22,7 @@ namespace fsfem {
 #endif
 constexpr int kChunkNodes = FSFEM_CHUNK_NODES;
 constexpr int kCapBlocks = FSFEM_CAP_BLOCKS;
+constexpr int kMaxDeps = 48;
 struct SpmvChunk {
   int32_t n0, n1, Ps0, Ps1, Pt0, Pt1, pad0, pad1;
 };
@@ -42,6 +43,22 @@ struct Pattern {
   DevBuf<int2> tlist;        // [ntb] (stored block index of K_ji, node j), ascending j
   int64_t nchunks = 0;
   DevBuf<SpmvChunk> chunks;  // [nchunks] SpMV streaming chunks
+  // Dataflow push SpMV (pcg.cu k_spmv_df): the transposed product K_ij^T x_i of stored block
+  // b = (i, j) is written by row i to tbuf[tpos[b]] (the slot of K_ji in row j's transposed list),
+  // and row j sums its contiguous slots once every chunk holding a producer row has finished.
+  DevBuf<int32_t> tpos;      // [nsb + 4] slot in the transposed list, or -1 (diagonal, halo, beyond range)
+  DevBuf<double> tbuf;       // [3 ntb + 2] pushed transposed products
+  DevBuf<int32_t> deps;      // [nchunks * kMaxDeps] distinct earlier chunks holding producer rows
+  DevBuf<int32_t> ndeps;     // [nchunks] their number, or -1 (more than kMaxDeps: no dataflow SpMV)
+  DevBuf<uint32_t> cflags;   // [nchunks] epoch at which the chunk became ready for phase 2
+  DevBuf<uint32_t> sync;     // [2] epoch, last-CTA ticket
+  // chunk d needs ndeps[d] + 1 finished phase-1 chunks (its producers and itself);
+  // dep_ptr/dep_list = for each chunk c the chunks d that need it (c itself first), with that count.
+  bool df_ok = false;        // every chunk's producer list fits kMaxDeps
+  DevBuf<int32_t> dep_ptr;   // [nchunks + 1]
+  DevBuf<int2> dep_list;     // [dep_ptr[nchunks]] (chunk d, need[d])
+  DevBuf<uint32_t> cnt;      // [nchunks] arrival counters (mod need)
+  DevBuf<double> dotc;       // [nchunks] per-chunk p.q partials
   DevBuf<int64_t> nf_ptr;    // [nloc+1]
   DevBuf<int32_t> nf_idx;    // [nfi] faces whose field holds node i, ascending
 };

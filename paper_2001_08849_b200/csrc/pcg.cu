@@ -7,6 +7,9 @@
 // fixed-shape tree (warp shuffles, fixed CTA order, "last CTA reduces") so results are
 // bitwise reproducible.  Scalars live on the device; the host only polls `done` between
 // CUDA-graph batches of iterations.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "pcg.cuh"
 
@@ -34,14 +37,14 @@ __device__ __forceinline__ bool cta_scalars(const PcgState* st, const double* fi
 }
 
 // Deterministic CTA sum of one double per thread (result valid in thread 0).
-__device__ __forceinline__ double block_sum(double v, double* sh /*[kWarps]*/) {
+__device__ __forceinline__ double block_sum(double v, double* sh /*[blockDim / 32]*/) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) sh[w] = v;
   __syncthreads();
   double r = 0.0;
   if (threadIdx.x == 0)
-    for (int k = 0; k < kWarps; ++k) r += sh[k];
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) r += sh[k];
   __syncthreads();
   return r;
 }
@@ -50,7 +53,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh /*[kWarps]*/) {
 // all partials in a fixed tree and returns true (results in out[0..NV) of thread 0).
 template <int NV>
 __device__ __forceinline__ bool grid_reduce(const double (&mine)[NV], double* part, unsigned int* ticket, double* out) {
-  __shared__ double sh[kWarps];
+  __shared__ double sh[32];
   __shared__ bool last;
   double tot[NV];
 #pragma unroll
@@ -67,7 +70,7 @@ __device__ __forceinline__ bool grid_reduce(const double (&mine)[NV], double* pa
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     double s = 0.0;
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) s += ld_cg(part + v * gridDim.x + b);
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += ld_cg(part + v * gridDim.x + b);
     out[v] = block_sum(s, sh);
   }
   if (threadIdx.x == 0) *ticket = 0u;
@@ -147,6 +150,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// L2 eviction-priority policies (per-access cache hints).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // Copy elements [e0, e1) of a global array (element size `es`) to smem `dst` with 16-B aligned
 // source and size; returns the element offset of e0 inside dst and adds the bytes to `tx`.
 // The global arrays are allocated with >= 16 B of slack, so the rounded-up tail is readable.
@@ -160,6 +178,24 @@ __device__ __forceinline__ int stage_copy(void* dst, const void* base, int64_t e
   bulk_g2s(dst, reinterpret_cast<const void*>(a0), bytes, bar);
   tx += bytes;
   return static_cast<int>((b + e0 * es - a0) / es);
+}
+
+__device__ __forceinline__ int stage_copy_hint(void* dst, const void* base, int64_t e0, int64_t e1, int es,
+                                               uint64_t* bar, uint32_t& tx, uint64_t pol) {
+  if (e1 <= e0) return 0;
+  const uintptr_t b = reinterpret_cast<uintptr_t>(base);
+  const uintptr_t a0 = (b + e0 * es) & ~uintptr_t(15);
+  const uintptr_t a1 = (b + e1 * es + 15) & ~uintptr_t(15);
+  const uint32_t bytes = static_cast<uint32_t>(a1 - a0);
+  bulk_g2s_hint(dst, reinterpret_cast<const void*>(a0), bytes, bar, pol);
+  tx += bytes;
+  return static_cast<int>((b + e0 * es - a0) / es);
+}
+
+// element offset of element e0 inside its 16-B aligned bulk copy (what stage_copy returns)
+__device__ __forceinline__ int stage_off(const void* base, int64_t e0, int es) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(base) + e0 * es;
+  return static_cast<int>((a & uintptr_t(15)) / es);
 }
 
 struct StageInfo {  // written by the issuing thread, read after the mbarrier wait
@@ -383,6 +419,438 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
     } else {
       finish_alpha(st, out[0]);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Push form of the symmetric product (k_spmv_df below).  For a stored block b = (i, j), j > i,
+// the row-i pass already holds K_ij in shared memory and x_i in registers, so it computes the
+// transposed product t = K_ij^T x_i there and stores it to tbuf[tpos[b]], the slot of K_ji in
+// row j's (contiguous, ascending) transposed list; row j later only sums its slots.  Traffic vs
+// the gather kernel: the 72-B K_ji and 24-B x_j gathers of a transposed block become one 24-B
+// store and one contiguous 24-B load (L2-resident in between).
+struct PushLayout {  // every region 16-B aligned
+  static constexpr int kPtr = 0;                                            // kChunkNodes + 4 int64
+  static constexpr int kXo = kPtr + (kChunkNodes + 4) * 8;                  // 3 kChunkNodes + 4 double
+  static constexpr int kSnbr = kXo + (3 * kChunkNodes + 4) * 8;             // kCapBlocks + 4 int32
+  static constexpr int kTp = kSnbr + ((kCapBlocks + 4) * 4 + 15) / 16 * 16;  // kCapBlocks + 4 int32
+  static constexpr int kVals = kTp + ((kCapBlocks + 4) * 4 + 15) / 16 * 16;  // 9 kCapBlocks + 2 double
+  static constexpr int kBytes = kVals + (9 * kCapBlocks + 2) * 8;
+};
+static_assert(PushLayout::kXo % 16 == 0 && PushLayout::kSnbr % 16 == 0 && PushLayout::kTp % 16 == 0 &&
+                  PushLayout::kVals % 16 == 0 && PushLayout::kBytes % 16 == 0,
+              "push stage regions must be 16-B aligned");
+#ifndef FSFEM_PUSH_ITEMS
+#define FSFEM_PUSH_ITEMS 5
+#endif
+constexpr int kPushItems = FSFEM_PUSH_ITEMS;
+struct PushInfo {
+  int n0, nn, Ps0, dptr, dsn, dtp, dval, dxo;
+};
+
+__device__ __forceinline__ void issue_chunk_push(const SpmvChunk& ch, const int64_t* sptr, const int32_t* snbr,
+                                                 const int32_t* tpos, const double* vals, const double* xown,
+                                                 unsigned char* stage, uint64_t* bar, PushInfo* info) {
+  uint32_t tx = 0;
+  const int64_t n0 = ch.n0, n1 = ch.n1, Ps0 = ch.Ps0, Ps1 = ch.Ps1;
+  auto rbytes = [](const void* base, int64_t e0, int64_t e1, int es) -> uint32_t {
+    if (e1 <= e0) return 0;
+    const uintptr_t b = reinterpret_cast<uintptr_t>(base);
+    return static_cast<uint32_t>(((b + e1 * es + 15) & ~uintptr_t(15)) - ((b + e0 * es) & ~uintptr_t(15)));
+  };
+  const uint32_t total = rbytes(sptr, n0, n1 + 1, 8) + rbytes(snbr, Ps0, Ps1, 4) + rbytes(tpos, Ps0, Ps1, 4) +
+                         rbytes(vals, 9 * Ps0, 9 * Ps1, 8) + rbytes(xown, 3 * n0, 3 * n1, 8);
+  // the stage description is stored before the arrival, so the phase completion publishes it
+  PushInfo in;
+  in.n0 = static_cast<int>(n0);
+  in.nn = static_cast<int>(n1 - n0);
+  in.Ps0 = static_cast<int>(Ps0);
+  in.dptr = stage_off(sptr, n0, 8);
+  in.dsn = stage_off(snbr, Ps0, 4);
+  in.dtp = stage_off(tpos, Ps0, 4);
+  in.dval = stage_off(vals, 9 * Ps0, 8);
+  in.dxo = stage_off(xown, 3 * n0, 8);
+  *info = in;
+  mbar_arrive_expect_tx(bar, total);
+  // the matrix streams through L2 once per product: evict it first (keeps x and tbuf resident)
+  const uint64_t pol = policy_evict_first();
+  stage_copy_hint(stage + PushLayout::kPtr, sptr, n0, n1 + 1, 8, bar, tx, pol);
+  stage_copy_hint(stage + PushLayout::kSnbr, snbr, Ps0, Ps1, 4, bar, tx, pol);
+  stage_copy_hint(stage + PushLayout::kTp, tpos, Ps0, Ps1, 4, bar, tx, pol);
+  stage_copy_hint(stage + PushLayout::kVals, vals, 9 * Ps0, 9 * Ps1, 8, bar, tx, pol);
+  stage_copy(stage + PushLayout::kXo, xown, 3 * n0, 3 * n1, 8, bar, tx);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void st_release_cta_s32(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Dataflow push SpMV (one kernel).  Same product and pushes as k_spmv_push; the row sums of the
+// pushed products (phase 2) run in the same launch, each chunk as soon as every chunk holding
+// one of its producer rows has finished phase 1:
+//   compute warps (8):  P1(c) of the CTA's chunks (TMA ring): y'_i into y, pushes into tbuf;
+//   loader warp:        the TMA ring; after P1(c) counts c as done for every chunk d that needs
+//                       it (c itself and the chunks of its rows' transposed partners; atomic
+//                       acq_rel counters).  The CTA whose count completes d queues d;
+//   phase-2 warp:       per queued chunk d: y_i = y'_i + sum of row i's tbuf slots (ascending),
+//                       the chunk's p.q partial; then the chunk's tbuf lines are dropped from L2
+//                       without write-back (they are rewritten before the next read).
+// Every sum has a fixed order and the p.q partials are per chunk, reduced in chunk order by the
+// last CTA: bitwise reproducible.  Phase-2 warps wait for other CTAs' chunks, so the launch is
+// cooperative (every CTA resident); the waits point to chunks whose phase 1 never waits.
+#ifndef FSFEM_DF_BATCH
+#define FSFEM_DF_BATCH 4
+#endif
+constexpr int kDfBatch = FSFEM_DF_BATCH;
+constexpr int kDfMinChunksPerCta = 16;
+constexpr int kDfThreads = kThreads + 96;  // 8 compute warps, loader, phase-2 and counter warps
+struct P2Layout {  // phase-2 buffer: node pointers, P1 sums, pushed slots of one chunk
+  static constexpr int kPtr = 0;                               // kChunkNodes + 4 int64
+  static constexpr int kY = kPtr + (kChunkNodes + 4) * 8;      // 3 kChunkNodes + 4 double
+  static constexpr int kT = kY + (3 * kChunkNodes + 4) * 8;    // 3 kCapBlocks + 4 double
+  static constexpr int kBytes = kT + (3 * kCapBlocks + 4) * 8;
+};
+static_assert(P2Layout::kY % 16 == 0 && P2Layout::kT % 16 == 0 && P2Layout::kBytes % 16 == 0,
+              "phase-2 buffer regions must be 16-B aligned");
+struct P2Info {
+  int n0, nn, Pt0, Pt1, dptr, dy, dt, pad;
+};
+constexpr int kDfSmem = 128 + 192 + 2 * PushLayout::kBytes + 2 * P2Layout::kBytes;
+
+template <bool kPcg>
+__global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
+    const SpmvChunk* __restrict__ chunks, int nchunks, const int64_t* __restrict__ sptr,
+    const int64_t* __restrict__ tptr, const int32_t* __restrict__ snbr, const int32_t* __restrict__ tpos,
+    const double* __restrict__ vals, const int32_t* __restrict__ dep_ptr, const int2* __restrict__ dep_list,
+    uint32_t* cnt, uint32_t* ready, double* dotc, uint32_t* sync, double* tbuf,
+    const double* __restrict__ x, int64_t own_off, double* y, PcgState* st) {
+  static_assert(kChunkNodes <= kWarps * (32 / kGroupLanes), "one pass of the compute warps per chunk");
+  static_assert(kChunkNodes <= 32, "phase 2: one lane per node");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [2] P1 stage loaded
+  uint64_t* empty = full + 2;                                 // [2] P1 stage consumed (8 warps)
+  uint64_t* p2full = full + 4;                                // [2] phase-2 buffer loaded
+  PushInfo* pinfo = reinterpret_cast<PushInfo*>(smem + 64);   // [2]
+  P2Info* qinfo = reinterpret_cast<P2Info*>(smem + 128);      // [2]
+  unsigned char* pst = smem + 192;                            // 2 P1 stages
+  unsigned char* qst = pst + 2 * PushLayout::kBytes;          // 2 phase-2 buffers
+  __shared__ uint32_t sh_epoch;
+  __shared__ int sh_done;
+  __shared__ int sh_p1done;  // chunks whose phase 1 the loader has seen complete
+  if (threadIdx.x == 0) {
+    sh_p1done = 0;
+    sh_epoch = __ldcg(sync) + 1u;
+    sh_done = kPcg ? (ld_cg(&st->done_d) != 0.0) : 0;
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kWarps);
+      mbar_init(&p2full[k], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (sh_done) return;  // uniform over the grid
+  const uint32_t epoch = sh_epoch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* xown = x + own_off;
+  const int K = nchunks > static_cast<int>(blockIdx.x) ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+#ifndef FSFEM_DF_TIMING
+#define FSFEM_DF_TIMING 0
+#endif
+  long long tA = 0, tB = 0, tC = 0, tq0 = FSFEM_DF_TIMING ? clock64() : 0;
+  int nitems = 0;
+#define DF_T(acc) if (FSFEM_DF_TIMING) { const long long tq1 = clock64(); acc += tq1 - tq0; tq0 = tq1; }
+  if (warp == kWarps) {
+    // ---------------- loader warp: P1 stages (TMA ring) ----------------
+    SpmvChunk nx = K > 2 ? chunks[blockIdx.x + 2 * gridDim.x] : SpmvChunk{};
+    for (int j = 0; j < 2 && j < K; ++j)
+      if (lane == 0)
+        issue_chunk_push(chunks[blockIdx.x + j * gridDim.x], sptr, snbr, tpos, vals, xown, pst + j * PushLayout::kBytes,
+                         &full[j], &pinfo[j]);
+    for (int j = 0; j < K; ++j) {
+      const int c = blockIdx.x + j * gridDim.x;
+      DF_T(tC)
+      mbar_wait(&empty[j & 1], (j >> 1) & 1);  // P1(c) done by every compute warp
+      DF_T(tA)
+      if (lane == 0 && j + 2 < K) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_chunk_push(nx, sptr, snbr, tpos, vals, xown, pst + (j & 1) * PushLayout::kBytes, &full[j & 1],
+                         &pinfo[j & 1]);
+      }
+      if (j + 3 < K) nx = chunks[c + 3 * gridDim.x];
+      if (lane == 0) st_release_cta_s32(&sh_p1done, j + 1);  // -> counter warp
+    }
+  } else if (warp == kWarps + 2) {
+    // ---------------- counter warp: dependency counts, in batches ----------------
+    // A gpu-scope fence costs microseconds under this load, so the warp takes every chunk whose
+    // phase 1 is complete (up to kDfBatch) per round: one release fence for all of their writes
+    // (ordered before the loader's observation of the mbarriers), relaxed increments, and one
+    // acquire fence before the completed chunks are published as ready.
+    constexpr int R = 2;  // rounds of 32 dependants per chunk kept in flight (more: slow path)
+    int2 e[kDfBatch][R];
+    int qq0[kDfBatch], qq1[kDfBatch];
+    auto prefetch = [&](int jb) {  // dependants of chunks jb .. jb + kDfBatch - 1
+#pragma unroll
+      for (int b = 0; b < kDfBatch; ++b) {
+        const int c = blockIdx.x + (jb + b) * gridDim.x;
+        qq0[b] = jb + b < K ? dep_ptr[c] : 0;
+        qq1[b] = jb + b < K ? dep_ptr[c + 1] : 0;
+      }
+#pragma unroll
+      for (int b = 0; b < kDfBatch; ++b)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int q = qq0[b] + 32 * r + lane;
+          e[b][r] = q < qq1[b] ? dep_list[q] : make_int2(-1, 1);
+        }
+    };
+    prefetch(0);
+    for (int j = 0; j < K; j += kDfBatch) {
+      const int jd = min(K, j + kDfBatch);
+      DF_T(tC)
+      while (ld_acquire_cta_s32(&sh_p1done) < jd) __nanosleep(32);
+      DF_T(tA)
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      DF_T(tB)
+      uint32_t old[kDfBatch][R];
+#pragma unroll
+      for (int b = 0; b < kDfBatch; ++b)
+#pragma unroll
+        for (int r = 0; r < R; ++r) old[b][r] = e[b][r].x >= 0 ? atomicAdd(cnt + e[b][r].x, 1u) : 0u;
+      for (int b = 0; b < jd - j; ++b)  // dependants beyond R * 32 (rare)
+        for (int q = qq0[b] + 32 * R + lane; q < qq1[b]; q += 32) {
+          const int2 ee = dep_list[q];
+          if ((atomicAdd(cnt + ee.x, 1u) + 1u) % static_cast<uint32_t>(ee.y) == 0u) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ready + ee.x), "r"(epoch) : "memory");
+          }
+        }
+      bool any_last = false;
+      int my_ready[kDfBatch * R];
+      int nready = 0;
+#pragma unroll
+      for (int b = 0; b < kDfBatch; ++b)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (e[b][r].x >= 0 && (old[b][r] + 1u) % static_cast<uint32_t>(e[b][r].y) == 0u) {
+            my_ready[nready++] = e[b][r].x;
+            any_last = true;
+          }
+      if (jd < K) prefetch(jd);  // in flight during the fence and the next wait
+      if (__any_sync(0xffffffffu, any_last)) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int k = 0; k < nready; ++k)
+          asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ready + my_ready[k]), "r"(epoch) : "memory");
+      }
+    }
+  } else if (warp == kWarps + 1) {
+    // ---------------- phase-2 warp: the CTA's own chunks in order, lane = node ----------------
+    // chunk d's node pointers, pushed slots and P1 sums are bulk-copied into buffer j & 1 once d
+    // is ready; the copy of the next chunk is issued before the current one is summed.
+    auto ready_now = [&](int d) { return __shfl_sync(0xffffffffu, lane == 0 ? ld_acquire_u32(ready + d) : 0u, 0) == epoch; };
+    auto issue = [&](int jj) {
+      const int d = blockIdx.x + jj * gridDim.x;
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.global;\nfence.proxy.async.shared::cta;" ::: "memory");
+        const SpmvChunk ch = chunks[d];
+        unsigned char* qb = qst + (jj & 1) * P2Layout::kBytes;
+        P2Info qi;
+        qi.n0 = ch.n0;
+        qi.nn = ch.n1 - ch.n0;
+        qi.Pt0 = ch.Pt0;
+        qi.Pt1 = ch.Pt1;
+        qi.dptr = stage_off(tptr, ch.n0, 8);
+        qi.dy = stage_off(y, 3 * (int64_t)ch.n0, 8);
+        qi.dt = stage_off(tbuf, 3 * (int64_t)ch.Pt0, 8);
+        qi.pad = 0;
+        qinfo[jj & 1] = qi;
+        auto rbytes = [](const void* base, int64_t e0, int64_t e1, int es) -> uint32_t {
+          if (e1 <= e0) return 0;
+          const uintptr_t bb = reinterpret_cast<uintptr_t>(base);
+          return static_cast<uint32_t>(((bb + e1 * es + 15) & ~uintptr_t(15)) - ((bb + e0 * es) & ~uintptr_t(15)));
+        };
+        mbar_arrive_expect_tx(&p2full[jj & 1], rbytes(tptr, ch.n0, ch.n1 + 1, 8) +
+                                                   rbytes(y, 3 * (int64_t)ch.n0, 3 * (int64_t)ch.n1, 8) +
+                                                   rbytes(tbuf, 3 * (int64_t)ch.Pt0, 3 * (int64_t)ch.Pt1, 8));
+        uint32_t tx = 0;
+        stage_copy(qb + P2Layout::kPtr, tptr, ch.n0, ch.n1 + 1, 8, &p2full[jj & 1], tx);
+        stage_copy(qb + P2Layout::kY, y, 3 * (int64_t)ch.n0, 3 * (int64_t)ch.n1, 8, &p2full[jj & 1], tx);
+        stage_copy(qb + P2Layout::kT, tbuf, 3 * (int64_t)ch.Pt0, 3 * (int64_t)ch.Pt1, 8, &p2full[jj & 1], tx);
+      }
+      __syncwarp();
+    };
+    int issued = 0;
+    for (int j = 0; j < K; ++j) {
+      DF_T(tC)
+      if (issued == j) {  // this chunk's copy must be in flight: wait for it to be ready
+        while (!ready_now(blockIdx.x + j * gridDim.x)) __nanosleep(32);
+        issue(j);
+        ++issued;
+      }
+      if (issued == j + 1 && j + 1 < K && ready_now(blockIdx.x + (j + 1) * gridDim.x)) {
+        issue(j + 1);
+        ++issued;
+      }
+      DF_T(tA)
+      ++nitems;
+      mbar_wait(&p2full[j & 1], (j >> 1) & 1);
+      DF_T(tB)
+      const unsigned char* qb = qst + (j & 1) * P2Layout::kBytes;
+      const P2Info qi = qinfo[j & 1];
+      const int64_t* tp = reinterpret_cast<const int64_t*>(qb + P2Layout::kPtr) + qi.dptr;
+      const double* yp = reinterpret_cast<const double*>(qb + P2Layout::kY) + qi.dy;
+      const double* tv = reinterpret_cast<const double*>(qb + P2Layout::kT) + qi.dt;
+      const bool act = lane < qi.nn;
+      const int mm = act ? lane : 0;
+      const int e0 = static_cast<int>(tp[mm] - qi.Pt0), e1 = act ? static_cast<int>(tp[mm + 1] - qi.Pt0) : e0;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int e = e0; e < e1; ++e) {
+        s0 += tv[3 * e];
+        s1 += tv[3 * e + 1];
+        s2 += tv[3 * e + 2];
+      }
+      s0 += yp[3 * mm];
+      s1 += yp[3 * mm + 1];
+      s2 += yp[3 * mm + 2];
+      double dt = 0.0;
+      const int64_t il = static_cast<int64_t>(qi.n0) + mm;
+      if (act) {
+        y[3 * il] = s0;
+        y[3 * il + 1] = s1;
+        y[3 * il + 2] = s2;
+        if (kPcg) {
+          const double* xo = xown + 3 * il;
+          dt = fma(__ldg(xo), s0, fma(__ldg(xo + 1), s1, __ldg(xo + 2) * s2));
+        }
+      }
+      if (kPcg) {
+        dt = warp_sum(dt);
+        if (lane == 0) dotc[blockIdx.x + j * gridDim.x] = dt;
+      }
+      // the chunk's pushed products are dead: drop their whole L2 lines without write-back
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(tbuf + 3 * (int64_t)qi.Pt0);
+      const uintptr_t hi = reinterpret_cast<uintptr_t>(tbuf + 3 * (int64_t)qi.Pt1);
+      for (uintptr_t ad = ((lo + 127) & ~uintptr_t(127)) + 128 * lane; ad + 128 <= hi; ad += 128 * 32)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(ad) : "memory");
+      __syncwarp();
+    }
+  } else {
+    // ---------------- compute warps: P1 ----------------
+    constexpr int G = kGroupLanes, NPW = 32 / kGroupLanes;
+    const int grp = lane / G, gl = lane % G;
+    const int m = warp * NPW + grp;  // this group's node inside every chunk
+    for (int j = 0; j < K; ++j) {
+      const int s = j & 1;
+      DF_T(tC)
+      mbar_wait(&full[s], (j >> 1) & 1);
+      DF_T(tA)
+      const unsigned char* stg = pst + s * PushLayout::kBytes;
+      const PushInfo in = pinfo[s];
+      const int64_t* sp = reinterpret_cast<const int64_t*>(stg + PushLayout::kPtr) + in.dptr;
+      const int32_t* sn = reinterpret_cast<const int32_t*>(stg + PushLayout::kSnbr) + in.dsn;
+      const int32_t* tq = reinterpret_cast<const int32_t*>(stg + PushLayout::kTp) + in.dtp;
+      const double* sv = reinterpret_cast<const double*>(stg + PushLayout::kVals) + in.dval;
+      const double* sx = reinterpret_cast<const double*>(stg + PushLayout::kXo) + in.dxo;
+      const bool act = m < in.nn;
+      const int mm = act ? m : 0;
+      const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
+      const int nus = act ? 3 * static_cast<int>(sp[m + 1] - sp[m]) : 0;
+      const double xi0 = sx[3 * mm], xi1 = sx[3 * mm + 1], xi2 = sx[3 * mm + 2];
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      int rounds = (nus + G * kPushItems - 1) / (G * kPushItems);
+#pragma unroll 1
+      for (int o = G; o < 32; o <<= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+      for (int r = 0; r < rounds; ++r) {
+        double xs[kPushItems];
+#pragma unroll
+        for (int u = 0; u < kPushItems; ++u) {
+          const int k = G * (kPushItems * r + u) + gl;
+          xs[u] = 0.0;
+          if (k < nus) {
+            const int b = k / 3, cc = k - 3 * b;
+            xs[u] = __ldg(x + 3 * sn[ls + b] + cc);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kPushItems; ++u) {
+          const int k = G * (kPushItems * r + u) + gl;
+          if (k < nus) {
+            const int b = k / 3, cc = k - 3 * b;
+            const double* pb = sv + 9 * (ls + b) + cc;
+            const double v0 = pb[0], v1 = pb[3], v2 = pb[6];
+            s0 = fma(v0, xs[u], s0);
+            s1 = fma(v1, xs[u], s1);
+            s2 = fma(v2, xs[u], s2);
+            const int tp = tq[ls + b];
+            if (tp >= 0) tbuf[3 * static_cast<int64_t>(tp) + cc] = fma(v2, xi2, fma(v1, xi1, v0 * xi0));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (act && gl == 0) {
+        const int64_t il = static_cast<int64_t>(in.n0) + m;
+        y[3 * il] = s0;
+        y[3 * il + 1] = s1;
+        y[3 * il + 2] = s2;
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // phase 2 reads them with bulk copies
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+#if FSFEM_DF_TIMING
+  if (lane == 0 && (warp == 0 || warp >= kWarps) && (blockIdx.x % 37) == 0)
+    printf("df blk %d %s K %d items %d: A %lld B %lld C %lld\n", blockIdx.x,
+           warp == kWarps ? "load" : (warp == kWarps + 1 ? "p2" : (warp > kWarps ? "count" : "comp")), K, nitems, tA,
+           tB, tC);
+#endif
+  // last CTA out: advances the epoch; PCG: p.q = sum of the per-chunk partials in chunk order
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(sync + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (kPcg) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int c = threadIdx.x; c < nchunks; c += blockDim.x) a += __ldcg(dotc + c);
+    const double pq = block_sum(a, sh);
+    if (threadIdx.x == 0) {
+      if (st->nranks > 1) {
+        st->local[0] = pq;
+      } else {
+        finish_alpha(st, pq);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    sync[1] = 0u;
+    __threadfence();
+    atomicExch(sync, epoch);
   }
 }
 
@@ -708,8 +1176,37 @@ int vec_grid(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pcg_grid(), ceil_div(n, kThreads * kVec))));
 }
 
+int df_grid() {
+  static int g = 0;
+  if (g == 0) {
+    int per_sm = 0;
+    FS_CUDA(cudaFuncSetAttribute(k_spmv_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
+    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_df<true>, kDfThreads, kDfSmem));
+    g = std::max(1, per_sm) * num_sms();
+  }
+  return g;
+}
+
 int spmv_grid(int64_t nchunks) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(FSFEM_SPMV_MINB * num_sms(), nchunks)));
+}
+
+// 0: k_spmv_small (fewer chunks than SMs), 1: k_spmv (gather), 2: k_spmv_df (dataflow push).
+// FSFEM_SPMV_KERNEL (tuning / tests) = "gather" or "dataflow" forces 1 or 2 on large meshes; by
+// default the dataflow kernel runs when the pattern allows it and every CTA gets enough chunks to
+// amortise its pipeline.  The choice depends only on the mesh: results stay reproducible.
+int spmv_kind(const Pattern& pat) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = std::getenv("FSFEM_SPMV_KERNEL");
+    forced = !e ? 0 : (std::strcmp(e, "gather") == 0 ? 1 : (std::strcmp(e, "dataflow") == 0 ? 2 : 0));
+    FS_CUDA(cudaFuncSetAttribute(k_spmv_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
+    FS_CUDA(cudaFuncSetAttribute(k_spmv_df<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
+  }
+  if (pat.nchunks < num_sms()) return 0;
+  if (forced == 1 || !pat.df_ok) return 1;
+  if (forced == 2) return 2;
+  return pat.nchunks >= static_cast<int64_t>(kDfMinChunksPerCta) * df_grid() ? 2 : 1;
 }
 
 void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
@@ -727,6 +1224,38 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     kern<<<g, kThreads, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.tptr.get(), pat.tlist.get(), vals, pat.nloc, x_full,
                                 own_off, y, st, part);
     FS_LAUNCH_CHECK();
+    return;
+  }
+  if (spmv_kind(pat) == 2) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::max(1, std::min(nch, df_grid())));
+    cfg.blockDim = dim3(kDfThreads);
+    cfg.dynamicSmemBytes = kDfSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // phase-2 waits need every CTA resident
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const SpmvChunk* chp = pat.chunks.get();
+    const int64_t* spp = pat.sptr.get();
+    const int64_t* tpp = pat.tptr.get();
+    const int32_t* snp = pat.snbr.get();
+    const int32_t* tps = pat.tpos.get();
+    const int32_t* dpp = pat.dep_ptr.get();
+    const int2* dpl = pat.dep_list.get();
+    uint32_t* cnt = pat.cnt.get();
+    uint32_t* rdy = pat.cflags.get();
+    double* dtc = pat.dotc.get();
+    uint32_t* syn = pat.sync.get();
+    double* tb = pat.tbuf.get();
+    if (pcg)
+      FS_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_df<true>, chp, nch, spp, tpp, snp, tps, vals, dpp, dpl, cnt, rdy, dtc, syn,
+                                 tb, x_full, own_off, y, st));
+    else
+      FS_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_df<false>, chp, nch, spp, tpp, snp, tps, vals, dpp, dpl, cnt, rdy, dtc, syn,
+                                 tb, x_full, own_off, y, st));
+    count_launch();
     return;
   }
   if (pcg)

@@ -68,6 +68,7 @@ __device__ __forceinline__ void finish_beta(PcgState* st, double rr, double rz) 
 }
 
 int pcg_grid();
+int spmv_kind(const Pattern& pat);  // 0 small, 1 gather, 2 dataflow (pcg.cu)
 void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
                  PcgState* st, double* part, bool pcg, cudaStream_t s);
 void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,

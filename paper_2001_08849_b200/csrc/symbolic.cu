@@ -239,6 +239,53 @@ __global__ void k_split_trans(const int64_t* __restrict__ node_ptr, const int32_
   }
 }
 
+// Push SpMV support: tpos[b] = slot of stored block b in the transposed list of its column row.
+__global__ void k_tpos(const int2* __restrict__ tlist, int64_t ntb, int32_t* __restrict__ tpos) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntb; k += (int64_t)gridDim.x * blockDim.x)
+    tpos[tlist[k].x] = static_cast<int32_t>(k);
+}
+
+// Warp per chunk c: the distinct chunks d < c that hold a producer row (j of a transposed entry
+// (K_ji, j) of the chunk's rows), ascending; more than kMaxDeps -> ndeps = -1 and the waiter
+// checks the whole range [deps[0], c).
+constexpr int kDepWarps = 4;
+__global__ void __launch_bounds__(kDepWarps * 32) k_chunk_deps(const SpmvChunk* __restrict__ ch, int nch,
+                                                                const int2* __restrict__ tlist, int64_t n_lo,
+                                                                int32_t* __restrict__ deps, int32_t* __restrict__ ndeps) {
+  __shared__ int32_t pcs[kDepWarps][kCapBlocks];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = blockIdx.x * kDepWarps + w; c < nch; c += gridDim.x * kDepWarps) {
+    const int Pt0 = ch[c].Pt0, n = ch[c].Pt1 - Pt0;
+    for (int k = lane; k < n; k += 32) {
+      const int32_t j = static_cast<int32_t>(tlist[Pt0 + k].y - n_lo);
+      int lo = 0, hi = c;  // last chunk d <= c with ch[d].n0 <= j
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ch[mid].n0 <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      pcs[w][k] = lo;
+    }
+    __syncwarp();
+    int last = -1, cnt = 0;
+    while (cnt <= kMaxDeps) {
+      int m = 0x7fffffff;
+      for (int k = lane; k < n; k += 32) {
+        const int v = pcs[w][k];
+        if (v < c && v > last) m = min(m, v);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (m == 0x7fffffff) break;
+      if (lane == 0 && cnt < kMaxDeps) deps[static_cast<int64_t>(c) * kMaxDeps + cnt] = m;
+      ++cnt;
+      last = m;
+    }
+    if (lane == 0) ndeps[c] = cnt <= kMaxDeps ? cnt : -1;
+    __syncwarp();
+  }
+}
+
 // Expand the symmetric block storage to the public CSR (row_ptr int64, col_idx int32, vals):
 // row 3i+a lists columns 3j+c for j in nbr(i) ascending.  In nbr order a row is
 // [halo stored (j < n_lo)] [transposed (n_lo <= j < i)] [stored j >= i]; the diagonal is the
@@ -411,6 +458,64 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   pat.chunks.ensure(std::max<size_t>(ch.size(), 1));
   if (!ch.empty())
     FS_CUDA(cudaMemcpyAsync(pat.chunks.get(), ch.data(), sizeof(SpmvChunk) * ch.size(), cudaMemcpyHostToDevice, s));
+  // push SpMV: slots of the stored blocks, per-chunk producer lists, fresh flags and epoch
+  pat.tpos.ensure(pat.nsb + 4);
+  pat.tbuf.ensure(3 * pat.ntb + 2);
+  pat.deps.ensure(std::max<int64_t>(pat.nchunks, 1) * kMaxDeps);
+  pat.ndeps.ensure(std::max<int64_t>(pat.nchunks, 1));
+  pat.cflags.ensure(std::max<int64_t>(pat.nchunks, 1));
+  pat.sync.ensure(2);
+  FS_CUDA(cudaMemsetAsync(pat.tpos.get(), 0xff, sizeof(int32_t) * (pat.nsb + 4), s));
+  FS_CUDA(cudaMemsetAsync(pat.cflags.get(), 0, sizeof(uint32_t) * std::max<int64_t>(pat.nchunks, 1), s));
+  FS_CUDA(cudaMemsetAsync(pat.sync.get(), 0, sizeof(uint32_t) * 2, s));
+  if (pat.ntb > 0) {
+    const int gp = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pat.ntb, 256), 8LL * sms)));
+    k_tpos<<<gp, 256, 0, s>>>(pat.tlist.get(), pat.ntb, pat.tpos.get());
+    FS_LAUNCH_CHECK();
+  }
+  if (pat.nchunks > 0) {
+    const int gd = static_cast<int>(std::min<int64_t>(ceil_div(pat.nchunks, kDepWarps), 16LL * sms));
+    k_chunk_deps<<<gd, kDepWarps * 32, 0, s>>>(pat.chunks.get(), static_cast<int>(pat.nchunks), pat.tlist.get(), n_lo,
+                                               pat.deps.get(), pat.ndeps.get());
+    FS_LAUNCH_CHECK();
+    // reverse lists for the dataflow SpMV (host, once per pattern)
+    const int64_t nch = pat.nchunks;
+    std::vector<int32_t> hnd(nch), hdeps(nch * kMaxDeps);
+    FS_CUDA(cudaMemcpyAsync(hnd.data(), pat.ndeps.get(), sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaMemcpyAsync(hdeps.data(), pat.deps.get(), sizeof(int32_t) * nch * kMaxDeps, cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaStreamSynchronize(s));
+    pat.df_ok = true;
+    std::vector<int32_t> hneed(nch), hptr(nch + 1, 0);
+    for (int64_t c = 0; c < nch; ++c) {
+      if (hnd[c] < 0) {
+        pat.df_ok = false;
+        break;
+      }
+      hneed[c] = hnd[c] + 1;
+      hptr[c + 1] += 1;  // c needs itself
+      for (int k = 0; k < hnd[c]; ++k) hptr[hdeps[c * kMaxDeps + k] + 1] += 1;
+    }
+    if (pat.df_ok) {
+      for (int64_t c = 0; c < nch; ++c) hptr[c + 1] += hptr[c];
+      std::vector<int2> hlist(hptr[nch]);
+      std::vector<int32_t> fill(hptr.begin(), hptr.end() - 1);
+      for (int64_t c = 0; c < nch; ++c) hlist[fill[c]++] = make_int2(static_cast<int32_t>(c), hneed[c]);
+      for (int64_t c = 0; c < nch; ++c)
+        for (int k = 0; k < hnd[c]; ++k) {
+          const int32_t d = hdeps[c * kMaxDeps + k];
+          hlist[fill[d]++] = make_int2(static_cast<int32_t>(c), hneed[c]);
+        }
+      pat.dep_ptr.ensure(nch + 1);
+      pat.dep_list.ensure(std::max<size_t>(hlist.size(), 1));
+      pat.cnt.ensure(nch);
+      pat.dotc.ensure(nch);
+      FS_CUDA(cudaMemcpyAsync(pat.dep_ptr.get(), hptr.data(), sizeof(int32_t) * (nch + 1), cudaMemcpyHostToDevice, s));
+      FS_CUDA(cudaMemcpyAsync(pat.dep_list.get(), hlist.data(), sizeof(int2) * hlist.size(), cudaMemcpyHostToDevice,
+                              s));
+      FS_CUDA(cudaMemsetAsync(pat.cnt.get(), 0, sizeof(uint32_t) * nch, s));
+      FS_CUDA(cudaStreamSynchronize(s));
+    }
+  }
   FS_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -39,7 +39,7 @@ class FsfemReport(ctypes.Structure):
                 ("t_spmv_ms", ctypes.c_double), ("spmv_launches", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("stored_blocks", ctypes.c_int64),
                 ("transposed_blocks", ctypes.c_int64), ("spmv_bytes", ctypes.c_int64),
-                ("assembly_bytes", ctypes.c_int64)]
+                ("assembly_bytes", ctypes.c_int64), ("spmv_kernel", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -356,6 +356,24 @@ def test_cfg5_solution_properties(fs):
     assert np.all(u[fixed] == 0.0)
 
 
+def test_cfg5_displacements_match_oracle(fs):
+    """cfg5 (9.8M tets, randomly relabelled: the library renumbers internally and translates
+    back): compliance, tip deflection and 4096 sampled dofs against the oracle's full solve
+    (tests/golden/oracle_cfg5.json, scripts/oracle_full_solve.py 5: oracle/ only, ~80 min on CPU)."""
+    m = config_mesh(5)
+    g, u, rep = _gpu_solve(fs, m)
+    gold = _golden(5)
+    assert rep["converged"] == 1 and rep["reordered"] == 1
+    f = m.loads.reshape(-1)
+    assert abs(f @ u - gold["f_dot_u"]) <= 1e-8 * abs(gold["f_dot_u"])
+    tip = u.reshape(-1, 3)[m.tip, 2].mean()
+    assert abs(tip - gold["tip_mean_uz"]) <= 1e-7 * abs(gold["tip_mean_uz"])
+    idx = np.asarray(gold["u_sample_idx"])
+    assert np.abs(u[idx] - np.asarray(gold["u_sample"])).max() <= U_TOL * gold["u_norm"]
+    assert abs(np.linalg.norm(u) - gold["u_norm"]) <= U_TOL * gold["u_norm"]
+    assert abs(rep["iterations"] - gold["pcg"]["iterations"]) <= 0.05 * gold["pcg"]["iterations"]
+
+
 # ---------------------------------------------------------------- error paths and edge cases
 def test_not_converged_reports_and_writes_u(fs):
     from paper_2001_08849_b200 import fsfem_pcg_solve

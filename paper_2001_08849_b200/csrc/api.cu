@@ -30,10 +30,10 @@ void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr
                        cudaStream_t s);
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
                    const int32_t* face_opp, int64_t nf, double* face_s, double* face_V, cudaStream_t s);
-void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
-                          const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
-                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
-                          cudaStream_t s);
+void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* rec_b, bool tet,
+                            DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s);
+void assemble_rows_device(const Pattern& pat, const int32_t* face_nodes, const int32_t* face_opp,
+                          const double* face_s, double lam, double mu, double* vals, bool tet, cudaStream_t s);
 void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s);
 void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, const double* rec_V,
                     int64_t nrec,
@@ -135,7 +135,7 @@ struct fsfem_ctx {
   // numeric
   int method = FSFEM_METHOD_FS;
   double E = 0, nu = 0;
-  DevBuf<double> face_s, face_V, vals;  // assembly records (144 B per face / tet) and volumes
+  DevBuf<double> face_s, face_V, vals;  // assembly records (128 B per face / tet) and volumes
   // internal node order (reorder.cu): perm user -> internal, iperm internal -> user
   int reorder_mode = 0;  // 0 auto, 1 always, 2 never
   bool reordered = false;
@@ -535,12 +535,17 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
                            c->nloc, c->stream, c->scratch, c->pat, c->h_flags, c->method == FSFEM_METHOD_FEM_T4);
       fsfem_status s = decode_flags(c, c->h_flags[0], "symbolic");
       if (s != FSFEM_OK) return s;
+      const bool tet = c->method == FSFEM_METHOD_FEM_T4;
+      build_assembly_program(c->pat, tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet,
+                             c->scratch, c->h_flags, c->stream);
+      s = decode_flags(c, c->h_flags[0], "assembly program");
+      if (s != FSFEM_OK) return s;
       if (9 * c->pat.nblk >= (1LL << 31)) return fail(c, FSFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
       FS_CUDA(cudaEventRecord(c->ev1, c->stream));
       FS_CUDA(cudaEventSynchronize(c->ev1));
       c->rep.t_symbolic_ms = elapsed(c->ev0, c->ev1);
       c->vals.ensure(9 * c->pat.nsb + 2);  // + slack for the SpMV bulk copies (pattern.cuh)
-      c->face_s.ensure(18 * std::max(c->nf, c->nt));
+      c->face_s.ensure(16 * std::max(c->nf, c->nt));
       c->face_V.ensure(std::max(c->nf, c->nt));
       c->have_pattern = true;
       drop_graph(c);
@@ -550,15 +555,12 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
     if (c->method == FSFEM_METHOD_FEM_T4) {
       tet_s_device(c->xyz.get(), c->tets.get(), c->nt, c->face_s.get(), c->face_V.get(), c->stream);
-      assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(),
-                           c->tets.get(), nullptr, c->face_s.get(), c->n_lo, c->nloc, lam, mu, c->vals.get(),
-                           c->pat.max_row_blocks, true, c->stream);
+      assemble_rows_device(c->pat, c->tets.get(), nullptr, c->face_s.get(), lam, mu, c->vals.get(), true, c->stream);
     } else {
       face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
                     c->face_s.get(), c->face_V.get(), c->stream);
-      assemble_rows_device(c->pat.sptr.get(), c->pat.snbr.get(), c->pat.nf_ptr.get(), c->pat.nf_idx.get(),
-                           c->face_nodes.get(), c->face_opp.get(), c->face_s.get(), c->n_lo, c->nloc, lam, mu,
-                           c->vals.get(), c->pat.max_row_blocks, false, c->stream);
+      assemble_rows_device(c->pat, c->face_nodes.get(), c->face_opp.get(), c->face_s.get(), lam, mu, c->vals.get(),
+                           false, c->stream);
     }
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     FS_CUDA(cudaEventSynchronize(c->ev1));

@@ -13,24 +13,42 @@
 // and the global block K_IJ = lambda M_IJ + mu M_IJ^T + mu tr(M_IJ) I with
 // M_IJ = sum over faces holding I and J of s_I s_J^T, summed in ascending face id.
 #include "common.cuh"
+#include "pattern.cuh"
 
 namespace fsfem {
 
 namespace {
 
-// Assembly record of a face (FS) or tet (FEM-T4), 144 bytes = 9 x 16 B:
-//   doubles [0, 15): s_K for the 5 field nodes K (tets: 4; the 5th zero);
-//   bytes [120, 140): int32 field node ids (a, b, c, opp0, opp1) (tets: 4 nodes, -1); 4 B pad.
-// The domain volumes V_k live in a separate array (strain recovery).
-constexpr int kRec = 18;  // doubles per record
-__device__ __forceinline__ const int32_t* rec_field(const double* rec) {
-  return reinterpret_cast<const int32_t*>(rec + 15);
+// Assembly record of a face (FS) or tet (FEM-T4), 128 bytes = one line:
+//   doubles [0, 15): s_K for the 5 field nodes K (tets: 4; the 5th zero); [15]: V_k.
+// The field node ids are not stored: the assembly program (below) names them by position.
+constexpr int kRec = 16;  // doubles per record
+
+// Field nodes of record r: FS (a, b, c, opp0, opp1) from face_nodes / face_opp; FEM-T4 the
+// 4 tet nodes and -1.
+__device__ __forceinline__ void field_of(const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
+                                         bool tet, int64_t r, int32_t (&fld)[5]) {
+  if (tet) {
+    const int4 v = reinterpret_cast<const int4*>(rec_a)[r];
+    fld[0] = v.x;
+    fld[1] = v.y;
+    fld[2] = v.z;
+    fld[3] = v.w;
+    fld[4] = -1;
+  } else {
+    fld[0] = rec_a[3 * r];
+    fld[1] = rec_a[3 * r + 1];
+    fld[2] = rec_a[3 * r + 2];
+    fld[3] = rec_b[2 * r];
+    fld[4] = rec_b[2 * r + 1];
+  }
 }
 
 __device__ __forceinline__ void load3(const double* __restrict__ xyz, int32_t v, double& x, double& y, double& z) {
-  x = xyz[3 * v];
-  y = xyz[3 * v + 1];
-  z = xyz[3 * v + 2];
+  // (32-B padded coordinates with one 256-bit load per vertex were slower: 326 vs 291 us, cfg4)
+  x = __ldg(xyz + 3 * (int64_t)v);
+  y = __ldg(xyz + 3 * (int64_t)v + 1);
+  z = __ldg(xyz + 3 * (int64_t)v + 2);
 }
 
 // Thread per face: s_K for the field nodes K = (a, b, c, d, e) of face f.
@@ -109,10 +127,7 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
       st[3 * K + 1] = g[K][1] * rs;
       st[3 * K + 2] = g[K][2] * rs;
     }
-    int32_t* sfld = reinterpret_cast<int32_t*>(st + 15);
-#pragma unroll
-    for (int K = 0; K < 5; ++K) sfld[K] = fld[K];
-    sfld[5] = 0;
+    st[15] = Vf;
     if (valid) face_V[f] = Vf;
     __syncthreads();
     const int64_t fb = f - threadIdx.x;  // first face of this block-iteration
@@ -162,13 +177,7 @@ __global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, c
       out[h] = -(a + b + c);
     }
     out[12] = out[13] = out[14] = 0.0;
-    int32_t* ofld = reinterpret_cast<int32_t*>(out + 15);
-    ofld[0] = v.x;
-    ofld[1] = v.y;
-    ofld[2] = v.z;
-    ofld[3] = v.w;
-    ofld[4] = -1;
-    ofld[5] = 0;
+    out[15] = V;
     tet_V[t] = V;
   }
 }
@@ -201,8 +210,8 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
       for (int64_t k = f0; k < f1; ++k) {
         const int32_t f = nf_idx[k];
         const double* sf = face_s + kRec * static_cast<int64_t>(f);
-        const int32_t* rf = rec_field(sf);
-        const int32_t fld[5] = {rf[0], rf[1], rf[2], rf[3], rf[4]};
+        int32_t fld[5];
+        field_of(face_nodes, face_opp, kTet, f, fld);
         int pi = 0, pj = -1;
 #pragma unroll
         for (int K = 0; K < 5; ++K) {
@@ -239,36 +248,91 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
 }
 
 
-// Fast path, warp per own node i with <= 32 stored blocks (diagonal + j > i + halo j < n_lo).
-// Rounds of 32 records (faces of F(i), or tets for FEM-T4; ascending):
-//   load: the warp copies the round's 32 records (144 B each) into shared memory with
-//      coalesced 16-byte loads (9 warp instructions, each covering ~4 records), instead of
-//      each lane gathering its own record piece by piece (the L1 wavefront bound);
-//   A. lane = face: add s_i s_i^T to the lane's diagonal partial sum, and for every other field node
-//      that is a stored column of row i record (slot, s_K) and set the face's bit in the slot's
-//      mask (order-independent OR);
-//   B. lane = stored slot: walk the mask bits in ascending face order and add s_i s_K^T.
-// Summation order (fixed, independent of timing): off-diagonal blocks in ascending face id, or
-// for rows with <= 16 stored blocks (the common case) ascending over the even then the odd
-// positions of each 32-face round; the diagonal block as per-lane sums over faces lane,
-// lane+32, ... then a fixed warp tree.
+// Assembly program (once per pattern; thread per own node, faces of F(i) in ascending order):
+// nf_pi[k] = field position of i in the k-th face; for every other field node v that is a
+// stored column of row i (v > i, or a halo column v < n_lo) the entry k | (position of v) << 13
+// is appended to the list of v's stored block, so every list is ascending in k.
+constexpr int kProgMaxFaces = 8000;  // k < 8192 - 32 keeps the 0xffff sentinel above every round
+__device__ __forceinline__ int find_slot(const int32_t* __restrict__ cols, int ds, int32_t v) {
+  int lo = 0, hi = ds;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cols[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <bool kFill>
+__global__ void __launch_bounds__(256) k_prog(const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr,
+                                              const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx,
+                                              const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
+                                              bool tet, int64_t n_lo, int64_t nloc, uint8_t* __restrict__ nf_pi,
+                                              int32_t* __restrict__ cnt, const int32_t* __restrict__ blk_ent,
+                                              uint16_t* __restrict__ prog, unsigned long long* __restrict__ err) {
+  for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = static_cast<int32_t>(n_lo + il);
+    const int64_t P = sptr[il];
+    const int ds = static_cast<int>(sptr[il + 1] - P);
+    if (ds > 32) continue;  // generic path (no program)
+    const int64_t f0 = nf_ptr[il];
+    const int nfc = static_cast<int>(nf_ptr[il + 1] - f0);
+    if (nfc >= kProgMaxFaces) {
+      if (!kFill) report_error(err, FSFEM_ERR_UNSUPPORTED, i);
+      continue;
+    }
+    int cur[32];
+    if (kFill)
+      for (int q = 0; q < ds; ++q) cur[q] = blk_ent[P + q];
+    for (int k = 0; k < nfc; ++k) {
+      int32_t fld[5];
+      field_of(rec_a, rec_b, tet, nf_idx[f0 + k], fld);
+      int pi = 0;
+#pragma unroll
+      for (int K = 0; K < 5; ++K) pi = (fld[K] == i) ? K : pi;
+      if (!kFill) nf_pi[f0 + k] = static_cast<uint8_t>(pi);
+#pragma unroll
+      for (int K = 0; K < 5; ++K) {
+        const int32_t v = fld[K];
+        if (K == pi || v < 0 || (v < i && v >= n_lo)) continue;
+        const int sl = find_slot(snbr + P, ds, v);
+        if (kFill) prog[cur[sl]++] = static_cast<uint16_t>(k | (K << 13));
+        else ++cnt[P + sl];
+      }
+    }
+  }
+}
+
+// Fast path, warp per own node i with <= 32 stored blocks (diagonal + j > i + halo j < n_lo),
+// driven by the assembly program.  Rounds of 32 records (faces of F(i), or tets for FEM-T4;
+// ascending):
+//   load: the warp copies the round's 32 records (128 B each) into shared memory with coalesced
+//      16-byte cp.async (8 warp instructions);
+//   diagonal: lane = face, s_i s_i^T into the lane's partial sum (fixed warp tree at the end);
+//   off-diagonal: lane = stored slot walks its program entries of the round (ascending face),
+//      adding s_i s_K^T; rows with <= 16 stored blocks give every slot two lanes, one for the
+//      even and one for the odd entries, combined at the end in that order.
+// Summation order is fixed by the program: results do not depend on timing.
 constexpr int kRowWarps = 4;
 #ifndef FSFEM_ASM_MINB
-#define FSFEM_ASM_MINB 6
+#define FSFEM_ASM_MINB 8
 #endif
-constexpr int kMaxTargets = 4;  // other field nodes of a face
+// Shared-memory record stride (doubles).  128-B records at a 128-B stride put every record's
+// s_K in the same banks (32-way conflicts when the lanes of a warp read the same K of different
+// records).  18 doubles (144 B) spreads them over 8 bank offsets with 16-B copies: 581 us vs
+// 806 us at 16 and 654 us at 17 (odd stride: conflict-free reads but 8-B copies), cfg4.
+#ifndef FSFEM_ASM_STRIDE
+#define FSFEM_ASM_STRIDE 18
+#endif
+constexpr int kSh = FSFEM_ASM_STRIDE;
 
-template <bool kTet>
-__global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_rows2(
+__global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_rows3(
     const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
-    const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
-    const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals) {
-  __shared__ __align__(16) double sh_rec[kRowWarps][32][kRec];
-  __shared__ int32_t sh_cols[kRowWarps][32];
-  __shared__ unsigned sh_mask[kRowWarps][32];
-  __shared__ int8_t sh_pi[kRowWarps][32];
-  __shared__ int8_t sh_tslot[kRowWarps][32][kMaxTargets];
-  __shared__ int8_t sh_tk[kRowWarps][32][kMaxTargets];
+    const int32_t* __restrict__ nf_idx, const uint8_t* __restrict__ nf_pi, const int32_t* __restrict__ blk_ent,
+    const uint16_t* __restrict__ prog, const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam,
+    double mu, double* __restrict__ vals) {
+  __shared__ __align__(16) double sh_rec[kRowWarps][32][kSh];
+  __shared__ uint8_t sh_pi[kRowWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t il = blockIdx.x * (int64_t)kRowWarps + w; il < nloc; il += (int64_t)gridDim.x * kRowWarps) {
     const int32_t self = static_cast<int32_t>(n_lo + il);
@@ -276,84 +340,74 @@ __global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_row
     const int ds = static_cast<int>(sptr[il + 1] - P);
     if (ds > 32) continue;  // generic path
     const bool split = ds <= 16;
-    sh_cols[w][lane] = lane < ds ? snbr[P + lane] : 0x7fffffff;
-    sh_mask[w][lane] = 0u;
+    const int slot = split ? (lane & 15) : lane;
+    const int step = split ? 2 : 1;
+    int e = 0, e_end = 0;
+    if (slot < ds) {
+      e = blk_ent[P + slot] + (split ? (lane >> 4) : 0);
+      e_end = blk_ent[P + slot + 1];
+    }
+    uint32_t ent = e < e_end ? prog[e] : 0xffffu;
+    const int32_t my_col = lane < ds ? snbr[P + lane] : -1;
     const int64_t f0 = nf_ptr[il];
     const int nfc = static_cast<int>(nf_ptr[il + 1] - f0);
     double d[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // diagonal partial: xx yy zz xy xz yz
     double M[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) M[q] = 0.0;
-    __syncwarp();
     for (int rb = 0; rb < nfc; rb += 32) {
-      // ---- load the round's records: chunk c = 16-byte piece (c % 9) of record (c / 9)
       const int nact = min(32, nfc - rb);
       const int32_t myr = lane < nact ? nf_idx[f0 + rb + lane] : 0;
-      // 16-byte cp.async (LDGSTS): global -> shared without registers, all 9 in flight
+      const int mypi = lane < nact ? nf_pi[f0 + rb + lane] : 0;
+      if (kSh % 2 == 0) {  // 16-B pieces (record slots 16-B aligned)
 #pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        const int c = lane + 32 * q;
-        const int k = c / 9, part = c - 9 * k;
-        const int32_t r = __shfl_sync(0xffffffffu, myr, k);
-        if (k < nact) {
-          const double2* src = reinterpret_cast<const double2*>(face_s + kRec * static_cast<int64_t>(r)) + part;
-          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&sh_rec[w][0][0])) + 16u * c;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        for (int q = 0; q < 8; ++q) {
+          const int c = lane + 32 * q;
+          const int k = c >> 3, part = c & 7;
+          const int32_t r = __shfl_sync(0xffffffffu, myr, k);
+          if (k < nact) {
+            const double2* src = reinterpret_cast<const double2*>(face_s + kRec * static_cast<int64_t>(r)) + part;
+            const uint32_t dst =
+                static_cast<uint32_t>(__cvta_generic_to_shared(&sh_rec[w][k][0])) + 16u * static_cast<uint32_t>(part);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+          }
+        }
+      } else {  // 8-B pieces (odd stride)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int c = lane + 32 * q;
+          const int k = c >> 4, part = c & 15;
+          const int32_t r = __shfl_sync(0xffffffffu, myr, k);
+          if (k < nact) {
+            const double* src = face_s + kRec * static_cast<int64_t>(r) + part;
+            const uint32_t dst =
+                static_cast<uint32_t>(__cvta_generic_to_shared(&sh_rec[w][k][0])) + 8u * static_cast<uint32_t>(part);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+          }
         }
       }
+      sh_pi[w][lane] = static_cast<uint8_t>(mypi);
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       __syncwarp();
-      // ---- A: lane = face
       if (lane < nact) {
         const double* sf = sh_rec[w][lane];
-        const int32_t* rf = rec_field(sf);
-        int32_t fld[5];
-#pragma unroll
-        for (int K = 0; K < 5; ++K) fld[K] = rf[K];
-        int pi = 0;
-#pragma unroll
-        for (int K = 0; K < 5; ++K) pi = (fld[K] == self) ? K : pi;
-        const double s0 = sf[3 * pi], s1 = sf[3 * pi + 1], s2 = sf[3 * pi + 2];
-        sh_pi[w][lane] = static_cast<int8_t>(pi);
+        const double s0 = sf[3 * mypi], s1 = sf[3 * mypi + 1], s2 = sf[3 * mypi + 2];
         d[0] = fma(s0, s0, d[0]);
         d[1] = fma(s1, s1, d[1]);
         d[2] = fma(s2, s2, d[2]);
         d[3] = fma(s0, s1, d[3]);
         d[4] = fma(s0, s2, d[4]);
         d[5] = fma(s1, s2, d[5]);
-        int t = 0;
-#pragma unroll
-        for (int K = 0; K < 5; ++K) {
-          const int32_t v = fld[K];
-          if (K == pi || v < 0 || (v < self && v >= n_lo)) continue;
-          // binary search of v in the stored columns (ascending, padded with INT_MAX)
-          int lo = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1)
-            if (sh_cols[w][lo + step - 1] < v) lo += step;
-          sh_tslot[w][lane][t] = static_cast<int8_t>(lo);
-          sh_tk[w][lane][t] = static_cast<int8_t>(K);
-          atomicOr(&sh_mask[w][lo], 1u << lane);
-          ++t;
-        }
-        for (; t < kMaxTargets; ++t) sh_tslot[w][lane][t] = -1;
       }
-      __syncwarp();
-      // ---- B: lane = stored slot; rows with <= 16 stored blocks give every slot 2 lanes, one for
-      // the even and one for the odd record positions (combined at the end in that order)
-      const int slot = split ? (lane & 15) : lane;
-      unsigned m = sh_mask[w][slot];
-      if (split) m &= (lane < 16) ? 0x55555555u : 0xAAAAAAAAu;
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        int t = 0;
-#pragma unroll
-        for (int q = 1; q < kMaxTargets; ++q) t = (sh_tslot[w][b][q] == slot) ? q : t;
-        const double* rb_ = sh_rec[w][b];
-        const int pb = sh_pi[w][b], K = sh_tk[w][b][t];
-        const double a0 = rb_[3 * pb], a1 = rb_[3 * pb + 1], a2 = rb_[3 * pb + 2];
-        const double c0 = rb_[3 * K], c1 = rb_[3 * K + 1], c2 = rb_[3 * K + 2];
+      const uint32_t kend = static_cast<uint32_t>(rb + 32);
+      while ((ent & 0x1fffu) < kend) {  // (0xffff: no more entries; its k = 8191 >= any kend)
+        const int kl = static_cast<int>(ent & 0x1fffu) - rb, K = static_cast<int>(ent >> 13);
+        e += step;
+        const uint32_t nxt = e < e_end ? prog[e] : 0xffffu;
+        const double* rf = sh_rec[w][kl];
+        const int pb = sh_pi[w][kl];
+        const double a0 = rf[3 * pb], a1 = rf[3 * pb + 1], a2 = rf[3 * pb + 2];
+        const double c0 = rf[3 * K], c1 = rf[3 * K + 1], c2 = rf[3 * K + 2];
         M[0] = fma(a0, c0, M[0]);
         M[1] = fma(a0, c1, M[1]);
         M[2] = fma(a0, c2, M[2]);
@@ -363,12 +417,11 @@ __global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_row
         M[6] = fma(a2, c0, M[6]);
         M[7] = fma(a2, c1, M[7]);
         M[8] = fma(a2, c2, M[8]);
+        ent = nxt;
       }
       __syncwarp();
-      sh_mask[w][lane] = 0u;
-      __syncwarp();
     }
-    if (split) {  // slot s = (even records) + (odd records): lane s adds lane s+16's partial
+    if (split) {  // slot s = (even entries) + (odd entries): lane s adds lane s+16's partial
 #pragma unroll
       for (int q = 0; q < 9; ++q) M[q] += __shfl_down_sync(0xffffffffu, M[q], 16);
     }
@@ -376,7 +429,6 @@ __global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_row
 #pragma unroll
     for (int q = 0; q < 6; ++q) d[q] = warp_sum(d[q]);
     double* blocks = vals + 9 * P;
-    const int32_t my_col = sh_cols[w][lane];
     if (lane < ds && my_col == self) {
       const double Md[9] = {d[0], d[3], d[4], d[3], d[1], d[5], d[4], d[5], d[2]};
 #pragma unroll
@@ -405,29 +457,64 @@ void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_n
   FS_LAUNCH_CHECK();
 }
 
+// Assembly program of the pattern (once; pattern.cuh).  rec_a/rec_b: FS face_nodes/face_opp,
+// FEM-T4 tets/unused.  Returns the error word (kNoError if fine).
+void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* rec_b, bool tet,
+                            DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s) {
+  const int64_t nloc = pat.nloc, nsb = pat.nsb;
+  pat.nf_pi.ensure(std::max<int64_t>(pat.nfi, 1));
+  pat.blk_ent.ensure(nsb + 1);
+  const size_t tb = scan_tmp_bytes(nsb + 1);
+  const size_t o_cnt = 0, o_flags = (sizeof(int32_t) * (nsb + 1) + 255) & ~size_t(255),
+               o_tmp = o_flags + 256;
+  unsigned char* base = scratch.ensure(o_tmp + tb);
+  int32_t* cnt = reinterpret_cast<int32_t*>(base + o_cnt);
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(base + o_flags);
+  FS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nsb + 1), s));
+  FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 16LL * num_sms())));
+  if (nloc > 0) {
+    k_prog<false><<<g, 256, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
+                                    tet, pat.n_lo, nloc, pat.nf_pi.get(), cnt, nullptr, nullptr, flags);
+    FS_LAUNCH_CHECK();
+  }
+  exclusive_scan_i32(cnt, pat.blk_ent.get(), nsb, s, base + o_tmp, tb);
+  int32_t total = 0;
+  FS_CUDA(cudaMemcpyAsync(&total, pat.blk_ent.get() + nsb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  if (h_flags[0] != kNoError) return;
+  pat.prog.ensure(std::max<int64_t>(total, 1));
+  if (nloc > 0) {
+    k_prog<true><<<g, 256, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
+                                   tet, pat.n_lo, nloc, nullptr, nullptr, pat.blk_ent.get(), pat.prog.get(), flags);
+    FS_LAUNCH_CHECK();
+  }
+  pat.have_prog = true;
+}
+
 // rec_a/rec_b: FS (kTet = false) face_nodes/face_opp; FEM-T4 (tet = true) tets/unused.
-void assemble_rows_device(const int64_t* node_ptr, const int32_t* nbr, const int64_t* nf_ptr, const int32_t* nf_idx,
-                          const int32_t* face_nodes, const int32_t* face_opp, const double* face_s, int64_t n_lo,
-                          int64_t nloc, double lam, double mu, double* vals, int64_t max_row_blocks, bool tet,
-                          cudaStream_t s) {
+void assemble_rows_device(const Pattern& pat, const int32_t* face_nodes, const int32_t* face_opp,
+                          const double* face_s, double lam, double mu, double* vals, bool tet, cudaStream_t s) {
+  const int64_t nloc = pat.nloc;
   if (nloc == 0) return;
   // Persistent grid of exactly the resident CTAs: warp w takes nodes w, w + W, ... so the nodes in
   // flight form one contiguous window that slides forward; the field nodes of a face (which span
   // less than two windows in a banded numbering) are then assembled close together in time and
   // the face's record is re-read from L2, not DRAM.
-  auto k2 = tet ? k_assemble_rows2<true> : k_assemble_rows2<false>;
-  static int per_sm[2] = {0, 0};
-  if (per_sm[tet] == 0) FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[tet], k2, kRowWarps * 32, 0));
+  static int per_sm = 0;
+  if (per_sm == 0) FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assemble_rows3, kRowWarps * 32, 0));
   const int g2 = static_cast<int>(
-      std::min<int64_t>(ceil_div(nloc, kRowWarps), static_cast<int64_t>(std::max(1, per_sm[tet])) * num_sms()));
-  k2<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo, nloc,
-                                                lam, mu, vals);
+      std::min<int64_t>(ceil_div(nloc, kRowWarps), static_cast<int64_t>(std::max(1, per_sm)) * num_sms()));
+  k_assemble_rows3<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(),
+                                                              pat.nf_idx.get(), pat.nf_pi.get(), pat.blk_ent.get(),
+                                                              pat.prog.get(), face_s, pat.n_lo, nloc, lam, mu, vals);
   FS_LAUNCH_CHECK();
-  if (max_row_blocks > 32) {
+  if (pat.max_row_blocks > 32) {
     const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
     auto k1 = tet ? k_assemble_rows<true> : k_assemble_rows<false>;
-    k1<<<std::max(grid, 1), 256, 0, s>>>(node_ptr, nbr, nf_ptr, nf_idx, face_nodes, face_opp, face_s, n_lo, nloc, lam,
-                                         mu, vals, 32);
+    k1<<<std::max(grid, 1), 256, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(),
+                                         face_nodes, face_opp, face_s, pat.n_lo, nloc, lam, mu, vals, 32);
     FS_LAUNCH_CHECK();
   }
 }

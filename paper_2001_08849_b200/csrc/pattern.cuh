@@ -61,6 +61,13 @@ struct Pattern {
   DevBuf<double> dotc;       // [nchunks] per-chunk p.q partials
   DevBuf<int64_t> nf_ptr;    // [nloc+1]
   DevBuf<int32_t> nf_idx;    // [nfi] faces whose field holds node i, ascending
+  // Assembly program (assemble.cu, built once per pattern): for the k-th face of F(i) the field
+  // position of i (nf_pi), and per stored block (i, j) the faces of F(i) holding j with j's field
+  // position, ascending: prog[blk_ent[b] .. blk_ent[b+1]) = k | (position << 13).
+  bool have_prog = false;
+  DevBuf<uint8_t> nf_pi;     // [nfi]
+  DevBuf<int32_t> blk_ent;   // [nsb + 1]
+  DevBuf<uint16_t> prog;     // [blk_ent[nsb]]
 };
 
 }  // namespace fsfem

@@ -13,7 +13,7 @@ namespace fsfem {
 
 namespace {
 
-constexpr int kRecStride = 18;  // doubles per assembly record (assemble.cu): s_K at 3K
+constexpr int kRecStride = 16;  // doubles per assembly record (assemble.cu): s_K at 3K
 
 __device__ __forceinline__ void domain_field(const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
                                              bool tet, int64_t r, int32_t (&fld)[5]) {

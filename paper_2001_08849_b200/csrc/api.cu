@@ -662,7 +662,7 @@ fsfem_status fsfem_spmv(fsfem_ctx* c, const double* p, double* q) {
     c->x_full.ensure(nfull);
     c->q.ensure(std::max<int64_t>(3 * c->nloc, 1));
     node_in(c, p, 3, c->x_full.get());
-    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
+    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
     node_out(c, q, c->q.get(), c->n_lo, c->nloc, 3);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
@@ -701,7 +701,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     const double* q0 = nullptr;
     if (!u0_is_zero) {
       node_in(c, u, 3, c->x_full.get());
-      launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
+      launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
       q0 = c->q.get();
     }
     launch_init(c->f.get(), q0, c->dinv.get(), c->r.get(), own_p, n, st, c->part.get(), c->stream);
@@ -753,7 +753,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     // true residual ||f - K x|| / ||f||
     gather_full(c, c->x_full.get());
-    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 0, c->q.get(), nullptr, nullptr, false, c->stream);
+    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
     launch_resid(c->f.get(), c->q.get(), n, st, c->part.get(), c->stream);
     if (c->nranks > 1) combine(c, 3);
     node_out(c, u, c->x_full.get(), 0, c->nn, 3);

@@ -69,6 +69,8 @@ __device__ __forceinline__ void finish_beta(PcgState* st, double rr, double rz) 
 
 int pcg_grid();
 int spmv_kind(const Pattern& pat);  // 0 small, 1 gather, 2 dataflow (pcg.cu)
+// y (own rows) = K x_full; own_off = 3 * n_lo, the offset of the own rows in x_full (the dataflow
+// kernel forms K_ij^T x_i from the own slice, PCG also the p.q partial).
 void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
                  PcgState* st, double* part, bool pcg, cudaStream_t s);
 void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,

@@ -76,3 +76,50 @@ def test_gather_and_dataflow_agree_cfg4(tmp_path):
     assert np.abs(a["y0"] - b["y0"]).max() <= 1e-12 * np.abs(a["y0"]).max()
     assert np.linalg.norm(a["u0"] - b["u0"]) <= 1e-7 * np.linalg.norm(a["u0"])
     assert np.array_equal(b["y0"], b["y1"]) and np.array_equal(b["u0"], b["u1"])
+
+
+_PART_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from fsfem_inputs import config_mesh
+from paper_2001_08849_b200 import FsFem, load_library
+load_library()
+m = config_mesh(3)
+x = np.random.default_rng(11).standard_normal(3 * m.n_nodes)
+g = FsFem()
+g.build_faces(m.xyz, m.tets)
+g.assemble_csr(1.0e6, 0.3)
+full = g.spmv(x)
+res = {{"full": full}}
+for nranks in (2, 3):
+    chunk = -(-m.n_nodes // nranks)
+    for r in range(nranks):
+        lo, hi = min(m.n_nodes, r * chunk), min(m.n_nodes, (r + 1) * chunk)
+        h = FsFem()
+        h.comm_init(None, r, nranks)
+        h.build_faces(m.xyz, m.tets)
+        h.assemble_csr(1.0e6, 0.3)
+        res[f"q{{nranks}}_{{r}}"] = h.spmv(x)[3 * lo:3 * hi]
+        res[f"k{{nranks}}_{{r}}"] = np.array([h.report()["spmv_kernel"]])
+np.savez({out!r}, **res)
+"""
+
+
+@pytest.mark.parametrize("kernel", ["gather", "dataflow"])
+def test_spmv_kernel_row_partition(kernel, tmp_path):
+    """Partition-only contexts (2 and 3 ranks' rows on one GPU, halo columns below the rank's
+    range stored in the rows): each rank's rows of K x equal the single-context product."""
+    out = str(tmp_path / f"part_{kernel}.npz")
+    env = dict(os.environ, FSFEM_SPMV_KERNEL=kernel)
+    subprocess.run([sys.executable, "-c", _PART_SCRIPT.format(root=ROOT, out=out)], env=env, check=True, timeout=600)
+    r = np.load(out)
+    full = r["full"]
+    n_nodes = full.size // 3
+    want = 1 if kernel == "gather" else 2
+    for nranks in (2, 3):
+        chunk = -(-n_nodes // nranks)
+        for k in range(nranks):
+            lo, hi = min(n_nodes, k * chunk), min(n_nodes, (k + 1) * chunk)
+            q = r[f"q{nranks}_{k}"]
+            assert np.abs(q - full[3 * lo:3 * hi]).max() <= 1e-12 * np.abs(full).max()
+            assert int(r[f"k{nranks}_{k}"][0]) in (0, want)  # small partitions may fall back to warp per node

@@ -40,7 +40,8 @@ void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const 
                     const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
                     double* strain, double* stress, double* node_stress, double* node_vm, cudaStream_t s);
 double mean_tet_span_device(const int32_t* tets, int64_t nt, unsigned long long* d_tmp, cudaStream_t s);
-void morton_order_host(const double* d_xyz, int64_t nn, std::vector<int32_t>& iperm, cudaStream_t s);
+void morton_order_device(const double* d_xyz, int64_t nn, int32_t* iperm, int32_t* perm, DevBuf<unsigned char>& scratch,
+                         cudaStream_t s);
 void perm_ids_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s);
 void perm_ids_valid_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, int64_t nn,
                            cudaStream_t s);
@@ -462,15 +463,9 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
                        (c->reorder_mode == 0 && c->mean_span > 16.0 * std::pow(static_cast<double>(n_nodes), 2.0 / 3.0)));
     c->reordered = false;
     if (want) {
-      std::vector<int32_t> hi_perm, h_perm(n_nodes);
-      morton_order_host(c->xyz.get(), n_nodes, hi_perm, c->stream);
-      for (int64_t k = 0; k < n_nodes; ++k) h_perm[hi_perm[k]] = static_cast<int32_t>(k);
       c->iperm.ensure(n_nodes);
       c->perm.ensure(n_nodes);
-      FS_CUDA(cudaMemcpyAsync(c->iperm.get(), hi_perm.data(), sizeof(int32_t) * n_nodes, cudaMemcpyHostToDevice,
-                              c->stream));
-      FS_CUDA(cudaMemcpyAsync(c->perm.get(), h_perm.data(), sizeof(int32_t) * n_nodes, cudaMemcpyHostToDevice,
-                              c->stream));
+      morton_order_device(c->xyz.get(), n_nodes, c->iperm.get(), c->perm.get(), c->scratch, c->stream);
       // the matrix path works on the renumbered mesh; faces keep their ids and order
       DevBuf<double> xyz_i;
       xyz_i.ensure(3 * n_nodes);

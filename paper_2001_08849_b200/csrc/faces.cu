@@ -401,4 +401,13 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   *n_interior = static_cast<int64_t>(h_flags[1]);
 }
 
+// Coordinate bounding box (lo xyz, hi xyz) into bbox[6] on the device (min/max: exact, any order).
+void bbox_device(const double* d_xyz, int64_t nn, double* part /*[6 * 16 * num_sms]*/, double* bbox, cudaStream_t s) {
+  const int nbb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nn, 256), 16LL * num_sms())));
+  k_bbox_partial<<<nbb, 256, 0, s>>>(d_xyz, nn, part);
+  FS_LAUNCH_CHECK();
+  k_bbox_final<<<1, 256, 0, s>>>(part, nbb, bbox);
+  FS_LAUNCH_CHECK();
+}
+
 }  // namespace fsfem

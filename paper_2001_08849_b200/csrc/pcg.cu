@@ -573,6 +573,8 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
 #define FSFEM_DF_TIMING 0
 #endif
   long long tA = 0, tB = 0, tC = 0, tq0 = FSFEM_DF_TIMING ? clock64() : 0;
+  const long long t_begin = tq0;
+  (void)t_begin;
   int nitems = 0;
 #define DF_T(acc) if (FSFEM_DF_TIMING) { const long long tq1 = clock64(); acc += tq1 - tq0; tq0 = tq1; }
   if (warp == kWarps) {
@@ -813,16 +815,18 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         y[3 * il + 1] = s1;
         y[3 * il + 2] = s2;
       }
+#ifndef FSFEM_DF_NOPROXY
       asm volatile("fence.proxy.async.global;" ::: "memory");  // phase 2 reads them with bulk copies
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
 #if FSFEM_DF_TIMING
   if (lane == 0 && (warp == 0 || warp >= kWarps) && (blockIdx.x % 37) == 0)
-    printf("df blk %d %s K %d items %d: A %lld B %lld C %lld\n", blockIdx.x,
+    printf("df blk %d %s K %d items %d: A %lld B %lld C %lld end %lld\n", blockIdx.x,
            warp == kWarps ? "load" : (warp == kWarps + 1 ? "p2" : (warp > kWarps ? "count" : "comp")), K, nitems, tA,
-           tB, tC);
+           tB, tC, clock64() - t_begin);
 #endif
   // last CTA out: advances the epoch; PCG: p.q = sum of the per-chunk partials in chunk order
   __syncthreads();

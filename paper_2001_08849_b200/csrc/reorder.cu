@@ -132,17 +132,144 @@ int grid_for(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 16LL * num_sms())));
 }
 
-uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
-  v &= 0x1fffffULL;
-  v = (v | v << 32) & 0x1f00000000ffffULL;
-  v = (v | v << 16) & 0x1f0000ff0000ffULL;
-  v = (v | v << 8) & 0x100f00f00f00f00fULL;
-  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
-  v = (v | v << 2) & 0x1249249249249249ULL;
+
+// ---- Morton order on the device: 30-bit keys (10 bits per axis over one common cell size), then a
+// stable LSD radix sort (4 passes of 8 bits) of (key, node id) starting from id order, so equal
+// keys keep ascending ids: the order is a pure function of the coordinates.
+__device__ __forceinline__ uint32_t spread3_10(uint32_t v) {  // 10 bits -> every third bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
   return v;
 }
 
+__global__ void k_morton_keys(const double* __restrict__ xyz, int64_t nn, const double* __restrict__ bbox,
+                              uint32_t* __restrict__ key, int32_t* __restrict__ val) {
+  const double ext = fmax(bbox[3] - bbox[0], fmax(bbox[4] - bbox[1], bbox[5] - bbox[2]));
+  const double sc = ext > 0.0 ? 1023.0 / ext : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t k = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double q = (xyz[3 * i + a] - bbox[a]) * sc;
+      k |= spread3_10(static_cast<uint32_t>(fmin(fmax(q, 0.0), 1023.0))) << a;
+    }
+    key[i] = k;
+    val[i] = static_cast<int32_t>(i);
+  }
+}
+
+constexpr int kRsThreads = 256, kRsItems = 8, kRsTile = kRsThreads * kRsItems;
+
+// per-tile digit counts, digit-major: hist[d * ntiles + tile]
+__global__ void __launch_bounds__(kRsThreads) k_rs_hist(const uint32_t* __restrict__ key, int64_t n, int shift,
+                                                        int32_t* __restrict__ hist, int ntiles) {
+  __shared__ int32_t cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRsTile;
+  for (int r = 0; r < kRsItems; ++r) {
+    const int64_t i = base + r * kRsThreads + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[(key[i] >> shift) & 255u], 1);
+  }
+  __syncthreads();
+  hist[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+// stable scatter: items of a tile in round-major order (index = base + r * 256 + t), ranked by
+// warp match + per-warp counts + a running per-digit counter of the tile
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint32_t* __restrict__ key,
+                                                           const int32_t* __restrict__ val, int64_t n, int shift,
+                                                           const int32_t* __restrict__ off, int ntiles,
+                                                           uint32_t* __restrict__ key_out, int32_t* __restrict__ val_out) {
+  __shared__ int32_t run[256];
+  __shared__ int32_t wcnt[kRsThreads / 32][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  run[threadIdx.x] = off[static_cast<int64_t>(threadIdx.x) * ntiles + blockIdx.x];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kRsTile;
+  for (int r = 0; r < kRsItems; ++r) {
+    for (int k = threadIdx.x; k < (kRsThreads / 32) * 256; k += kRsThreads) (&wcnt[0][0])[k] = 0;
+    __syncthreads();
+    const int64_t i = base + r * kRsThreads + threadIdx.x;
+    const bool ok = i < n;
+    const uint32_t kk = ok ? key[i] : 0u;
+    const int32_t vv = ok ? val[i] : 0;
+    const int d = ok ? static_cast<int>((kk >> shift) & 255u) : 256 + lane;  // inactive lanes: unique dummies
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (ok && rank == 0) wcnt[w][d] = __popc(peers);
+    __syncthreads();
+    int before = 0;
+    if (ok)
+      for (int q = 0; q < w; ++q) before += wcnt[q][d];
+    if (ok) {
+      const int64_t pos = run[d] + before + rank;
+      key_out[pos] = kk;
+      val_out[pos] = vv;
+    }
+    __syncthreads();
+    {  // advance the running counters by this round's totals
+      int tot = 0;
+      for (int q = 0; q < kRsThreads / 32; ++q) tot += wcnt[q][threadIdx.x];
+      run[threadIdx.x] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_inverse_perm(const int32_t* __restrict__ iperm, int64_t n, int32_t* __restrict__ perm) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    perm[iperm[k]] = static_cast<int32_t>(k);
+}
+
 }  // namespace
+
+void bbox_device(const double* d_xyz, int64_t nn, double* part, double* bbox, cudaStream_t s);
+
+// iperm (internal -> user) and perm (user -> internal) of the Morton order, on the device.
+void morton_order_device(const double* d_xyz, int64_t nn, int32_t* iperm, int32_t* perm,
+                         DevBuf<unsigned char>& scratch, cudaStream_t s) {
+  if (nn <= 0) return;
+  const int ntiles = static_cast<int>(ceil_div(nn, kRsTile));
+  const int64_t nh = 256LL * ntiles;
+  size_t o = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t at = o;
+    o += (bytes + 255) & ~size_t(255);
+    return at;
+  };
+  const size_t o_part = carve(sizeof(double) * 6 * 16 * num_sms()), o_bb = carve(sizeof(double) * 8),
+               o_k0 = carve(4 * nn), o_k1 = carve(4 * nn), o_v1 = carve(4 * nn), o_h = carve(4 * (nh + 1)),
+               o_off = carve(4 * (nh + 1)), o_tmp = carve(scan_tmp_bytes(nh + 1));
+  unsigned char* b = scratch.ensure(o);
+  double* part = reinterpret_cast<double*>(b + o_part);
+  double* bb = reinterpret_cast<double*>(b + o_bb);
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(b + o_k0);
+  uint32_t* k1 = reinterpret_cast<uint32_t*>(b + o_k1);
+  int32_t* v0 = iperm;  // the values end in iperm after the 4th (even) pass
+  int32_t* v1 = reinterpret_cast<int32_t*>(b + o_v1);
+  int32_t* hist = reinterpret_cast<int32_t*>(b + o_h);
+  int32_t* off = reinterpret_cast<int32_t*>(b + o_off);
+  bbox_device(d_xyz, nn, part, bb, s);
+  k_morton_keys<<<grid_for(nn), 256, 0, s>>>(d_xyz, nn, bb, k0, v0);
+  FS_LAUNCH_CHECK();
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 8 * pass;
+    uint32_t* kin = (pass & 1) ? k1 : k0;
+    uint32_t* kout = (pass & 1) ? k0 : k1;
+    int32_t* vin = (pass & 1) ? v1 : v0;
+    int32_t* vout = (pass & 1) ? v0 : v1;
+    k_rs_hist<<<ntiles, kRsThreads, 0, s>>>(kin, nn, shift, hist, ntiles);
+    FS_LAUNCH_CHECK();
+    exclusive_scan_i32(hist, off, nh, s, b + o_tmp, scan_tmp_bytes(nh + 1));
+    k_rs_scatter<<<ntiles, kRsThreads, 0, s>>>(kin, vin, nn, shift, off, ntiles, kout, vout);
+    FS_LAUNCH_CHECK();
+  }
+  k_inverse_perm<<<grid_for(nn), 256, 0, s>>>(iperm, nn, perm);
+  FS_LAUNCH_CHECK();
+}
 
 // Mean tet id span (user numbering), exact.
 double mean_tet_span_device(const int32_t* tets, int64_t nt, unsigned long long* d_tmp, cudaStream_t s) {
@@ -156,30 +283,6 @@ double mean_tet_span_device(const int32_t* tets, int64_t nt, unsigned long long*
 }
 
 // Morton order of the nodes (host; once per mesh): iperm[k] = user id of the k-th node.
-void morton_order_host(const double* d_xyz, int64_t nn, std::vector<int32_t>& iperm, cudaStream_t s) {
-  std::vector<double> x(3 * nn);
-  FS_CUDA(cudaMemcpyAsync(x.data(), d_xyz, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaStreamSynchronize(s));
-  double lo[3] = {x[0], x[1], x[2]}, hi[3] = {x[0], x[1], x[2]};
-  for (int64_t i = 0; i < nn; ++i)
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = std::min(lo[a], x[3 * i + a]);
-      hi[a] = std::max(hi[a], x[3 * i + a]);
-    }
-  // one common cell size (the beam is long and thin: per-axis scaling would distort the curve)
-  const double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
-  const double sc = ext > 0 ? 2097151.0 / ext : 0.0;
-  std::vector<std::pair<uint64_t, int32_t>> key(nn);
-  for (int64_t i = 0; i < nn; ++i) {
-    uint64_t k = 0;
-    for (int a = 0; a < 3; ++a) k |= spread3(static_cast<uint64_t>((x[3 * i + a] - lo[a]) * sc)) << a;
-    key[i] = {k, static_cast<int32_t>(i)};
-  }
-  std::sort(key.begin(), key.end());
-  iperm.resize(nn);
-  for (int64_t k = 0; k < nn; ++k) iperm[k] = key[k].second;
-}
-
 void perm_ids_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   k_perm_ids<<<grid_for(n), 256, 0, s>>>(perm, in, out, n);

@@ -253,24 +253,21 @@ __global__ void __launch_bounds__(256) k_assemble_rows(
 // stored column of row i (v > i, or a halo column v < n_lo) the entry k | (position of v) << 13
 // is appended to the list of v's stored block, so every list is ascending in k.
 constexpr int kProgMaxFaces = 8000;  // k < 8192 - 32 keeps the 0xffff sentinel above every round
-__device__ __forceinline__ int find_slot(const int32_t* __restrict__ cols, int ds, int32_t v) {
-  int lo = 0, hi = ds;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (cols[mid] < v) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
 
+// Warp per own node; the faces of F(i) in rounds of 32 (lane = face).  Count pass: nf_pi and the
+// number of entries of every stored block (shared counters; order irrelevant).  Fill pass: per
+// round, slot by slot, the lanes holding the slot's column write in lane (= ascending face) order.
+constexpr int kProgWarps = 8;
 template <bool kFill>
-__global__ void __launch_bounds__(256) k_prog(const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr,
-                                              const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx,
-                                              const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b,
-                                              bool tet, int64_t n_lo, int64_t nloc, uint8_t* __restrict__ nf_pi,
-                                              int32_t* __restrict__ cnt, const int32_t* __restrict__ blk_ent,
-                                              uint16_t* __restrict__ prog, unsigned long long* __restrict__ err) {
-  for (int64_t il = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; il < nloc; il += (int64_t)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(kProgWarps * 32) k_prog(
+    const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
+    const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b, bool tet,
+    int64_t n_lo, int64_t nloc, uint8_t* __restrict__ nf_pi, int32_t* __restrict__ cnt,
+    const int32_t* __restrict__ blk_ent, uint16_t* __restrict__ prog, unsigned long long* __restrict__ err) {
+  __shared__ int32_t sh_cols[kProgWarps][32];
+  __shared__ int32_t sh_cnt[kProgWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t il = blockIdx.x * (int64_t)kProgWarps + w; il < nloc; il += (int64_t)gridDim.x * kProgWarps) {
     const int32_t i = static_cast<int32_t>(n_lo + il);
     const int64_t P = sptr[il];
     const int ds = static_cast<int>(sptr[il + 1] - P);
@@ -278,28 +275,53 @@ __global__ void __launch_bounds__(256) k_prog(const int64_t* __restrict__ sptr, 
     const int64_t f0 = nf_ptr[il];
     const int nfc = static_cast<int>(nf_ptr[il + 1] - f0);
     if (nfc >= kProgMaxFaces) {
-      if (!kFill) report_error(err, FSFEM_ERR_UNSUPPORTED, i);
+      if (!kFill && lane == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, i);
       continue;
     }
-    int cur[32];
-    if (kFill)
-      for (int q = 0; q < ds; ++q) cur[q] = blk_ent[P + q];
-    for (int k = 0; k < nfc; ++k) {
-      int32_t fld[5];
-      field_of(rec_a, rec_b, tet, nf_idx[f0 + k], fld);
-      int pi = 0;
+    sh_cols[w][lane] = lane < ds ? snbr[P + lane] : 0x7fffffff;
+    sh_cnt[w][lane] = (kFill && lane < ds) ? blk_ent[P + lane] : 0;
+    __syncwarp();
+    for (int rb = 0; rb < nfc; rb += 32) {
+      const int k = rb + lane;
+      int tslot[4] = {-1, -1, -1, -1}, tk[4] = {0, 0, 0, 0};
+      if (k < nfc) {
+        int32_t fld[5];
+        field_of(rec_a, rec_b, tet, nf_idx[f0 + k], fld);
+        int pi = 0;
 #pragma unroll
-      for (int K = 0; K < 5; ++K) pi = (fld[K] == i) ? K : pi;
-      if (!kFill) nf_pi[f0 + k] = static_cast<uint8_t>(pi);
+        for (int K = 0; K < 5; ++K) pi = (fld[K] == i) ? K : pi;
+        if (!kFill) nf_pi[f0 + k] = static_cast<uint8_t>(pi);
+        int t = 0;
 #pragma unroll
-      for (int K = 0; K < 5; ++K) {
-        const int32_t v = fld[K];
-        if (K == pi || v < 0 || (v < i && v >= n_lo)) continue;
-        const int sl = find_slot(snbr + P, ds, v);
-        if (kFill) prog[cur[sl]++] = static_cast<uint16_t>(k | (K << 13));
-        else ++cnt[P + sl];
+        for (int K = 0; K < 5; ++K) {
+          const int32_t v = fld[K];
+          if (K == pi || v < 0 || (v < i && v >= n_lo)) continue;
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1)
+            if (sh_cols[w][lo + step - 1] < v) lo += step;
+          tslot[t] = lo;
+          tk[t] = K;
+          ++t;
+          if (!kFill) atomicAdd(&sh_cnt[w][lo], 1);
+        }
+      }
+      if (kFill) {
+        for (int sl = 0; sl < ds; ++sl) {  // warp-uniform: lane order = ascending face order
+          int K = -1;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) K = (tslot[t] == sl) ? tk[t] : K;
+          const unsigned m = __ballot_sync(0xffffffffu, K >= 0);
+          if (K >= 0) prog[sh_cnt[w][sl] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(k | (K << 13));
+          __syncwarp();
+          if (lane == 0) sh_cnt[w][sl] += __popc(m);
+          __syncwarp();
+        }
       }
     }
+    __syncwarp();
+    if (!kFill && lane < ds) cnt[P + lane] = sh_cnt[w][lane];
+    __syncwarp();
   }
 }
 
@@ -472,9 +494,9 @@ void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* r
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(base + o_flags);
   FS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nsb + 1), s));
   FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
-  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 16LL * num_sms())));
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kProgWarps), 32LL * num_sms())));
   if (nloc > 0) {
-    k_prog<false><<<g, 256, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
+    k_prog<false><<<g, kProgWarps * 32, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
                                     tet, pat.n_lo, nloc, pat.nf_pi.get(), cnt, nullptr, nullptr, flags);
     FS_LAUNCH_CHECK();
   }
@@ -486,7 +508,7 @@ void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* r
   if (h_flags[0] != kNoError) return;
   pat.prog.ensure(std::max<int64_t>(total, 1));
   if (nloc > 0) {
-    k_prog<true><<<g, 256, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
+    k_prog<true><<<g, kProgWarps * 32, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
                                    tet, pat.n_lo, nloc, nullptr, nullptr, pat.blk_ent.get(), pat.prog.get(), flags);
     FS_LAUNCH_CHECK();
   }

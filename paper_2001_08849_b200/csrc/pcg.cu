@@ -251,22 +251,8 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
     if (cta_scalars(st, nullptr, unused)) return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // Chunk walk of this CTA: a contiguous range of chunks (x neighbours i+-1, i+-row reuse L1
-  // across consecutive chunks), or grid-strided (FSFEM_SPMV_CONTIG=0, tuning).
-#ifndef FSFEM_SPMV_CONTIG
-#define FSFEM_SPMV_CONTIG 0
-#endif
-  int c_first, c_end, c_step;
-  if (FSFEM_SPMV_CONTIG) {
-    const int per = (nchunks + gridDim.x - 1) / gridDim.x;
-    c_first = min(nchunks, static_cast<int>(blockIdx.x) * per);
-    c_end = min(nchunks, c_first + per);
-    c_step = 1;
-  } else {
-    c_first = blockIdx.x;
-    c_end = nchunks;
-    c_step = gridDim.x;
-  }
+  // chunk walk: grid-strided (contiguous ranges per CTA were slower)
+  const int c_first = blockIdx.x, c_end = nchunks, c_step = gridDim.x;
   if (threadIdx.x == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -815,9 +801,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         y[3 * il + 1] = s1;
         y[3 * il + 2] = s2;
       }
-#ifndef FSFEM_DF_NOPROXY
       asm volatile("fence.proxy.async.global;" ::: "memory");  // phase 2 reads them with bulk copies
-#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }

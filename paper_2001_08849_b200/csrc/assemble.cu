@@ -63,60 +63,55 @@ __global__ void __launch_bounds__(256) k_face_s(const double* __restrict__ xyz, 
     const int64_t f = fb0 + threadIdx.x;
     const bool valid = f < nf;
     const int64_t fc = valid ? f : fb0;  // inactive threads recompute face fb0 and write nothing extra
-    int32_t fld[5] = {face_nodes[3 * fc], face_nodes[3 * fc + 1], face_nodes[3 * fc + 2], face_opp[2 * fc],
-                      face_opp[2 * fc + 1]};
-    const int32_t tt[2] = {face_tet[2 * fc], face_tet[2 * fc + 1]};
+    // The two tets of the face are (a, b, c, d) and (a, b, c, e) with its field nodes
+    // (a, b, c, d, e) = (face nodes, opposite vertices of face_tet[0], face_tet[1]): only 5 distinct
+    // vertices, and each tet's vertex weights land on known field positions (no matching).  The
+    // weights do not depend on the vertex order of the tet: the sign of det fixes the orientation.
+    const int32_t na = face_nodes[3 * fc], nb = face_nodes[3 * fc + 1], nc = face_nodes[3 * fc + 2];
+    const int32_t nd = face_opp[2 * fc], ne = face_opp[2 * fc + 1];
+    double ax, ay, az, bx, by, bz, cx, cy, cz, dx, dy, dz;
+    load3(xyz, na, ax, ay, az);
+    load3(xyz, nb, bx, by, bz);
+    load3(xyz, nc, cx, cy, cz);
+    load3(xyz, nd, dx, dy, dz);
+    double ex = 0.0, ey = 0.0, ez = 0.0;
+    if (ne >= 0) load3(xyz, ne, ex, ey, ez);
+    const double e1x = bx - ax, e1y = by - ay, e1z = bz - az;
+    const double e2x = cx - ax, e2y = cy - ay, e2z = cz - az;
+    // e1 x e2 is shared by both tets (weight of the opposite vertex, up to the tet's scale)
+    const double c3x = e1y * e2z - e1z * e2y, c3y = e1z * e2x - e1x * e2z, c3z = e1x * e2y - e1y * e2x;
     double g[5][3];
-#pragma unroll
-    for (int K = 0; K < 5; ++K) g[K][0] = g[K][1] = g[K][2] = 0.0;
     double Vf = 0.0;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int32_t t = tt[e];
-      if (t < 0) continue;
-      const int4 v = reinterpret_cast<const int4*>(tets)[t];
-      const int32_t vid[4] = {v.x, v.y, v.z, v.w};
-      double x0, y0, z0, x1, y1, z1, x2, y2, z2, x3, y3, z3;
-      load3(xyz, v.x, x0, y0, z0);
-      load3(xyz, v.y, x1, y1, z1);
-      load3(xyz, v.z, x2, y2, z2);
-      load3(xyz, v.w, x3, y3, z3);
-      const double e1x = x1 - x0, e1y = y1 - y0, e1z = z1 - z0;
-      const double e2x = x2 - x0, e2y = y2 - y0, e2z = z2 - z0;
-      const double e3x = x3 - x0, e3y = y3 - y0, e3z = z3 - z0;
-      // c1 = e2 x e3, c2 = e3 x e1, c3 = e1 x e2 ; det = e1 . c1
-      double w[4][3];
-      w[1][0] = e2y * e3z - e2z * e3y;
-      w[1][1] = e2z * e3x - e2x * e3z;
-      w[1][2] = e2x * e3y - e2y * e3x;
-      w[2][0] = e3y * e1z - e3z * e1y;
-      w[2][1] = e3z * e1x - e3x * e1z;
-      w[2][2] = e3x * e1y - e3y * e1x;
-      w[3][0] = e1y * e2z - e1z * e2y;
-      w[3][1] = e1z * e2x - e1x * e2z;
-      w[3][2] = e1x * e2y - e1y * e2x;
-      const double det = e1x * w[1][0] + e1y * w[1][1] + e1z * w[1][2];
+    {  // tet (a, b, c, d)
+      const double e3x = dx - ax, e3y = dy - ay, e3z = dz - az;
+      const double c1x = e2y * e3z - e2z * e3y, c1y = e2z * e3x - e2x * e3z, c1z = e2x * e3y - e2y * e3x;
+      const double c2x = e3y * e1z - e3z * e1y, c2y = e3z * e1x - e3x * e1z, c2z = e3x * e1y - e3y * e1x;
+      const double det = e1x * c1x + e1y * c1y + e1z * c1z;
       const double sc = (det > 0.0 ? 1.0 : -1.0) * (1.0 / 24.0);
+      g[1][0] = c1x * sc; g[1][1] = c1y * sc; g[1][2] = c1z * sc;
+      g[2][0] = c2x * sc; g[2][1] = c2y * sc; g[2][2] = c2z * sc;
+      g[3][0] = c3x * sc; g[3][1] = c3y * sc; g[3][2] = c3z * sc;
+#pragma unroll
+      for (int h = 0; h < 3; ++h) g[0][h] = -(g[1][h] + g[2][h] + g[3][h]);
+      g[4][0] = g[4][1] = g[4][2] = 0.0;
+      Vf = fabs(det) * (1.0 / 24.0);
+    }
+    if (ne >= 0) {  // tet (a, b, c, e)
+      const double e3x = ex - ax, e3y = ey - ay, e3z = ez - az;
+      const double c1x = e2y * e3z - e2z * e3y, c1y = e2z * e3x - e2x * e3z, c1z = e2x * e3y - e2y * e3x;
+      const double c2x = e3y * e1z - e3z * e1y, c2y = e3z * e1x - e3x * e1z, c2z = e3x * e1y - e3y * e1x;
+      const double det = e1x * c1x + e1y * c1y + e1z * c1z;
+      const double sc = (det > 0.0 ? 1.0 : -1.0) * (1.0 / 24.0);
+      const double w1[3] = {c1x * sc, c1y * sc, c1z * sc}, w2[3] = {c2x * sc, c2y * sc, c2z * sc},
+                   w3[3] = {c3x * sc, c3y * sc, c3z * sc};
 #pragma unroll
       for (int h = 0; h < 3; ++h) {
-        w[1][h] *= sc;
-        w[2][h] *= sc;
-        w[3][h] *= sc;
-        w[0][h] = -(w[1][h] + w[2][h] + w[3][h]);
+        g[0][h] += -(w1[h] + w2[h] + w3[h]);
+        g[1][h] += w1[h];
+        g[2][h] += w2[h];
+        g[4][h] = w3[h];
       }
       Vf += fabs(det) * (1.0 / 24.0);
-      // scatter the tet's 4 vertex weights onto the field positions
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-#pragma unroll
-        for (int K = 0; K < 5; ++K) {
-          if (fld[K] == vid[q]) {
-            g[K][0] += w[q][0];
-            g[K][1] += w[q][1];
-            g[K][2] += w[q][2];
-          }
-        }
-      }
     }
     const double rs = 1.0 / sqrt(Vf);
     // stage the record of each face of the block in shared memory, then store coalesced

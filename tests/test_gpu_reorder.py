@@ -79,3 +79,22 @@ def test_auto_reorder_triggers_on_random_numbering(fs):
     # same beam: compare tip deflections (the two meshes are the same geometry and loads)
     tips = [u.reshape(-1, 3)[m.tip, 2].mean() for _, m, u in out.values()]
     assert abs(tips[0] - tips[1]) <= 1e-7 * abs(tips[0])
+
+
+def test_reordered_solve_is_bitwise_reproducible(fs):
+    """The internal Morton order (device radix sort, ties by node id) and everything after it are
+    pure functions of the input: two full runs on a randomly relabelled mesh give identical bytes."""
+    m = kuhn_beam(24, 6, 6, L=4.0, jitter=0.2, jitter_seed=3, node_perm_seed=5, tet_perm_seed=6)
+    outs = []
+    for _ in range(2):
+        g = fs()
+        g.set_reorder(1)
+        g.build_faces(m.xyz, m.tets)
+        g.assemble_csr(E, NU)
+        v = g.get_csr(with_pattern=False).vals.copy()
+        g.apply_bc(m.dirichlet, m.loads.reshape(-1))
+        u, rep = g.pcg_solve()
+        assert rep["reordered"] == 1
+        outs.append((v, u, rep["iterations"]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1]) and outs[0][2] == outs[1][2]

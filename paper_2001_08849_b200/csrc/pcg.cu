@@ -1202,7 +1202,10 @@ int spmv_kind(const Pattern& pat) {
     FS_CUDA(cudaFuncSetAttribute(k_spmv_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
     FS_CUDA(cudaFuncSetAttribute(k_spmv_df<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
   }
-  if (pat.nchunks < num_sms()) return 0;
+#ifndef FSFEM_SMALL_CHUNKS_PER_SM
+#define FSFEM_SMALL_CHUNKS_PER_SM 1
+#endif
+  if (pat.nchunks < FSFEM_SMALL_CHUNKS_PER_SM * num_sms()) return 0;
   if (forced == 1 || !pat.df_ok) return 1;
   if (forced == 2) return 2;
   return pat.nchunks >= static_cast<int64_t>(kDfMinChunksPerCta) * df_grid() ? 2 : 1;
@@ -1217,7 +1220,7 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     attr_set = true;
   }
   const int nch = static_cast<int>(pat.nchunks);
-  if (nch < num_sms()) {  // small mesh: plain warp-per-node kernel
+  if (spmv_kind(pat) == 0) {  // small mesh: plain warp-per-node kernel
     const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(pcg_grid(), ceil_div(pat.nloc, kWarps))));
     auto kern = pcg ? k_spmv_small<true> : k_spmv_small<false>;
     kern<<<g, kThreads, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.tptr.get(), pat.tlist.get(), vals, pat.nloc, x_full,

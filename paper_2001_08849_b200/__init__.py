@@ -25,6 +25,7 @@ from .fsfem import (  # noqa: F401
     fsfem_recover_stress,
     fsfem_set_method,
     fsfem_set_reorder,
+    fsfem_set_pcg_variant,
     fsfem_spmv,
     fsfem_surface_loads,
     load_library,

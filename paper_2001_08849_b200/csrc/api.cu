@@ -139,6 +139,8 @@ struct fsfem_ctx {
   DevBuf<double> face_s, face_V, vals;  // assembly records (128 B per face / tet) and volumes
   // internal node order (reorder.cu): perm user -> internal, iperm internal -> user
   int reorder_mode = 0;  // 0 auto, 1 always, 2 never
+  int pcg_variant = 0;   // FSFEM_PCG_STANDARD / FSFEM_PCG_SINGLE_REDUCTION
+  DevBuf<double> cg_p, cg_s;  // single-reduction variant: direction p and s = K p (own rows)
   bool reordered = false;
   double mean_span = 0.0;
   DevBuf<int32_t> perm, iperm, tmp_i;
@@ -290,7 +292,28 @@ void gather_full(fsfem_ctx* c, double* full) {
   FS_NCCL(nccl().AllGather(full + 3 * c->chunk * c->rank, full, 3 * c->chunk, ncclDouble, c->comm, c->stream));
 }
 
+// Single-reduction iteration (Chronopoulos-Gear): update (x, r, u = D^-1 r,
+// p, s; partials of r.u and r.r), [all-gather of u], SpMV w = K u with u.w, and ONE combined
+// reduction (u.w, r.u, r.r) -> alpha, beta.  p_full holds u, q holds w.
+void pcg_iteration_cg(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
+  PcgState* st = c->st.get();
+  double* own_u = c->p_full.get() + 3 * c->n_lo;
+  double* own_x = c->x_full.get() + 3 * c->n_lo;
+  const int64_t n = 3 * c->nloc;
+  launch_cg_update(own_x, c->r.get(), own_u, c->cg_p.get(), c->cg_s.get(), c->q.get(), c->dinv.get(), n, st,
+                   c->part.get() + 4 * pcg_grid(), c->stream);
+  if (c->nranks > 1) gather_full(c, c->p_full.get());
+  if (e0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+  launch_spmv(c->pat, c->vals.get(), c->p_full.get(), 3 * c->n_lo, c->q.get(), st, c->part.get(), true, c->stream);
+  if (e1) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  if (c->nranks > 1) combine(c, 4);
+}
+
 void pcg_iteration(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
+  if (c->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION) {
+    pcg_iteration_cg(c, e0, e1);
+    return;
+  }
   PcgState* st = c->st.get();
   double* own_p = c->p_full.get() + 3 * c->n_lo;
   double* own_x = c->x_full.get() + 3 * c->n_lo;
@@ -416,6 +439,16 @@ fsfem_status fsfem_set_method(fsfem_ctx* c, int method) {
       drop_graph(c);
       if (c->stage > kFaces) c->stage = kFaces;
     }
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_set_pcg_variant(fsfem_ctx* c, int variant) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (variant != FSFEM_PCG_STANDARD && variant != FSFEM_PCG_SINGLE_REDUCTION)
+      return fail(c, FSFEM_ERR_INVALID_ARG, "pcg variant must be 0 (standard) or 1 (single reduction)");
+    if (variant != c->pcg_variant) drop_graph(c);
+    c->pcg_variant = variant;
     return FSFEM_OK;
   });
 }
@@ -679,13 +712,22 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     c->p_full.ensure(nfull);
     c->r.ensure(std::max<int64_t>(n, 1));
     c->q.ensure(std::max<int64_t>(n, 1));
-    c->part.ensure(4 * static_cast<size_t>(pcg_grid()));
+    c->part.ensure(8 * static_cast<size_t>(pcg_grid()));  // SpMV / dot partials; [4g, 6g): update partials
     c->all.ensure(4 * static_cast<size_t>(c->nranks));
     PcgState* st = c->st.get();
     std::memset(c->h_st, 0, sizeof(PcgState));
     c->h_st->tol = rel_tol;
     c->h_st->max_iter = max_iter;
     c->h_st->nranks = c->nranks;
+    const bool cg1 = c->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION;
+    c->h_st->variant = cg1 ? 1 : 0;
+    c->h_st->cg_first = cg1 ? 1 : 0;
+    c->h_st->upd_part = c->part.get() + 4 * pcg_grid();
+    c->h_st->upd_n = cg_update_grid(n);
+    if (cg1) {
+      c->cg_p.ensure(std::max<int64_t>(n, 1));
+      c->cg_s.ensure(std::max<int64_t>(n, 1));
+    }
 
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
     FS_CUDA(cudaMemcpyAsync(st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
@@ -703,6 +745,12 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     if (c->nranks > 1) {
       combine(c, 0);
       gather_full(c, c->p_full.get());
+    }
+    if (cg1) {  // p = s = 0, then w = K u and the first alpha (u = D^-1 r is in p_full)
+      FS_CUDA(cudaMemsetAsync(c->cg_p.get(), 0, sizeof(double) * std::max<int64_t>(n, 1), c->stream));
+      FS_CUDA(cudaMemsetAsync(c->cg_s.get(), 0, sizeof(double) * std::max<int64_t>(n, 1), c->stream));
+      launch_spmv(c->pat, c->vals.get(), c->p_full.get(), 3 * c->n_lo, c->q.get(), st, c->part.get(), true, c->stream);
+      if (c->nranks > 1) combine(c, 4);
     }
     FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
     FS_CUDA(cudaStreamSynchronize(c->stream));
@@ -735,7 +783,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     while (c->h_st->done_d == 0.0) {
       const long long before = c->h_st->iters;
       FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
-      count_launch((c->nranks > 1 ? 5 : 2) * kBatch);
+      count_launch((c->nranks > 1 ? (cg1 ? 3 : 5) : 2) * kBatch);
       FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
       FS_CUDA(cudaStreamSynchronize(c->stream));
       const long long ran = std::min<long long>(kBatch, c->h_st->iters - before);

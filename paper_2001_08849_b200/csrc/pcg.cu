@@ -77,6 +77,43 @@ __device__ __forceinline__ bool grid_reduce(const double (&mine)[NV], double* pa
   return true;
 }
 
+// Last CTA of a PCG SpMV, all threads: dot = p.q (valid in thread 0).  Standard recurrence:
+// alpha.  Single-reduction variant: also sums the update kernel's partials of gamma and r.r in
+// CTA order (the one combined reduction of the iteration) and runs finish_cg.  Multi-rank: the
+// rank's sums go to st->local for the host-side collective.
+__device__ void spmv_finish(PcgState* st, double dot) {
+  __shared__ double sh_f[32];
+  const int variant = st->variant;  // uniform
+  if (variant == 0) {
+    if (threadIdx.x == 0) {
+      if (st->nranks > 1) st->local[0] = dot;
+      else finish_alpha(st, dot);
+    }
+    return;
+  }
+  const int first = st->cg_first;
+  double g = 0.0, rr = 0.0;
+  if (!first) {
+    const double* up = st->upd_part;
+    const int un = st->upd_n;
+    for (int k = threadIdx.x; k < un; k += blockDim.x) {
+      g += ld_cg(up + k);
+      rr += ld_cg(up + un + k);
+    }
+  }
+  g = block_sum(g, sh_f);
+  rr = block_sum(rr, sh_f);
+  if (threadIdx.x == 0) {
+    if (st->nranks > 1) {
+      st->local[0] = dot;
+      st->local[1] = g;
+      st->local[2] = rr;
+    } else {
+      finish_cg(st, dot, g, rr);
+    }
+  }
+}
+
 // SpMV over the symmetric block storage (pattern.cuh):
 //   y_i = sum_{stored j} K_ij x_j + sum_{n_lo <= j < i} K_ji^T x_j.
 //
@@ -399,13 +436,7 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   if (!kPcg) return;
   const double mine[1] = {dot};
   double out[1];
-  if (grid_reduce<1>(mine, part, &st->ticket[0], out) && threadIdx.x == 0) {
-    if (st->nranks > 1) {
-      st->local[0] = out[0];  // combined across ranks by the host-side collective
-    } else {
-      finish_alpha(st, out[0]);
-    }
-  }
+  if (grid_reduce<1>(mine, part, &st->ticket[0], out)) spmv_finish(st, out[0]);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -838,13 +869,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       for (int u = 0; u < U; ++u) a += v[u];
     }
     const double pq = block_sum(a, sh);
-    if (threadIdx.x == 0) {
-      if (st->nranks > 1) {
-        st->local[0] = pq;
-      } else {
-        finish_alpha(st, pq);
-      }
-    }
+    spmv_finish(st, pq);
   }
   if (threadIdx.x == 0) {
     sync[1] = 0u;
@@ -918,13 +943,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_small(const int64_t* __restri
   if (!kPcg) return;
   const double mine[1] = {dot};
   double out[1];
-  if (grid_reduce<1>(mine, part, &st->ticket[0], out) && threadIdx.x == 0) {
-    if (st->nranks > 1) {
-      st->local[0] = out[0];
-    } else {
-      finish_alpha(st, out[0]);
-    }
-  }
+  if (grid_reduce<1>(mine, part, &st->ticket[0], out)) spmv_finish(st, out[0]);
 }
 
 // Vector kernels: each thread takes kVec elements per pass at stride gridDim*blockDim (coalesced)
@@ -999,6 +1018,65 @@ __global__ void __launch_bounds__(kThreads) k_direction(double* __restrict__ p, 
       const int64_t k = b + j * T;
       if (k < n) p[k] = fma(beta, pv[j], dv[j] * rv[j]);
     }
+  }
+}
+
+// Single-reduction variant (f1): one pass, no grid-wide step (alpha, beta were set by the last
+// SpMV).  Per-thread partials in element order, CTA sums into upd_part (reduced by the SpMV's
+// last CTA together with u.w).
+__global__ void __launch_bounds__(kThreads) k_cg_update(double* __restrict__ x, double* __restrict__ r,
+                                                        double* __restrict__ u, double* __restrict__ p,
+                                                        double* __restrict__ sv, const double* __restrict__ w,
+                                                        const double* __restrict__ dinv, int64_t n, PcgState* st,
+                                                        double* __restrict__ upd_part) {
+  __shared__ double sh[32];
+  __shared__ double sh_sc[3];
+  if (threadIdx.x == 0) {
+    sh_sc[0] = ld_cg(&st->done_d);
+    sh_sc[1] = ld_cg(&st->alpha);
+    sh_sc[2] = ld_cg(&st->beta);
+  }
+  __syncthreads();
+  if (sh_sc[0] != 0.0) return;
+  const double alpha = sh_sc[1], beta = sh_sc[2];
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double g = 0.0, rr = 0.0;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+    double uv[kVec], wv[kVec], pv[kVec], sv_[kVec], xv[kVec], rv[kVec], dv[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      const bool ok = k < n;
+      uv[j] = ok ? u[k] : 0.0;
+      wv[j] = ok ? w[k] : 0.0;
+      pv[j] = ok ? p[k] : 0.0;
+      sv_[j] = ok ? sv[k] : 0.0;
+      xv[j] = ok ? x[k] : 0.0;
+      rv[j] = ok ? r[k] : 0.0;
+      dv[j] = ok ? dinv[k] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      if (k < n) {
+        const double pk = fma(beta, pv[j], uv[j]);
+        const double sk = fma(beta, sv_[j], wv[j]);
+        const double rk = fma(-alpha, sk, rv[j]);
+        const double zk = dv[j] * rk;
+        p[k] = pk;
+        sv[k] = sk;
+        x[k] = fma(alpha, pk, xv[j]);
+        r[k] = rk;
+        u[k] = zk;
+        g = fma(rk, zk, g);
+        rr = fma(rk, rk, rr);
+      }
+    }
+  }
+  const double tg = block_sum(g, sh), trr = block_sum(rr, sh);
+  if (threadIdx.x == 0) {
+    upd_part[blockIdx.x] = tg;
+    upd_part[gridDim.x + blockIdx.x] = trr;
   }
 }
 
@@ -1164,6 +1242,10 @@ __global__ void k_combine(PcgState* st, const double* __restrict__ all, int stag
     finish_beta(st, s[1], s[2]);
   }
   if (stage == 3) st->local[3] = s[3];
+  if (stage == 4) {  // single-reduction variant: (u.w, gamma', r.r) in one collective
+    if (ld_cg(&st->done_d) != 0.0) return;
+    finish_cg(st, s[0], s[1], s[2]);
+  }
 }
 
 }  // namespace
@@ -1316,6 +1398,14 @@ void launch_init(const double* f, const double* q, const double* dinv, double* r
 
 void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s) {
   k_resid<<<vec_grid(n), kThreads, 0, s>>>(f, q, n, st, part);
+  FS_LAUNCH_CHECK();
+}
+
+int cg_update_grid(int64_t n) { return vec_grid(n); }
+
+void launch_cg_update(double* x, double* r, double* u, double* p, double* sv, const double* w, const double* dinv,
+                      int64_t n, PcgState* st, double* upd_part, cudaStream_t s) {
+  k_cg_update<<<cg_update_grid(n), kThreads, 0, s>>>(x, r, u, p, sv, w, dinv, n, st, upd_part);
   FS_LAUNCH_CHECK();
 }
 

@@ -20,6 +20,14 @@ struct PcgState {
   int nranks;
   unsigned int ticket[4];
   unsigned int bar_count, bar_gen;  // grid barrier of the fused update/direction kernel
+  // single-reduction variant (Chronopoulos-Gear): rho = gamma = r.u,
+  // alpha_prev, the partial sums of gamma and r.r written by the update kernel (upd_n CTAs)
+  int variant;      // 0: standard recurrence, 1: single reduction per iteration
+  int cg_first;     // 1 until the SpMV after the initial residual has set the first alpha
+  double alpha_prev;
+  const double* upd_part;  // [2 * upd_n]: gamma partials, then r.r partials
+  int upd_n;
+  int pad_;
 };
 
 __device__ __forceinline__ void pcg_stop(PcgState* st, int status) {
@@ -67,6 +75,49 @@ __device__ __forceinline__ void finish_beta(PcgState* st, double rr, double rz) 
   }
 }
 
+// Single-reduction recurrence, once delta = u.w (w = K u) and the update kernel's sums
+// gamma' = r.u and r.r of the same iteration are known (one combined reduction per iteration):
+//   first call:  alpha = gamma / delta, beta = 0
+//   then:        iters += 1; stop tests on r.r; beta = gamma'/gamma,
+//                alpha = gamma' / (delta - beta gamma' / alpha_prev); gamma = gamma'
+// (mathematically the PCG recurrence of finish_alpha / finish_beta, with p = u + beta p and
+// s = K p carried as w + beta s).
+__device__ __forceinline__ void finish_cg(PcgState* st, double delta, double gamma_new, double rr) {
+  if (st->cg_first) {
+    st->cg_first = 0;
+    st->pq = delta;
+    if (!(delta > 0.0) || !isfinite(delta)) {
+      pcg_stop(st, FSFEM_ERR_BREAKDOWN);
+      return;
+    }
+    st->alpha = st->rho / delta;
+    st->beta = 0.0;
+    st->alpha_prev = st->alpha;
+    return;
+  }
+  st->iters += 1;
+  st->rr = rr;
+  if (!isfinite(rr) || !isfinite(gamma_new) || !isfinite(delta)) {
+    pcg_stop(st, FSFEM_ERR_BREAKDOWN);
+  } else if (sqrt(rr) <= st->tol * sqrt(st->ff)) {
+    pcg_stop(st, FSFEM_OK);
+  } else if (st->iters >= st->max_iter) {
+    pcg_stop(st, FSFEM_ERR_NOT_CONVERGED);
+  } else {
+    const double beta = gamma_new / st->rho;
+    const double den = delta - beta * gamma_new / st->alpha_prev;
+    st->pq = den;
+    if (!(den > 0.0) || !isfinite(den)) {
+      pcg_stop(st, FSFEM_ERR_BREAKDOWN);
+      return;
+    }
+    st->beta = beta;
+    st->alpha = gamma_new / den;
+    st->alpha_prev = st->alpha;
+    st->rho = gamma_new;
+  }
+}
+
 int pcg_grid();
 int spmv_kind(const Pattern& pat);  // 0 small, 1 gather, 2 dataflow (pcg.cu)
 // y (own rows) = K x_full; own_off = 3 * n_lo, the offset of the own rows in x_full (the dataflow
@@ -83,5 +134,10 @@ void launch_init(const double* f, const double* q, const double* dinv, double* r
                  double* part, cudaStream_t s);
 void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s);
 void launch_combine(PcgState* st, const double* all, int stage, cudaStream_t s);
+// Single-reduction variant: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s,
+// u = dinv r; per-CTA partials of r.u and r.r into upd_part (no grid-wide step).
+void launch_cg_update(double* x, double* r, double* u, double* p, double* sv, const double* w, const double* dinv,
+                      int64_t n, PcgState* st, double* upd_part, cudaStream_t s);
+int cg_update_grid(int64_t n);
 
 }  // namespace fsfem

@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
 # Every symbol include/fsfem.h declares (checked by tests/test_abi.py).
 METHOD_FS, METHOD_FEM_T4 = 0, 1
 
-EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method", "fsfem_set_reorder",
+EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
            "fsfem_surface_loads"]
@@ -72,6 +72,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_comm_init": (I, [P, P, I, I]),
         "fsfem_set_method": (I, [P, I]),
         "fsfem_set_reorder": (I, [P, I]),
+        "fsfem_set_pcg_variant": (I, [P, I]),
         "fsfem_nccl_get_unique_id": (I, [P]),
         "fsfem_build_faces": (I, [P, P, I64, P, I64, P, P]),
         "fsfem_get_faces": (I, [P, P, P, P]),
@@ -158,6 +159,11 @@ def fsfem_comm_init(ctx, unique_id: bytes | None, rank: int, nranks: int) -> Non
 
 def fsfem_set_method(ctx, method: int) -> None:
     _raise(ctx, load_library().fsfem_set_method(ctx, int(method)))
+
+
+def fsfem_set_pcg_variant(ctx, variant: int) -> None:
+    """0: standard PCG recurrence, 1: single reduction per iteration (Chronopoulos-Gear)."""
+    _raise(ctx, load_library().fsfem_set_pcg_variant(ctx, int(variant)))
 
 
 def fsfem_set_reorder(ctx, mode: int) -> None:
@@ -264,6 +270,9 @@ class FsFem:
 
     def set_reorder(self, mode: int):
         fsfem_set_reorder(self.ctx, mode)
+
+    def set_pcg_variant(self, variant: int):
+        fsfem_set_pcg_variant(self.ctx, variant)
 
     def set_method(self, method: int):
         fsfem_set_method(self.ctx, method)

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--pcg-iters", type=int, default=64)
     ap.add_argument("--reassemble", type=int, default=2)
     ap.add_argument("--reorder", type=int, default=0, help="0 auto, 1 always, 2 never")
+    ap.add_argument("--pcg-variant", type=int, default=0, help="0 standard, 1 single reduction")
     a = ap.parse_args()
     import torch
     from fsfem_inputs import config_mesh
@@ -26,6 +27,7 @@ def main():
     dev = torch.device("cuda", 0)
     g = FsFem(device=0, stream=torch.cuda.current_stream().cuda_stream)
     g.set_reorder(a.reorder)
+    g.set_pcg_variant(a.pcg_variant)
     xyz = torch.from_numpy(m.xyz).to(dev)
     tets = torch.from_numpy(m.tets).to(dev)
     dirichlet = torch.from_numpy(m.dirichlet).to(dev)

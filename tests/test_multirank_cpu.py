@@ -8,7 +8,9 @@ oracle solve:
   * partition: rank r owns nodes [r*ceil(N/G), min(N, (r+1)*ceil(N/G))) (include/fsfem.h);
   * BCs (MODIFY) applied on own rows with the global clamp mask (bc.cu);
   * per iteration: all_gather of equal padded p slices (ncclAllGather in gather_full), dot
-    partials all_gathered and summed in rank order (combine), the same recurrence as pcg.cuh.
+    partials all_gathered and summed in rank order (combine), the same recurrence as pcg.cuh;
+  * the single-reduction variant (fsfem_set_pcg_variant): one combined all_gather of
+    (u.w, r.u, r.r) per iteration (k_combine stage 4).
 The GPU side of the partition (halo blocks, transposed lists, per-rank CSR/SpMV/BC rows) is
 covered by tests/test_gpu_parity.py::test_row_partition_contexts.
 """
@@ -32,7 +34,7 @@ def _partition(nn, nranks, r):
     return lo, min(nn, lo + chunk), chunk
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, variant="standard"):
     import torch
     import torch.distributed as dist
     from oracle import Oracle
@@ -94,7 +96,34 @@ def _worker(rank, world, port, out_dir):
     rho, rr, ff = combine(r @ z, r @ r, f @ f)
     it = 0
     tol = 1e-10
-    while np.sqrt(rr) > tol * np.sqrt(ff) and it < 5000:
+    if variant == "single_reduction":
+        # Chronopoulos-Gear (pcg.cuh finish_cg, api.cu pcg_iteration_cg): ONE combined collective
+        # of (u.w, r.u, r.r) per iteration; u = D^-1 r gathered, w = K u on own rows
+        u = z
+        w = spmv(gather_full(u))
+        (delta,) = combine(u @ w)
+        gamma = rho
+        alpha = gamma / delta
+        beta = 0.0
+        alpha_prev = alpha
+        ps = np.zeros(nrow)
+        ss = np.zeros(nrow)
+        while True:
+            ps = u + beta * ps
+            ss = w + beta * ss
+            x += alpha * ps
+            r -= alpha * ss
+            u = dinv * r
+            w = spmv(gather_full(u))
+            delta, gamma_new, rr = combine(u @ w, r @ u, r @ r)
+            it += 1
+            if np.sqrt(rr) <= tol * np.sqrt(ff) or it >= 5000:
+                break
+            beta = gamma_new / gamma
+            alpha = gamma_new / (delta - beta * gamma_new / alpha_prev)
+            alpha_prev = alpha
+            gamma = gamma_new
+    while variant == "standard" and np.sqrt(rr) > tol * np.sqrt(ff) and it < 5000:
         q = spmv(gather_full(p))
         (pq,) = combine(p @ q)
         alpha = rho / pq
@@ -120,11 +149,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_partition_pcg_over_gloo(tmp_path, world):
+@pytest.mark.parametrize("world,variant", [(2, "standard"), (3, "standard"), (2, "single_reduction")])
+def test_row_partition_pcg_over_gloo(tmp_path, world, variant):
     import torch.multiprocessing as mp
     from oracle import Oracle
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), variant), nprocs=world, join=True)
     m = _mesh()
     o = Oracle(m.xyz, m.tets)
     o.build_faces()

@@ -127,13 +127,14 @@ fsfem_status fsfem_set_method(fsfem_ctx* ctx, int method);
  * fsfem_build_faces.  Errors: INVALID_ARG. */
 fsfem_status fsfem_set_reorder(fsfem_ctx* ctx, int mode);
 
-/* PCG recurrence (default FSFEM_PCG_STANDARD).  FSFEM_PCG_SINGLE_REDUCTION runs the
+/* PCG recurrence (default FSFEM_PCG_AUTO: single reduction with several ranks, standard on
+ * one GPU).  FSFEM_PCG_STANDARD is the recurrence of the oracle.  FSFEM_PCG_SINGLE_REDUCTION runs the
  * Chronopoulos-Gear form of the same Jacobi-PCG: s = K p is carried as a
  * vector, so each iteration has one SpMV (w = K u, u = D^-1 r) and ONE combined reduction of
  * (u.w, r.u, r.r) instead of two -- one collective per iteration on several GPUs.  Same
  * stopping test (||r|| <= rel_tol ||f||); rounding differs from the standard form, so iteration
  * counts may differ by a few percent.  Takes effect at the next pcg_solve.  Errors: INVALID_ARG. */
-enum { FSFEM_PCG_STANDARD = 0, FSFEM_PCG_SINGLE_REDUCTION = 1 };
+enum { FSFEM_PCG_STANDARD = 0, FSFEM_PCG_SINGLE_REDUCTION = 1, FSFEM_PCG_AUTO = 2 };
 fsfem_status fsfem_set_pcg_variant(fsfem_ctx* ctx, int variant);
 
 /* S1: extract the unique faces of the mesh.

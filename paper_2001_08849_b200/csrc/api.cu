@@ -139,7 +139,8 @@ struct fsfem_ctx {
   DevBuf<double> face_s, face_V, vals;  // assembly records (128 B per face / tet) and volumes
   // internal node order (reorder.cu): perm user -> internal, iperm internal -> user
   int reorder_mode = 0;  // 0 auto, 1 always, 2 never
-  int pcg_variant = 0;   // FSFEM_PCG_STANDARD / FSFEM_PCG_SINGLE_REDUCTION
+  int pcg_variant = FSFEM_PCG_AUTO;  // requested recurrence (fsfem_set_pcg_variant)
+  bool cg_active = false;            // recurrence of the current solve / captured graph
   DevBuf<double> cg_p, cg_s;  // single-reduction variant: direction p and s = K p (own rows)
   bool reordered = false;
   double mean_span = 0.0;
@@ -310,7 +311,7 @@ void pcg_iteration_cg(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
 }
 
 void pcg_iteration(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
-  if (c->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION) {
+  if (c->cg_active) {
     pcg_iteration_cg(c, e0, e1);
     return;
   }
@@ -445,8 +446,8 @@ fsfem_status fsfem_set_method(fsfem_ctx* c, int method) {
 
 fsfem_status fsfem_set_pcg_variant(fsfem_ctx* c, int variant) {
   return guarded(c, [&]() -> fsfem_status {
-    if (variant != FSFEM_PCG_STANDARD && variant != FSFEM_PCG_SINGLE_REDUCTION)
-      return fail(c, FSFEM_ERR_INVALID_ARG, "pcg variant must be 0 (standard) or 1 (single reduction)");
+    if (variant != FSFEM_PCG_STANDARD && variant != FSFEM_PCG_SINGLE_REDUCTION && variant != FSFEM_PCG_AUTO)
+      return fail(c, FSFEM_ERR_INVALID_ARG, "pcg variant must be 0 (standard), 1 (single reduction) or 2 (auto)");
     if (variant != c->pcg_variant) drop_graph(c);
     c->pcg_variant = variant;
     return FSFEM_OK;
@@ -719,7 +720,11 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     c->h_st->tol = rel_tol;
     c->h_st->max_iter = max_iter;
     c->h_st->nranks = c->nranks;
-    const bool cg1 = c->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION;
+    // auto: one collective per iteration on several GPUs, the standard recurrence on one
+    const bool cg1 = c->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION ||
+                     (c->pcg_variant == FSFEM_PCG_AUTO && c->nranks > 1);
+    if (cg1 != c->cg_active) drop_graph(c);
+    c->cg_active = cg1;
     c->h_st->variant = cg1 ? 1 : 0;
     c->h_st->cg_first = cg1 ? 1 : 0;
     c->h_st->upd_part = c->part.get() + 4 * pcg_grid();

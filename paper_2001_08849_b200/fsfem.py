@@ -162,7 +162,8 @@ def fsfem_set_method(ctx, method: int) -> None:
 
 
 def fsfem_set_pcg_variant(ctx, variant: int) -> None:
-    """0: standard PCG recurrence, 1: single reduction per iteration (Chronopoulos-Gear)."""
+    """0: standard PCG recurrence, 1: single reduction per iteration (Chronopoulos-Gear),
+    2: auto (default: single reduction with several ranks, standard on one GPU)."""
     _raise(ctx, load_library().fsfem_set_pcg_variant(ctx, int(variant)))
 
 

@@ -78,7 +78,7 @@ def test_variant_switch_and_errors(fs):
     m = config_mesh(1)
     g = fs()
     with pytest.raises(FsfemError) as e:
-        g.set_pcg_variant(2)
+        g.set_pcg_variant(3)
     assert e.value.status == "INVALID_ARG"
     g.build_faces(m.xyz, m.tets)
     g.assemble_csr(E, NU)
@@ -88,3 +88,6 @@ def test_variant_switch_and_errors(fs):
     g.set_pcg_variant(0)
     u0, r0 = g.pcg_solve()
     assert np.linalg.norm(u1 - u0) <= 1e-8 * np.linalg.norm(u0)
+    g.set_pcg_variant(2)  # auto: standard on one GPU
+    u2, r2 = g.pcg_solve()
+    assert np.array_equal(u2, u0) and r2["iterations"] == r0["iterations"]

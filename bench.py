@@ -221,6 +221,7 @@ def run_gpu(args):
         uid = [fsfem_nccl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         g.comm_init(uid[0], rank, world)
+        g.set_exchange(1 if args.exchange == "halo" else 0)
     dev = torch.device("cuda", local)
     xyz_d = torch.from_numpy(m.xyz).to(dev)
     tets_d = torch.from_numpy(m.tets).to(dev)
@@ -314,7 +315,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config), "n_nodes": m.n_nodes, "n_tets": m.n_tets,
-                       "n_faces": nf, "nnz": nnz, "parallelism": f"row-block x{world}" if world > 1 else "single GPU",
+                       "n_faces": nf, "nnz": nnz, "parallelism": f"row-block x{world} ({args.exchange})" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)"},
             "components": {"assembly_faces_per_s": nf / (t_num / 1e3), "assembly_ms": t_num,
                            "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,
@@ -344,6 +345,8 @@ def main():
     ap.add_argument("--impl", default="fsfem", choices=["fsfem", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
+                    help="multi-GPU exchange of the search direction (fsfem_set_exchange)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

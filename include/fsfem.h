@@ -110,6 +110,20 @@ fsfem_status fsfem_comm_init(fsfem_ctx* ctx, const void* nccl_unique_id, int ran
  * (resolved at run time).  Errors: INVALID_ARG (NULL), NCCL. */
 fsfem_status fsfem_nccl_get_unique_id(void* out);
 
+/* Exchange of the search direction between ranks before each SpMV.
+ * FSFEM_EXCHANGE_ALLGATHER (default): ncclAllGather of every rank's slice (8 * 3 N_n bytes).
+ * FSFEM_EXCHANGE_HALO: each rank receives only its halo -- the columns of its rows owned by other
+ * ranks (fsfem_get_halo) -- with ncclSend/ncclRecv, the sizes agreed once per mesh at the first
+ * assemble_csr; remote entries outside the halo are never read.  The final solution is still
+ * all-gathered.  Set before the first assemble_csr of a mesh.  Errors: INVALID_ARG, STATE,
+ * NCCL (send/recv unavailable). */
+enum { FSFEM_EXCHANGE_ALLGATHER = 0, FSFEM_EXCHANGE_HALO = 1 };
+fsfem_status fsfem_set_exchange(fsfem_ctx* ctx, int mode);
+/* The rank's halo after assemble_csr: *n = number of nodes (0 with one rank); nodes (host or
+ * device, may be NULL) receives their global ids, ascending (so grouped by owner rank).  Works
+ * on partition-only contexts.  Errors: STATE. */
+fsfem_status fsfem_get_halo(const fsfem_ctx* ctx, int32_t* nodes, int64_t* n);
+
 /* Discretisation of the stiffness (default FSFEM_METHOD_FS).  FSFEM_METHOD_FEM_T4 assembles the
  * conventional linear-tet stiffness K_e = V_e B^T c B over the tet node graph instead (the paper's
  * comparison column, PAPER.md:531 and Table 4 at 598-607); faces, BCs, SpMV

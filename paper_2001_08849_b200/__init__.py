@@ -26,6 +26,8 @@ from .fsfem import (  # noqa: F401
     fsfem_set_method,
     fsfem_set_reorder,
     fsfem_set_pcg_variant,
+    fsfem_set_exchange,
+    fsfem_get_halo,
     fsfem_spmv,
     fsfem_surface_loads,
     load_library,

@@ -30,6 +30,10 @@ void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr
                        cudaStream_t s);
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
                    const int32_t* face_opp, int64_t nf, double* face_s, double* face_V, cudaStream_t s);
+void build_halo_device(Pattern& pat, int64_t nn, int64_t chunk, int nranks, std::vector<int64_t>& need,
+                       DevBuf<unsigned char>& scratch, cudaStream_t s);
+void halo_pack_device(const double* full, const int32_t* nodes, int64_t n, double* buf, cudaStream_t s);
+void halo_unpack_device(const double* buf, const int32_t* nodes, int64_t n, double* full, cudaStream_t s);
 void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* rec_b, bool tet,
                             DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s);
 void assemble_rows_device(const Pattern& pat, const int32_t* face_nodes, const int32_t* face_opp,
@@ -85,7 +89,12 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   bool ok = false;
+  bool p2p = false;  // send/recv available (halo exchange)
 };
 static NcclApi& nccl() {
   static NcclApi api;
@@ -100,6 +109,11 @@ static NcclApi& nccl() {
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString;
+    api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.p2p = api.Send && api.Recv && api.GroupStart && api.GroupEnd;
   });
   return api;
 }
@@ -140,6 +154,11 @@ struct fsfem_ctx {
   // internal node order (reorder.cu): perm user -> internal, iperm internal -> user
   int reorder_mode = 0;  // 0 auto, 1 always, 2 never
   int pcg_variant = FSFEM_PCG_AUTO;  // requested recurrence (fsfem_set_pcg_variant)
+  int exchange = FSFEM_EXCHANGE_ALLGATHER;  // p exchange between ranks (fsfem_set_exchange)
+  bool halo_ready = false;                  // send lists agreed with the peers for this pattern
+  std::vector<int64_t> halo_need, halo_send;  // per peer: nodes received from / sent to it
+  DevBuf<int32_t> halo_send_nodes;          // global ids of own nodes sent, grouped by peer
+  DevBuf<double> halo_sbuf, halo_rbuf;      // packed values
   bool cg_active = false;            // recurrence of the current solve / captured graph
   DevBuf<double> cg_p, cg_s;  // single-reduction variant: direction p and s = K p (own rows)
   bool reordered = false;
@@ -288,9 +307,75 @@ void combine(fsfem_ctx* c, int stage) {
 }
 
 // p_full own slice -> everyone (in-place allgather, equal padded slices)
-void gather_full(fsfem_ctx* c, double* full) {
+void allgather_full(fsfem_ctx* c, double* full) {
   if (c->nranks == 1) return;
   FS_NCCL(nccl().AllGather(full + 3 * c->chunk * c->rank, full, 3 * c->chunk, ncclDouble, c->comm, c->stream));
+}
+
+// Halo mode: each rank receives only the entries of its halo (halo.cu) from their owners and
+// sends the entries its peers need; the other remote entries of `full` are left stale (the SpMV
+// never reads them).  Fixed send/recv sizes per peer, agreed once per pattern (setup_halo).
+void halo_exchange(fsfem_ctx* c, double* full) {
+  const int nr = c->nranks;
+  int64_t ns = 0;
+  for (int q = 0; q < nr; ++q) ns += c->halo_send[q];
+  halo_pack_device(full, c->halo_send_nodes.get(), ns, c->halo_sbuf.get(), c->stream);
+  FS_NCCL(nccl().GroupStart());
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < nr; ++q) {
+    if (c->halo_send[q] > 0)
+      FS_NCCL(nccl().Send(c->halo_sbuf.get() + 3 * so, 3 * c->halo_send[q], ncclDouble, q, c->comm, c->stream));
+    if (c->halo_need[q] > 0)
+      FS_NCCL(nccl().Recv(c->halo_rbuf.get() + 3 * ro, 3 * c->halo_need[q], ncclDouble, q, c->comm, c->stream));
+    so += c->halo_send[q];
+    ro += c->halo_need[q];
+  }
+  FS_NCCL(nccl().GroupEnd());
+  halo_unpack_device(c->halo_rbuf.get(), c->pat.halo.get(), c->pat.nhalo, full, c->stream);
+}
+
+// The search direction (p, or u in the single-reduction form) before an SpMV.
+void gather_full(fsfem_ctx* c, double* full) {
+  if (c->nranks == 1) return;
+  if (c->exchange == FSFEM_EXCHANGE_HALO && c->halo_ready) halo_exchange(c, full);
+  else allgather_full(c, full);
+}
+
+// Agree on the halo exchange with the peers (once per pattern): all-gather of the per-peer
+// counts, then every rank sends each owner the list of that owner's nodes it needs.
+void setup_halo(fsfem_ctx* c) {
+  const int nr = c->nranks, me = c->rank;
+  DevBuf<int64_t> cnt, all;
+  cnt.ensure(nr);
+  all.ensure(static_cast<size_t>(nr) * nr);
+  FS_CUDA(cudaMemcpyAsync(cnt.get(), c->halo_need.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice, c->stream));
+  FS_NCCL(nccl().AllGather(cnt.get(), all.get(), nr, ncclInt64, c->comm, c->stream));
+  std::vector<int64_t> h(static_cast<size_t>(nr) * nr);
+  FS_CUDA(cudaMemcpyAsync(h.data(), all.get(), sizeof(int64_t) * nr * nr, cudaMemcpyDeviceToHost, c->stream));
+  FS_CUDA(cudaStreamSynchronize(c->stream));
+  c->halo_send.assign(nr, 0);
+  int64_t ns = 0, nneed = 0;
+  for (int q = 0; q < nr; ++q) {
+    c->halo_send[q] = q == me ? 0 : h[static_cast<size_t>(q) * nr + me];  // what q needs from me
+    ns += c->halo_send[q];
+    nneed += c->halo_need[q];
+  }
+  c->halo_send_nodes.ensure(std::max<int64_t>(ns, 1));
+  c->halo_sbuf.ensure(3 * std::max<int64_t>(ns, 1));
+  c->halo_rbuf.ensure(3 * std::max<int64_t>(nneed, 1));
+  FS_NCCL(nccl().GroupStart());
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < nr; ++q) {
+    if (c->halo_need[q] > 0)
+      FS_NCCL(nccl().Send(c->pat.halo.get() + ro, c->halo_need[q], ncclInt32, q, c->comm, c->stream));
+    if (c->halo_send[q] > 0)
+      FS_NCCL(nccl().Recv(c->halo_send_nodes.get() + so, c->halo_send[q], ncclInt32, q, c->comm, c->stream));
+    so += c->halo_send[q];
+    ro += c->halo_need[q];
+  }
+  FS_NCCL(nccl().GroupEnd());
+  FS_CUDA(cudaStreamSynchronize(c->stream));
+  c->halo_ready = true;
 }
 
 // Single-reduction iteration (Chronopoulos-Gear): update (x, r, u = D^-1 r,
@@ -444,6 +529,29 @@ fsfem_status fsfem_set_method(fsfem_ctx* c, int method) {
   });
 }
 
+fsfem_status fsfem_set_exchange(fsfem_ctx* c, int mode) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (mode != FSFEM_EXCHANGE_ALLGATHER && mode != FSFEM_EXCHANGE_HALO)
+      return fail(c, FSFEM_ERR_INVALID_ARG, "exchange must be 0 (all-gather) or 1 (halo)");
+    if (c->stage >= kAssembled && mode != c->exchange)
+      return fail(c, FSFEM_ERR_STATE, "set the exchange before the first assemble_csr of a mesh");
+    c->exchange = mode;
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_get_halo(const fsfem_ctx* cc, int32_t* nodes, int64_t* n) {
+  fsfem_ctx* c = const_cast<fsfem_ctx*>(cc);
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
+    const int64_t nh = c->nranks > 1 ? c->pat.nhalo : 0;
+    if (n) *n = nh;
+    if (nodes && nh > 0) from_device(nodes, c->pat.halo.get(), sizeof(int32_t) * nh, c->stream);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    return FSFEM_OK;
+  });
+}
+
 fsfem_status fsfem_set_pcg_variant(fsfem_ctx* c, int variant) {
   return guarded(c, [&]() -> fsfem_status {
     if (variant != FSFEM_PCG_STANDARD && variant != FSFEM_PCG_SINGLE_REDUCTION && variant != FSFEM_PCG_AUTO)
@@ -577,6 +685,14 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       c->face_s.ensure(16 * std::max(c->nf, c->nt));
       c->face_V.ensure(std::max(c->nf, c->nt));
       c->have_pattern = true;
+      c->halo_ready = false;
+      if (c->nranks > 1) {
+        build_halo_device(c->pat, c->nn, c->chunk, c->nranks, c->halo_need, c->scratch, c->stream);
+        if (c->comm && c->exchange == FSFEM_EXCHANGE_HALO) {
+          if (!nccl().p2p) return fail(c, FSFEM_ERR_NCCL, "ncclSend/ncclRecv not available for the halo exchange");
+          setup_halo(c);
+        }
+      }
       drop_graph(c);
     }
     const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
@@ -800,7 +916,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     }
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     // true residual ||f - K x|| / ||f||
-    gather_full(c, c->x_full.get());
+    allgather_full(c, c->x_full.get());  // every rank returns the whole solution
     launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
     launch_resid(c->f.get(), c->q.get(), n, st, c->part.get(), c->stream);
     if (c->nranks > 1) combine(c, 3);

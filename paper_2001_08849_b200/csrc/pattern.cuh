@@ -8,6 +8,7 @@
 // entry (a, c) of stored block b is vals[9*b + 3*a + c].  Arrays the SpMV streams with bulk
 // copies (sptr, tptr, snbr, tlist, vals) carry >= 16 B of slack after their last element.
 #pragma once
+#include <vector>
 #include "common.cuh"
 
 namespace fsfem {
@@ -59,6 +60,9 @@ struct Pattern {
   DevBuf<int2> dep_list;     // [dep_ptr[nchunks]] (chunk d, need[d])
   DevBuf<uint32_t> cnt;      // [nchunks] arrival counters (mod need)
   DevBuf<double> dotc;       // [nchunks] per-chunk p.q partials
+  // halo of the rank (halo.cu, row partitions only): columns of the own rows outside the range
+  int64_t nhalo = 0;
+  DevBuf<int32_t> halo;      // [nhalo] global node ids, ascending (grouped by owner rank)
   DevBuf<int64_t> nf_ptr;    // [nloc+1]
   DevBuf<int32_t> nf_idx;    // [nfi] faces whose field holds node i, ascending
   // Assembly program (assemble.cu, built once per pattern): for the k-th face of F(i) the field

@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
 # Every symbol include/fsfem.h declares (checked by tests/test_abi.py).
 METHOD_FS, METHOD_FEM_T4 = 0, 1
 
-EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant",
+EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
            "fsfem_surface_loads"]
@@ -73,6 +73,8 @@ def load_library(path: str = LIB_PATH):
         "fsfem_set_method": (I, [P, I]),
         "fsfem_set_reorder": (I, [P, I]),
         "fsfem_set_pcg_variant": (I, [P, I]),
+        "fsfem_set_exchange": (I, [P, I]),
+        "fsfem_get_halo": (I, [P, P, P]),
         "fsfem_nccl_get_unique_id": (I, [P]),
         "fsfem_build_faces": (I, [P, P, I64, P, I64, P, P]),
         "fsfem_get_faces": (I, [P, P, P, P]),
@@ -165,6 +167,22 @@ def fsfem_set_pcg_variant(ctx, variant: int) -> None:
     """0: standard PCG recurrence, 1: single reduction per iteration (Chronopoulos-Gear),
     2: auto (default: single reduction with several ranks, standard on one GPU)."""
     _raise(ctx, load_library().fsfem_set_pcg_variant(ctx, int(variant)))
+
+
+def fsfem_set_exchange(ctx, mode: int) -> None:
+    """0: all-gather of the search direction (default), 1: halo-only send/recv."""
+    _raise(ctx, load_library().fsfem_set_exchange(ctx, int(mode)))
+
+
+def fsfem_get_halo(ctx) -> np.ndarray:
+    """The rank's halo node ids (ascending); empty with one rank."""
+    lib = load_library()
+    n = ctypes.c_int64(0)
+    _raise(ctx, lib.fsfem_get_halo(ctx, None, ctypes.byref(n)))
+    out = np.zeros(max(n.value, 0), np.int32)
+    if n.value > 0:
+        _raise(ctx, lib.fsfem_get_halo(ctx, out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(n)))
+    return out
 
 
 def fsfem_set_reorder(ctx, mode: int) -> None:
@@ -274,6 +292,12 @@ class FsFem:
 
     def set_pcg_variant(self, variant: int):
         fsfem_set_pcg_variant(self.ctx, variant)
+
+    def set_exchange(self, mode: int):
+        fsfem_set_exchange(self.ctx, mode)
+
+    def halo(self) -> np.ndarray:
+        return fsfem_get_halo(self.ctx)
 
     def set_method(self, method: int):
         fsfem_set_method(self.ctx, method)

@@ -10,7 +10,9 @@ oracle solve:
   * per iteration: all_gather of equal padded p slices (ncclAllGather in gather_full), dot
     partials all_gathered and summed in rank order (combine), the same recurrence as pcg.cuh;
   * the single-reduction variant (fsfem_set_pcg_variant): one combined all_gather of
-    (u.w, r.u, r.r) per iteration (k_combine stage 4).
+    (u.w, r.u, r.r) per iteration (k_combine stage 4);
+  * the halo exchange (fsfem_set_exchange): only the halo entries of p are sent / received
+    (remote entries outside the halo are NaN and must never be read).
 The GPU side of the partition (halo blocks, transposed lists, per-rank CSR/SpMV/BC rows) is
 covered by tests/test_gpu_parity.py::test_row_partition_contexts.
 """
@@ -34,7 +36,7 @@ def _partition(nn, nranks, r):
     return lo, min(nn, lo + chunk), chunk
 
 
-def _worker(rank, world, port, out_dir, variant="standard"):
+def _worker(rank, world, port, out_dir, variant="standard", exchange="allgather"):
     import torch
     import torch.distributed as dist
     from oracle import Oracle
@@ -73,12 +75,67 @@ def _worker(rank, world, port, out_dir, variant="standard"):
             q[k] = s
         return q
 
-    def gather_full(v_own):
+    def allgather_full(v_own):
         buf = torch.zeros(3 * chunk, dtype=torch.float64)
         buf[:nrow] = torch.from_numpy(v_own)
         parts = [torch.zeros(3 * chunk, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, buf)
         return torch.cat(parts).numpy()[:3 * nn]
+
+    # halo exchange (api.cu setup_halo / halo_exchange): the halo = columns of the own rows
+    # outside the range, ascending; counts all-gathered, then each rank sends every owner the
+    # list of that owner's nodes it needs; per exchange: send the needed entries, receive the halo
+    cols = np.unique(ci // 3)
+    halo = cols[(cols < lo) | (cols >= hi)]
+    owner = np.minimum(halo // chunk, world - 1)
+    need = np.array([np.sum(owner == q) for q in range(world)], np.int64)
+    allneed = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allneed, torch.from_numpy(need))
+    send_cnt = [int(allneed[q][rank]) if q != rank else 0 for q in range(world)]
+    send_nodes = {}
+    for q in range(world):  # pairwise, in rank order on both sides (no deadlock with gloo)
+        if q == rank:
+            continue
+        lst = torch.from_numpy(halo[owner == q].astype(np.int64))
+        got = torch.zeros(send_cnt[q], dtype=torch.int64)
+        if rank < q:
+            if lst.numel():
+                dist.send(lst, q)
+            if got.numel():
+                dist.recv(got, q)
+        else:
+            if got.numel():
+                dist.recv(got, q)
+            if lst.numel():
+                dist.send(lst, q)
+        send_nodes[q] = got.numpy()
+    full_p = np.full(3 * nn, np.nan)  # remote entries outside the halo stay NaN: never read
+
+    def halo_full(v_own):
+        full_p[3 * lo:3 * hi] = v_own
+        for q in range(world):
+            if q == rank:
+                continue
+            sbuf = torch.from_numpy(np.stack([full_p[3 * send_nodes[q] + a] for a in range(3)], 1).reshape(-1).copy())
+            rn = halo[owner == q]
+            rbuf = torch.zeros(3 * rn.size, dtype=torch.float64)
+            if rank < q:
+                if sbuf.numel():
+                    dist.send(sbuf, q)
+                if rbuf.numel():
+                    dist.recv(rbuf, q)
+            else:
+                if rbuf.numel():
+                    dist.recv(rbuf, q)
+                if sbuf.numel():
+                    dist.send(sbuf, q)
+            rb = rbuf.numpy().reshape(-1, 3)
+            for a in range(3):
+                full_p[3 * rn + a] = rb[:, a]
+        return full_p.copy()
+
+    def gather_full(v_own):
+        return halo_full(v_own) if exchange == "halo" else allgather_full(v_own)
 
     def combine(*vals):
         mine = torch.tensor(vals, dtype=torch.float64)
@@ -137,7 +194,7 @@ def _worker(rank, world, port, out_dir, variant="standard"):
         beta = rz / rho
         rho = rz
         p = z + beta * p
-    u = gather_full(x)
+    u = allgather_full(x)
     np.save(os.path.join(out_dir, f"u{rank}.npy"), u)
     np.save(os.path.join(out_dir, f"it{rank}.npy"), np.array([it]))
     dist.destroy_process_group()
@@ -149,11 +206,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,variant", [(2, "standard"), (3, "standard"), (2, "single_reduction")])
-def test_row_partition_pcg_over_gloo(tmp_path, world, variant):
+@pytest.mark.parametrize("world,variant,exchange", [(2, "standard", "allgather"), (3, "standard", "allgather"),
+                                                    (2, "single_reduction", "allgather"),
+                                                    (3, "single_reduction", "halo"), (3, "standard", "halo")])
+def test_row_partition_pcg_over_gloo(tmp_path, world, variant, exchange):
     import torch.multiprocessing as mp
     from oracle import Oracle
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), variant), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), variant, exchange), nprocs=world, join=True)
     m = _mesh()
     o = Oracle(m.xyz, m.tets)
     o.build_faces()

@@ -316,6 +316,7 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config), "n_nodes": m.n_nodes, "n_tets": m.n_tets,
                        "n_faces": nf, "nnz": nnz, "parallelism": f"row-block x{world} ({args.exchange})" if world > 1 else "single GPU",
+                       "pcg": "single-reduction Jacobi-PCG" if world > 1 else "Jacobi-PCG",
                        "l2": "inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)"},
             "components": {"assembly_faces_per_s": nf / (t_num / 1e3), "assembly_ms": t_num,
                            "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,

@@ -15,3 +15,4 @@ from .kuhn_beam import (  # noqa: F401
     splitmix64_stream,
     uniform01,
 )
+from .delaunay import delaunay_beam  # noqa: F401,E402

@@ -84,6 +84,11 @@ typedef struct {
   int64_t spmv_kernel;       /* SpMV kernel of this pattern: 0 warp per node (small meshes),
                                 1 gather (transposed blocks read from their rows), 2 dataflow push
                                                                                    */
+  double residual_floor;     /* rounding floor of the true residual at exit:
+                                2^-52 * ||K||_F * ||u||_2 / ||f||_2 (||K||_F bounded from above)   */
+  int64_t restarts;          /* residual-replacement restarts of the last pcg_solve              */
+  int64_t assembly_aux_bytes; /* bytes of the precomputed assembly tiles read per numeric assembly
+                                 (domain lists, field positions, block programs)   */
 } fsfem_report;
 
 /* Human-readable name of a status code (static string). */
@@ -101,11 +106,33 @@ const char* fsfem_last_error(const fsfem_ctx* ctx);
 /* Multi-GPU: join an NCCL communicator of `nranks` processes, one GPU each.
  * `nccl_unique_id` is the 128-byte ncclUniqueId (host memory) created by rank 0 and
  * broadcast by the caller.  Rank r then owns the contiguous node range
- * [r*ceil(N_n/nranks), min(N_n, (r+1)*ceil(N_n/nranks))) and builds only those rows.
+ * [ranges[r], ranges[r+1]) (fsfem_get_partition) and builds only those rows.  The ranges are
+ * computed at build_faces, identically on every rank, so that the node-face incidences (the
+ * rows' share of assembly work and nnz) are balanced; they are aligned to 32 nodes (to 256 nodes
+ * with fsfem_set_deterministic).
  * nccl_unique_id == NULL with nranks > 1 gives a partition-only context: faces, assembly, BCs,
- * get_csr and spmv of rank r's rows work without any communicator (one GPU can hold every
- * rank's context, which is how the row partition is tested); pcg_solve returns STATE. */
+ * get_csr and spmv of rank r's rows work without any communicator; pcg_solve returns STATE.
+ * Call before build_faces.  Errors: INVALID_ARG, STATE, NCCL. */
 fsfem_status fsfem_comm_init(fsfem_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
+/* Loopback group (SURVEY.md §4 "simulated partition"): ctxs[0..nranks) become ranks 0..nranks-1 of
+ * ONE process, on one device and one stream (all created with the same cuda_device and
+ * cuda_stream).  Each rank's faces, assembly and BCs are called on its own context as with NCCL;
+ * fsfem_pcg_solve on any context of the group then runs the solve of every rank, with each
+ * collective of the NCCL path (all-gather of partials, all-gather(v) or halo exchange of the
+ * search direction, deterministic chunk partials) replaced by device-to-device copies on that
+ * stream -- the multi-rank code path on one GPU.  The contexts stay owned by the caller (destroy
+ * every one).  Call before build_faces.  Errors: INVALID_ARG (NULL, duplicates, different
+ * device/stream), STATE. */
+fsfem_status fsfem_comm_init_loopback(fsfem_ctx** ctxs, int nranks);
+/* Node ranges of the ranks after build_faces: ranges [host, nranks + 1].  Errors: STATE. */
+fsfem_status fsfem_get_partition(const fsfem_ctx* ctx, int64_t* ranges);
+/* Deterministic dots (SURVEY.md 8(e) "Deterministic option"): every dot product of the solve is
+ * a sum of per-chunk partials over fixed global chunks of 256 nodes, exchanged and summed in
+ * chunk order; the SpMV runs in a canonical (partition-independent) order.  The displacements
+ * are then bit-identical for any number of ranks (at some cost in speed).  Uses the standard
+ * recurrence.  Set before build_faces (the ranges are aligned to the chunks); every rank must
+ * agree.  Errors: STATE. */
+fsfem_status fsfem_set_deterministic(fsfem_ctx* ctx, int on);
 /* Rank 0 helper: write a fresh 128-byte ncclUniqueId to out [host].  Needs libnccl.so.2
  * (resolved at run time).  Errors: INVALID_ARG (NULL), NCCL. */
 fsfem_status fsfem_nccl_get_unique_id(void* out);
@@ -141,8 +168,9 @@ fsfem_status fsfem_set_method(fsfem_ctx* ctx, int method);
  * fsfem_build_faces.  Errors: INVALID_ARG. */
 fsfem_status fsfem_set_reorder(fsfem_ctx* ctx, int mode);
 
-/* PCG recurrence (default FSFEM_PCG_AUTO: single reduction with several ranks, standard on
- * one GPU).  FSFEM_PCG_STANDARD is the recurrence of the oracle.  FSFEM_PCG_SINGLE_REDUCTION runs the
+/* PCG recurrence (default FSFEM_PCG_AUTO = the standard recurrence; the single-reduction form is
+ * opt-in until the multi-GPU variants are measured).  FSFEM_PCG_STANDARD is the recurrence of the
+ * oracle.  FSFEM_PCG_SINGLE_REDUCTION runs the
  * Chronopoulos-Gear form of the same Jacobi-PCG: s = K p is carried as a
  * vector, so each iteration has one SpMV (w = K u, u = D^-1 r) and ONE combined reduction of
  * (u.w, r.u, r.r) instead of two -- one collective per iteration on several GPUs.  Same
@@ -189,6 +217,12 @@ fsfem_status fsfem_apply_bc(fsfem_ctx* ctx, const int32_t* dirichlet_nodes, int6
 
 /* S8-S9: solve K u = f by Jacobi-PCG, stopping when ||r||_2 <= rel_tol * ||f||_2 on the
  * recurrence residual (rel_tol <= 0 means 1e-10; max_iter <= 0 means max(1000, 20*sqrt(n))).
+ * At exit the true residual t = ||f - K u|| / ||f|| is recomputed; success (FSFEM_OK,
+ * rep.converged = 1) requires t <= max(rel_tol, floor), floor = rep.residual_floor = the
+ * fp64 rounding floor 2^-52 ||K||_F ||u|| / ||f|| (two PCGs stopped at 1e-10
+ * cannot be asked for a true residual below the rounding of K u).  If the recurrence converged but
+ * t misses, the solve restarts from u with r = f - K u (residual replacement, at most 2 restarts,
+ * within max_iter) and returns NOT_CONVERGED if t still misses.
  *   u [3*n_nodes]: in = initial guess unless u0_is_zero, out = solution (full vector on every
  *   rank).  rep [host] may be NULL.  NOT_CONVERGED still writes u and rep. */
 fsfem_status fsfem_pcg_solve(fsfem_ctx* ctx, double* u, int u0_is_zero, double rel_tol,

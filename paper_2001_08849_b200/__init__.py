@@ -15,6 +15,9 @@ from .fsfem import (  # noqa: F401
     fsfem_assemble_csr,
     fsfem_build_faces,
     fsfem_comm_init,
+    fsfem_comm_init_loopback,
+    fsfem_get_partition,
+    fsfem_set_deterministic,
     fsfem_create,
     fsfem_destroy,
     fsfem_get_csr,

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -30,14 +31,14 @@ void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr
                        cudaStream_t s);
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
                    const int32_t* face_opp, int64_t nf, double* face_s, double* face_V, cudaStream_t s);
-void build_halo_device(Pattern& pat, int64_t nn, int64_t chunk, int nranks, std::vector<int64_t>& need,
+void build_halo_device(Pattern& pat, int64_t nn, const std::vector<int64_t>& ranges, std::vector<int64_t>& need,
                        DevBuf<unsigned char>& scratch, cudaStream_t s);
 void halo_pack_device(const double* full, const int32_t* nodes, int64_t n, double* buf, cudaStream_t s);
 void halo_unpack_device(const double* buf, const int32_t* nodes, int64_t n, double* full, cudaStream_t s);
-void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* rec_b, bool tet,
-                            DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s);
-void assemble_rows_device(const Pattern& pat, const int32_t* face_nodes, const int32_t* face_opp,
-                          const double* face_s, double lam, double mu, double* vals, bool tet, cudaStream_t s);
+void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a, const int32_t* rec_b, bool tet,
+                          DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s);
+void assemble_tiles_device(const Pattern& pat, const double* xyz, double lam, double mu, double* vals, bool tet,
+                           cudaStream_t s);
 void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s);
 void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, const double* rec_V,
                     int64_t nrec,
@@ -65,11 +66,17 @@ void apply_bc_device(const int64_t* node_ptr, const int32_t* nbr, const int32_t*
 
 static std::atomic<long long> g_launches{0};
 static thread_local bool g_capturing = false;
+static thread_local long long g_captured = 0;  // kernels recorded into the graph being captured
 void count_launch(long long n) {
   if (!g_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
+  else g_captured += n;
 }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
-void set_capturing(bool on) { g_capturing = on; }
+void set_capturing(bool on) {
+  if (on) g_captured = 0;
+  g_capturing = on;
+}
+long long captured_launches() { return g_captured; }
 
 static int g_sms = 0;
 int num_sms() {
@@ -88,6 +95,7 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -108,12 +116,14 @@ static NcclApi& nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString;
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(dlsym(h, "ncclBroadcast"));
     api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     api.p2p = api.Send && api.Recv && api.GroupStart && api.GroupEnd;
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GetErrorString &&
+             api.Broadcast && api.GroupStart && api.GroupEnd;
   });
   return api;
 }
@@ -135,10 +145,16 @@ struct fsfem_ctx {
   bool own_stream = false;
   std::string err;
   int stage = kCreated;
-  // partition
+  // partition: rank r owns nodes [ranges[r], ranges[r + 1]) (det.cu: balanced node-face incidences)
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
-  int64_t n_lo = 0, nloc = 0, chunk = 0;
+  int64_t n_lo = 0, nloc = 0;
+  std::vector<int64_t> ranges{0, 0};
+  // loopback group (fsfem_comm_init_loopback): every rank's context in this process, rank order,
+  // one device and one stream; collectives become device copies (SURVEY.md §4 simulated partition)
+  std::shared_ptr<std::vector<fsfem_ctx*>> loop;
+  bool det = false;             // deterministic dots (fsfem_set_deterministic)
+  DevBuf<double> dpart;         // det: [3 * global chunks] chunk partials
   // mesh
   int64_t nn = 0, nt = 0, nf = 0, ni = 0;
   DevBuf<double> xyz;
@@ -183,10 +199,11 @@ struct fsfem_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> spmv_ev;
   fsfem_report rep{};
-  // graph cache
+  // graph cache: every pointer and size the captured iterations bake in (graph_key_of)
   cudaGraphExec_t graph = nullptr;
-  int graph_batch = 0;
-  const void* graph_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<uintptr_t> graph_key;
+  long long graph_launches = 0;  // kernels per replay of the graph (counted at capture)
+  int max_restarts = 2;  // residual-replacement restarts when the true residual misses (fsfem_pcg_solve)
 };
 
 namespace {
@@ -298,53 +315,166 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 void drop_graph(fsfem_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   c->graph = nullptr;
+  c->graph_key.clear();
 }
 
-// allgather of the 4 per-rank partials and the combine step (multi-rank only)
-void combine(fsfem_ctx* c, int stage) {
-  FS_NCCL(nccl().AllGather(c->st.get()->local, c->all.get(), 4, ncclDouble, c->comm, c->stream));
-  launch_combine(c->st.get(), c->all.get(), stage, c->stream);
+// ---- collectives over the ranks of one solve ---------------------------------------------------
+// `cs` holds the contexts this process drives: {c} with NCCL (one rank per process), or every
+// rank's context with the loopback group.  The per-rank kernels are the same in both cases;
+// only the data movement of a collective differs (NCCL calls vs device-to-device copies on the
+// shared stream), so the loopback group executes the multi-rank code path on one GPU.
+using Ranks = std::vector<fsfem_ctx*>;
+
+Ranks ranks_of(fsfem_ctx* c) { return c->loop ? *c->loop : Ranks{c}; }
+
+void d2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes) FS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
 }
 
-// p_full own slice -> everyone (in-place allgather, equal padded slices)
-void allgather_full(fsfem_ctx* c, double* full) {
-  if (c->nranks == 1) return;
-  FS_NCCL(nccl().AllGather(full + 3 * c->chunk * c->rank, full, 3 * c->chunk, ncclDouble, c->comm, c->stream));
+// Every rank's 4 partials (st->local) into every rank's `all` (rank order), then the combine step.
+void coll_partials(const Ranks& cs, int stage) {
+  fsfem_ctx* c0 = cs[0];
+  if (c0->nranks == 1) return;
+  if (c0->loop) {
+    for (fsfem_ctx* d : cs)
+      for (fsfem_ctx* q : cs) d2d(d->all.get() + 4 * q->rank, q->st.get()->local, 4 * sizeof(double), d->stream);
+  } else {
+    FS_NCCL(nccl().AllGather(c0->st.get()->local, c0->all.get(), 4, ncclDouble, c0->comm, c0->stream));
+  }
+  for (fsfem_ctx* c : cs) launch_combine(c->st.get(), c->all.get(), stage, c->nranks, c->stream);
+}
+
+// All-gather (v) of the own node-range slices of a full-length vector (3 doubles per node).
+void coll_allgatherv(const Ranks& cs, DevBuf<double> fsfem_ctx::*buf) {
+  fsfem_ctx* c0 = cs[0];
+  if (c0->nranks == 1) return;
+  const std::vector<int64_t>& R = c0->ranges;
+  if (c0->loop) {
+    for (fsfem_ctx* q : cs) {
+      const int64_t lo = R[q->rank], n = R[q->rank + 1] - lo;
+      for (fsfem_ctx* d : cs)
+        if (d != q) d2d((d->*buf).get() + 3 * lo, (q->*buf).get() + 3 * lo, sizeof(double) * 3 * n, d->stream);
+    }
+    return;
+  }
+  double* full = (c0->*buf).get();
+  FS_NCCL(nccl().GroupStart());
+  for (int q = 0; q < c0->nranks; ++q) {
+    const int64_t lo = R[q], n = R[q + 1] - lo;
+    if (n > 0) FS_NCCL(nccl().Broadcast(full + 3 * lo, full + 3 * lo, 3 * n, ncclDouble, q, c0->comm, c0->stream));
+  }
+  FS_NCCL(nccl().GroupEnd());
 }
 
 // Halo mode: each rank receives only the entries of its halo (halo.cu) from their owners and
-// sends the entries its peers need; the other remote entries of `full` are left stale (the SpMV
-// never reads them).  Fixed send/recv sizes per peer, agreed once per pattern (setup_halo).
-void halo_exchange(fsfem_ctx* c, double* full) {
-  const int nr = c->nranks;
-  int64_t ns = 0;
-  for (int q = 0; q < nr; ++q) ns += c->halo_send[q];
-  halo_pack_device(full, c->halo_send_nodes.get(), ns, c->halo_sbuf.get(), c->stream);
-  FS_NCCL(nccl().GroupStart());
-  int64_t so = 0, ro = 0;
-  for (int q = 0; q < nr; ++q) {
-    if (c->halo_send[q] > 0)
-      FS_NCCL(nccl().Send(c->halo_sbuf.get() + 3 * so, 3 * c->halo_send[q], ncclDouble, q, c->comm, c->stream));
-    if (c->halo_need[q] > 0)
-      FS_NCCL(nccl().Recv(c->halo_rbuf.get() + 3 * ro, 3 * c->halo_need[q], ncclDouble, q, c->comm, c->stream));
-    so += c->halo_send[q];
-    ro += c->halo_need[q];
+// sends the entries its peers need; the other remote entries of the vector are left stale (the
+// SpMV never reads them).  Fixed send/recv sizes per peer, agreed once per pattern (setup_halo).
+void coll_halo(const Ranks& cs, DevBuf<double> fsfem_ctx::*buf) {
+  for (fsfem_ctx* c : cs) {
+    int64_t ns = 0;
+    for (int q = 0; q < c->nranks; ++q) ns += c->halo_send[q];
+    halo_pack_device((c->*buf).get(), c->halo_send_nodes.get(), ns, c->halo_sbuf.get(), c->stream);
   }
-  FS_NCCL(nccl().GroupEnd());
-  halo_unpack_device(c->halo_rbuf.get(), c->pat.halo.get(), c->pat.nhalo, full, c->stream);
+  fsfem_ctx* c0 = cs[0];
+  const int nr = c0->nranks;
+  if (c0->loop) {
+    for (fsfem_ctx* q : cs) {  // sender q -> receiver d
+      int64_t so = 0;
+      for (fsfem_ctx* d : cs) {
+        const int64_t n = q->halo_send[d->rank];
+        int64_t ro = 0;
+        for (int k = 0; k < q->rank; ++k) ro += d->halo_need[k];
+        if (d != q) d2d(d->halo_rbuf.get() + 3 * ro, q->halo_sbuf.get() + 3 * so, sizeof(double) * 3 * n, d->stream);
+        so += n;
+      }
+    }
+  } else {
+    FS_NCCL(nccl().GroupStart());
+    int64_t so = 0, ro = 0;
+    for (int q = 0; q < nr; ++q) {
+      if (c0->halo_send[q] > 0)
+        FS_NCCL(nccl().Send(c0->halo_sbuf.get() + 3 * so, 3 * c0->halo_send[q], ncclDouble, q, c0->comm, c0->stream));
+      if (c0->halo_need[q] > 0)
+        FS_NCCL(nccl().Recv(c0->halo_rbuf.get() + 3 * ro, 3 * c0->halo_need[q], ncclDouble, q, c0->comm, c0->stream));
+      so += c0->halo_send[q];
+      ro += c0->halo_need[q];
+    }
+    FS_NCCL(nccl().GroupEnd());
+  }
+  for (fsfem_ctx* c : cs) halo_unpack_device(c->halo_rbuf.get(), c->pat.halo.get(), c->pat.nhalo, (c->*buf).get(), c->stream);
 }
 
 // The search direction (p, or u in the single-reduction form) before an SpMV.
-void gather_full(fsfem_ctx* c, double* full) {
-  if (c->nranks == 1) return;
-  if (c->exchange == FSFEM_EXCHANGE_HALO && c->halo_ready) halo_exchange(c, full);
-  else allgather_full(c, full);
+void coll_full(const Ranks& cs, DevBuf<double> fsfem_ctx::*buf) {
+  if (cs[0]->nranks == 1) return;
+  if (cs[0]->exchange == FSFEM_EXCHANGE_HALO) coll_halo(cs, buf);
+  else coll_allgatherv(cs, buf);
 }
 
-// Agree on the halo exchange with the peers (once per pattern): all-gather of the per-peer
-// counts, then every rank sends each owner the list of that owner's nodes it needs.
-void setup_halo(fsfem_ctx* c) {
-  const int nr = c->nranks, me = c->rank;
+// Deterministic mode: the chunk partials of every rank's chunk range to every rank.
+void coll_dpart(const Ranks& cs) {
+  fsfem_ctx* c0 = cs[0];
+  if (c0->nranks == 1) return;
+  const std::vector<int64_t>& R = c0->ranges;
+  auto crange = [&](int q, int64_t& a, int64_t& n) {
+    a = R[q] / kDetChunkNodes;
+    n = ceil_div(R[q + 1], kDetChunkNodes) - a;
+    if (R[q + 1] <= R[q]) n = 0;
+  };
+  if (c0->loop) {
+    for (fsfem_ctx* q : cs) {
+      int64_t a, n;
+      crange(q->rank, a, n);
+      for (fsfem_ctx* d : cs)
+        if (d != q) d2d(d->dpart.get() + 3 * a, q->dpart.get() + 3 * a, sizeof(double) * 3 * n, d->stream);
+    }
+    return;
+  }
+  FS_NCCL(nccl().GroupStart());
+  for (int q = 0; q < c0->nranks; ++q) {
+    int64_t a, n;
+    crange(q, a, n);
+    if (n > 0)
+      FS_NCCL(nccl().Broadcast(c0->dpart.get() + 3 * a, c0->dpart.get() + 3 * a, 3 * n, ncclDouble, q, c0->comm,
+                               c0->stream));
+  }
+  FS_NCCL(nccl().GroupEnd());
+}
+
+// Agree on the halo exchange (once per pattern): every rank learns from each owner how many of
+// the owner's nodes it needs and sends it the list (NCCL: all-gather of the counts, send/recv of
+// the lists; loopback: read directly from the peers' contexts).
+void setup_halo(const Ranks& cs) {
+  fsfem_ctx* c0 = cs[0];
+  const int nr = c0->nranks;
+  if (c0->loop) {
+    for (fsfem_ctx* q : cs) {  // q sends to d what d needs from q: a slice of d's halo (grouped by owner)
+      q->halo_send.assign(nr, 0);
+      int64_t ns = 0;
+      for (fsfem_ctx* d : cs) {
+        q->halo_send[d->rank] = d == q ? 0 : d->halo_need[q->rank];
+        ns += q->halo_send[d->rank];
+      }
+      q->halo_send_nodes.ensure(std::max<int64_t>(ns, 1));
+      q->halo_sbuf.ensure(3 * std::max<int64_t>(ns, 1));
+      int64_t so = 0;
+      for (fsfem_ctx* d : cs) {
+        int64_t off = 0;
+        for (int k = 0; k < q->rank; ++k) off += d->halo_need[k];
+        d2d(q->halo_send_nodes.get() + so, d->pat.halo.get() + off, sizeof(int32_t) * q->halo_send[d->rank], q->stream);
+        so += q->halo_send[d->rank];
+      }
+      int64_t nneed = 0;
+      for (int k = 0; k < nr; ++k) nneed += q->halo_need[k];
+      q->halo_rbuf.ensure(3 * std::max<int64_t>(nneed, 1));
+    }
+    FS_CUDA(cudaStreamSynchronize(c0->stream));
+    for (fsfem_ctx* q : cs) q->halo_ready = true;
+    return;
+  }
+  fsfem_ctx* c = c0;
+  const int me = c->rank;
+  if (!nccl().p2p) throw Error(FSFEM_ERR_NCCL, "ncclSend/ncclRecv not available for the halo exchange");
   DevBuf<int64_t> cnt, all;
   cnt.ensure(nr);
   all.ensure(static_cast<size_t>(nr) * nr);
@@ -378,44 +508,117 @@ void setup_halo(fsfem_ctx* c) {
   c->halo_ready = true;
 }
 
-// Single-reduction iteration (Chronopoulos-Gear, SURVEY.md 8(f) f1): update (x, r, u = D^-1 r,
-// p, s; partials of r.u and r.r), [all-gather of u], SpMV w = K u with u.w, and ONE combined
-// reduction (u.w, r.u, r.r) -> alpha, beta.  p_full holds u, q holds w.
-void pcg_iteration_cg(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
-  PcgState* st = c->st.get();
-  double* own_u = c->p_full.get() + 3 * c->n_lo;
-  double* own_x = c->x_full.get() + 3 * c->n_lo;
-  const int64_t n = 3 * c->nloc;
-  launch_cg_update(own_x, c->r.get(), own_u, c->cg_p.get(), c->cg_s.get(), c->q.get(), c->dinv.get(), n, st,
-                   c->part.get() + 4 * pcg_grid(), c->stream);
-  if (c->nranks > 1) gather_full(c, c->p_full.get());
-  if (e0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
-  launch_spmv(c->pat, c->vals.get(), c->p_full.get(), 3 * c->n_lo, c->q.get(), st, c->part.get(), true, c->stream);
-  if (e1) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
-  if (c->nranks > 1) combine(c, 4);
+// ---- one PCG iteration over the ranks ----------------------------------------------------------
+double* own_p(fsfem_ctx* c) { return c->p_full.get() + 3 * c->n_lo; }
+double* own_x(fsfem_ctx* c) { return c->x_full.get() + 3 * c->n_lo; }
+
+void spmv_of(fsfem_ctx* c, const double* x_full, double* y, bool pcg) {
+  if (c->det) launch_spmv_canon(c->pat, c->vals.get(), x_full, y, pcg ? c->st.get() : nullptr, c->stream);
+  else launch_spmv(c->pat, c->vals.get(), x_full, 3 * c->n_lo, y, pcg ? c->st.get() : nullptr, c->part.get(), pcg,
+                   c->stream);
 }
 
-void pcg_iteration(fsfem_ctx* c, cudaEvent_t e0, cudaEvent_t e1) {
-  if (c->cg_active) {
-    pcg_iteration_cg(c, e0, e1);
+// Single-reduction iteration (Chronopoulos-Gear, SURVEY.md 8(f) f1): update (x, r, u = D^-1 r,
+// p, s; partials of r.u and r.r), exchange of u, SpMV w = K u with u.w, and ONE combined
+// reduction (u.w, r.u, r.r) -> alpha, beta.  p_full holds u, q holds w.
+void iter_cg(const Ranks& cs, cudaEvent_t e0, cudaEvent_t e1) {
+  for (fsfem_ctx* c : cs)
+    launch_cg_update(own_x(c), c->r.get(), own_p(c), c->cg_p.get(), c->cg_s.get(), c->q.get(), c->dinv.get(),
+                     3 * c->nloc, c->st.get(), c->part.get() + 4 * pcg_grid(), c->stream);
+  coll_full(cs, &fsfem_ctx::p_full);
+  for (fsfem_ctx* c : cs) {
+    if (e0 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+    spmv_of(c, c->p_full.get(), c->q.get(), true);
+    if (e1 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  }
+  coll_partials(cs, 4);
+}
+
+// Deterministic dots (det.cu): SpMV in canonical order, chunk partials of p.q, exchange, sum in
+// chunk order -> alpha; update with chunk partials of r.r, r.z, exchange -> beta; direction.
+void iter_det(const Ranks& cs, cudaEvent_t e0, cudaEvent_t e1) {
+  for (fsfem_ctx* c : cs) {
+    if (e0 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+    spmv_of(c, c->p_full.get(), c->q.get(), true);
+    if (e1 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+    launch_det_dots(1, c->n_lo, c->nloc, nullptr, c->q.get(), nullptr, nullptr, own_p(c), nullptr, c->st.get(),
+                    c->dpart.get(), c->stream);
+  }
+  coll_dpart(cs);
+  for (fsfem_ctx* c : cs) {
+    launch_det_finish(c->st.get(), c->dpart.get(), det_nchunks(c->nn), 1, c->stream);
+    launch_det_dots(2, c->n_lo, c->nloc, nullptr, c->q.get(), c->dinv.get(), c->r.get(), own_p(c), own_x(c),
+                    c->st.get(), c->dpart.get(), c->stream);
+  }
+  coll_dpart(cs);
+  for (fsfem_ctx* c : cs) {
+    launch_det_finish(c->st.get(), c->dpart.get(), det_nchunks(c->nn), 2, c->stream);
+    launch_direction(own_p(c), c->r.get(), c->dinv.get(), 3 * c->nloc, c->st.get(), c->stream);
+  }
+  coll_full(cs, &fsfem_ctx::p_full);
+}
+
+void pcg_iteration(const Ranks& cs, cudaEvent_t e0, cudaEvent_t e1) {
+  fsfem_ctx* c0 = cs[0];
+  if (c0->det) return iter_det(cs, e0, e1);
+  if (c0->cg_active) return iter_cg(cs, e0, e1);
+  for (fsfem_ctx* c : cs) {
+    if (e0 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+    spmv_of(c, c->p_full.get(), c->q.get(), true);
+    if (e1 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  }
+  if (c0->nranks == 1) {
+    launch_update_direction(own_x(c0), c0->r.get(), own_p(c0), c0->q.get(), c0->dinv.get(), 3 * c0->nloc,
+                            c0->st.get(), c0->part.get(), c0->stream);
     return;
   }
-  PcgState* st = c->st.get();
-  double* own_p = c->p_full.get() + 3 * c->n_lo;
-  double* own_x = c->x_full.get() + 3 * c->n_lo;
-  const int64_t n = 3 * c->nloc;
-  if (e0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
-  launch_spmv(c->pat, c->vals.get(), c->p_full.get(), 3 * c->n_lo, c->q.get(), st, c->part.get(), true, c->stream);
-  if (e1) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
-  if (c->nranks > 1) combine(c, 1);
-  if (c->nranks == 1) {
-    launch_update_direction(own_x, c->r.get(), own_p, c->q.get(), c->dinv.get(), n, st, c->part.get(), c->stream);
-    return;
+  coll_partials(cs, 1);
+  for (fsfem_ctx* c : cs)
+    launch_update(own_x(c), c->r.get(), own_p(c), c->q.get(), c->dinv.get(), 3 * c->nloc, c->st.get(), c->part.get(),
+                  c->stream);
+  coll_partials(cs, 2);
+  for (fsfem_ctx* c : cs) launch_direction(own_p(c), c->r.get(), c->dinv.get(), 3 * c->nloc, c->st.get(), c->stream);
+  coll_full(cs, &fsfem_ctx::p_full);
+}
+
+// Everything a captured batch of iterations bakes in: buffer pointers of every rank, sizes,
+// halo counts, variant and mode.  A graph is replayed only while its key is unchanged.
+std::vector<uintptr_t> graph_key_of(const Ranks& cs) {
+  std::vector<uintptr_t> k;
+  auto P = [&](const void* p) { k.push_back(reinterpret_cast<uintptr_t>(p)); };
+  for (fsfem_ctx* c : cs) {
+    P(c);
+    P(c->stream);
+    P(c->vals.get());
+    P(c->x_full.get());
+    P(c->p_full.get());
+    P(c->r.get());
+    P(c->q.get());
+    P(c->f.get());
+    P(c->dinv.get());
+    P(c->part.get());
+    P(c->all.get());
+    P(c->st.get());
+    P(c->cg_p.get());
+    P(c->cg_s.get());
+    P(c->dpart.get());
+    P(c->halo_sbuf.get());
+    P(c->halo_rbuf.get());
+    P(c->halo_send_nodes.get());
+    P(c->pat.halo.get());
+    P(c->pat.sptr.get());
+    P(c->pat.tbuf.get());
+    k.push_back(static_cast<uintptr_t>(c->n_lo));
+    k.push_back(static_cast<uintptr_t>(c->nloc));
+    k.push_back(static_cast<uintptr_t>(c->nranks));
+    k.push_back(static_cast<uintptr_t>(c->exchange));
+    k.push_back(static_cast<uintptr_t>(c->cg_active));
+    k.push_back(static_cast<uintptr_t>(c->det));
+    for (int64_t v : c->halo_send) k.push_back(static_cast<uintptr_t>(v));
+    for (int64_t v : c->halo_need) k.push_back(static_cast<uintptr_t>(v));
+    for (int64_t v : c->ranges) k.push_back(static_cast<uintptr_t>(v));
   }
-  launch_update(own_x, c->r.get(), own_p, c->q.get(), c->dinv.get(), n, st, c->part.get(), c->stream);
-  combine(c, 2);
-  launch_direction(own_p, c->r.get(), c->dinv.get(), n, st, c->stream);
-  gather_full(c, c->p_full.get());
+  return k;
 }
 
 }  // namespace
@@ -511,6 +714,49 @@ fsfem_status fsfem_comm_init(fsfem_ctx* c, const void* uid, int rank, int nranks
     }
     c->rank = rank;
     c->nranks = nranks;
+    c->loop.reset();
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_comm_init_loopback(fsfem_ctx** ctxs, int nranks) {
+  if (!ctxs || nranks < 1) return FSFEM_ERR_INVALID_ARG;
+  for (int r = 0; r < nranks; ++r)
+    if (!ctxs[r]) return FSFEM_ERR_INVALID_ARG;
+  for (int r = 0; r < nranks; ++r)
+    for (int q = 0; q < r; ++q)
+      if (ctxs[q] == ctxs[r]) return fail(ctxs[0], FSFEM_ERR_INVALID_ARG, "the contexts of a loopback group must be distinct");
+  for (int r = 0; r < nranks; ++r) {
+    fsfem_ctx* c = ctxs[r];
+    if (c->stage != kCreated) return fail(ctxs[0], FSFEM_ERR_STATE, "comm_init_loopback must precede build_faces");
+    if (c->device != ctxs[0]->device || c->stream != ctxs[0]->stream)
+      return fail(ctxs[0], FSFEM_ERR_INVALID_ARG, "a loopback group shares one device and one stream");
+    if (c->comm) return fail(ctxs[0], FSFEM_ERR_STATE, "context already joined an NCCL communicator");
+  }
+  auto group = std::make_shared<std::vector<fsfem_ctx*>>(ctxs, ctxs + nranks);
+  for (int r = 0; r < nranks; ++r) {
+    ctxs[r]->rank = r;
+    ctxs[r]->nranks = nranks;
+    ctxs[r]->loop = group;
+  }
+  return FSFEM_OK;
+}
+
+fsfem_status fsfem_set_deterministic(fsfem_ctx* c, int on) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage != kCreated) return fail(c, FSFEM_ERR_STATE, "set_deterministic must precede build_faces");
+    c->det = on != 0;
+    drop_graph(c);
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_get_partition(const fsfem_ctx* cc, int64_t* ranges) {
+  fsfem_ctx* c = const_cast<fsfem_ctx*>(cc);
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kFaces) return fail(c, FSFEM_ERR_STATE, "build_faces first");
+    if (!ranges) return fail(c, FSFEM_ERR_INVALID_ARG, "null ranges");
+    for (int r = 0; r <= c->nranks; ++r) ranges[r] = c->ranges[r];
     return FSFEM_OK;
   });
 }
@@ -579,11 +825,9 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
     drop_graph(c);
     c->stage = kCreated;
     c->have_pattern = false;
+    c->halo_ready = false;
     c->nn = n_nodes;
     c->nt = n_tets;
-    c->chunk = ceil_div(n_nodes, c->nranks);
-    c->n_lo = std::min<int64_t>(n_nodes, c->chunk * c->rank);
-    c->nloc = std::min<int64_t>(n_nodes, c->n_lo + c->chunk) - c->n_lo;
     c->xyz.ensure(3 * n_nodes);
     c->tets.ensure(4 * n_tets);
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -595,6 +839,12 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
                        c->face_opp, c->tet_face, &nf, &ni, c->h_flags);
     fsfem_status s = decode_flags(c, c->h_flags[0], "build_faces");
     if (s != FSFEM_OK) return s;
+    // row partition: node ranges balanced by node-face incidences, aligned to
+    // the deterministic dot chunk when that mode is on (every rank computes the same ranges)
+    partition_ranges_device(c->face_nodes.get(), c->face_opp.get(), nf, n_nodes, c->nranks, c->det ? kDetChunkNodes : 32,
+                            c->scratch, c->stream, c->ranges);
+    c->n_lo = c->ranges[c->rank];
+    c->nloc = c->ranges[c->rank + 1] - c->n_lo;
     // Internal node order (reorder.cu): renumber in Morton order when the caller's numbering is
     // not banded (mean tet id span > 16 N^(2/3)), never with several ranks (the documented row
     // partition is in the caller's numbering).
@@ -673,40 +923,27 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       fsfem_status s = decode_flags(c, c->h_flags[0], "symbolic");
       if (s != FSFEM_OK) return s;
       const bool tet = c->method == FSFEM_METHOD_FEM_T4;
-      build_assembly_program(c->pat, tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet,
-                             c->scratch, c->h_flags, c->stream);
-      s = decode_flags(c, c->h_flags[0], "assembly program");
+      build_assembly_tiles(c->pat, c->xyz.get(), tet ? c->tets.get() : c->face_nodes.get(),
+                           tet ? nullptr : c->face_opp.get(), tet, c->scratch, c->h_flags, c->stream);
+      s = decode_flags(c, c->h_flags[0], "assembly tiles");
       if (s != FSFEM_OK) return s;
       if (9 * c->pat.nblk >= (1LL << 31)) return fail(c, FSFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
       FS_CUDA(cudaEventRecord(c->ev1, c->stream));
       FS_CUDA(cudaEventSynchronize(c->ev1));
       c->rep.t_symbolic_ms = elapsed(c->ev0, c->ev1);
       c->vals.ensure(9 * c->pat.nsb + 2);  // + slack for the SpMV bulk copies (pattern.cuh)
-      c->face_s.ensure(16 * std::max(c->nf, c->nt));
-      c->face_V.ensure(std::max(c->nf, c->nt));
       c->have_pattern = true;
       c->halo_ready = false;
       if (c->nranks > 1) {
-        build_halo_device(c->pat, c->nn, c->chunk, c->nranks, c->halo_need, c->scratch, c->stream);
-        if (c->comm && c->exchange == FSFEM_EXCHANGE_HALO) {
-          if (!nccl().p2p) return fail(c, FSFEM_ERR_NCCL, "ncclSend/ncclRecv not available for the halo exchange");
-          setup_halo(c);
-        }
+        // the exchange lists are agreed with the peers at the first pcg_solve (setup_halo)
+        build_halo_device(c->pat, c->nn, c->ranges, c->halo_need, c->scratch, c->stream);
       }
       drop_graph(c);
     }
     const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
     const double mu = E / (2.0 * (1.0 + nu));
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
-    if (c->method == FSFEM_METHOD_FEM_T4) {
-      tet_s_device(c->xyz.get(), c->tets.get(), c->nt, c->face_s.get(), c->face_V.get(), c->stream);
-      assemble_rows_device(c->pat, c->tets.get(), nullptr, c->face_s.get(), lam, mu, c->vals.get(), true, c->stream);
-    } else {
-      face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
-                    c->face_s.get(), c->face_V.get(), c->stream);
-      assemble_rows_device(c->pat, c->face_nodes.get(), c->face_opp.get(), c->face_s.get(), lam, mu, c->vals.get(),
-                           false, c->stream);
-    }
+    assemble_tiles_device(c->pat, c->xyz.get(), lam, mu, c->vals.get(), c->method == FSFEM_METHOD_FEM_T4, c->stream);
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
     FS_CUDA(cudaEventSynchronize(c->ev1));
     c->rep.t_numeric_ms = elapsed(c->ev0, c->ev1);
@@ -721,6 +958,11 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
                         (c->rep.spmv_kernel == 2 ? 4 * c->pat.nsb : 8 * c->pat.ntb) + 16 * (c->nloc + 1) +
                         24 * c->nn + 24 * c->nloc;
     c->rep.assembly_bytes = 24 * c->nn + 16 * c->nt + 72 * c->pat.nsb;
+    {
+      int64_t blob = 0;
+      FS_CUDA(cudaMemcpy(&blob, c->pat.tile_off.get() + c->pat.ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
+      c->rep.assembly_aux_bytes = blob;
+    }
     if (row_begin) *row_begin = 3 * c->n_lo;
     if (n_rows) *n_rows = 3 * c->nloc;
     if (nnz) *nnz = 9 * c->pat.nblk;
@@ -803,11 +1045,10 @@ fsfem_status fsfem_spmv(fsfem_ctx* c, const double* p, double* q) {
   return guarded(c, [&]() -> fsfem_status {
     if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first");
     if (!p || !q) return fail(c, FSFEM_ERR_INVALID_ARG, "null vector");
-    const int64_t nfull = 3 * c->chunk * c->nranks;
-    c->x_full.ensure(nfull);
+    c->x_full.ensure(3 * c->nn);
     c->q.ensure(std::max<int64_t>(3 * c->nloc, 1));
     node_in(c, p, 3, c->x_full.get());
-    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
+    spmv_of(c, c->x_full.get(), c->q.get(), false);
     node_out(c, q, c->q.get(), c->n_lo, c->nloc, 3);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
@@ -817,68 +1058,102 @@ fsfem_status fsfem_spmv(fsfem_ctx* c, const double* p, double* q) {
 fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel_tol, int64_t max_iter,
                              fsfem_report* rep) {
   return guarded(c, [&]() -> fsfem_status {
-    if (c->stage < kBc) return fail(c, FSFEM_ERR_STATE, "apply_bc first");
-    if (c->nranks > 1 && !c->comm) return fail(c, FSFEM_ERR_STATE, "partition-only context: no communicator");
+    const Ranks cs = ranks_of(c);
+    fsfem_ctx* c0 = cs[0];
+    for (fsfem_ctx* r : cs) {
+      if (r->stage < kBc) return fail(c, FSFEM_ERR_STATE, "apply_bc first (on every rank of the loopback group)");
+      if (r->det != c0->det || r->exchange != c0->exchange || r->pcg_variant != c0->pcg_variant || r->nn != c0->nn)
+        return fail(c, FSFEM_ERR_INVALID_ARG, "the ranks disagree on mode, exchange, variant or mesh");
+    }
+    if (c->nranks > 1 && !c->comm && !c->loop) return fail(c, FSFEM_ERR_STATE, "partition-only context: no communicator");
     if (!u) return fail(c, FSFEM_ERR_INVALID_ARG, "null u");
-    const int64_t n = 3 * c->nloc;
     const int64_t nglob = 3 * c->nn;
-    const int64_t nfull = 3 * c->chunk * c->nranks;
     if (rel_tol <= 0.0) rel_tol = 1e-10;
     if (max_iter <= 0) max_iter = std::max<int64_t>(1000, static_cast<int64_t>(20.0 * std::sqrt(double(nglob))));
-    c->x_full.ensure(nfull);
-    c->p_full.ensure(nfull);
-    c->r.ensure(std::max<int64_t>(n, 1));
-    c->q.ensure(std::max<int64_t>(n, 1));
-    c->part.ensure(8 * static_cast<size_t>(pcg_grid()));  // SpMV / dot partials; [4g, 6g): update partials
-    c->all.ensure(4 * static_cast<size_t>(c->nranks));
-    PcgState* st = c->st.get();
-    std::memset(c->h_st, 0, sizeof(PcgState));
-    c->h_st->tol = rel_tol;
-    c->h_st->max_iter = max_iter;
-    c->h_st->nranks = c->nranks;
-    // auto: one collective per iteration on several GPUs, the standard recurrence on one
-    const bool cg1 = c->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION ||
-                     (c->pcg_variant == FSFEM_PCG_AUTO && c->nranks > 1);
-    if (cg1 != c->cg_active) drop_graph(c);
-    c->cg_active = cg1;
-    c->h_st->variant = cg1 ? 1 : 0;
-    c->h_st->cg_first = cg1 ? 1 : 0;
-    c->h_st->upd_part = c->part.get() + 4 * pcg_grid();
-    c->h_st->upd_n = cg_update_grid(n);
-    if (cg1) {
-      c->cg_p.ensure(std::max<int64_t>(n, 1));
-      c->cg_s.ensure(std::max<int64_t>(n, 1));
+    // recurrence: the standard form unless the single-reduction form is asked for (AUTO keeps the
+    // standard one until the multi-GPU variants are measured); deterministic mode is standard
+    const bool cg1 = !c0->det && c0->pcg_variant == FSFEM_PCG_SINGLE_REDUCTION;
+    for (fsfem_ctx* r : cs) {
+      const int64_t n = 3 * r->nloc;
+      r->x_full.ensure(nglob);
+      r->p_full.ensure(nglob);
+      r->r.ensure(std::max<int64_t>(n, 1));
+      r->q.ensure(std::max<int64_t>(n, 1));
+      r->part.ensure(8 * static_cast<size_t>(pcg_grid()));  // SpMV / dot partials; [4g, 6g): update partials
+      r->all.ensure(4 * static_cast<size_t>(r->nranks));
+      if (r->det) r->dpart.ensure(3 * det_nchunks(r->nn));
+      if (cg1) {
+        r->cg_p.ensure(std::max<int64_t>(n, 1));
+        r->cg_s.ensure(std::max<int64_t>(n, 1));
+      }
+      r->cg_active = cg1;
     }
+    if (c0->nranks > 1 && c0->exchange == FSFEM_EXCHANGE_HALO && !c0->halo_ready) setup_halo(cs);
+    const bool det = c0->det;
+    const int64_t nchg = det ? det_nchunks(c0->nn) : 0;
+
+    auto set_state = [&](int64_t budget) {
+      for (fsfem_ctx* r : cs) {
+        std::memset(r->h_st, 0, sizeof(PcgState));
+        r->h_st->tol = rel_tol;
+        r->h_st->max_iter = budget;
+        r->h_st->nranks = det ? 1 : r->nranks;  // det: every rank sums all chunk partials itself
+        r->h_st->variant = cg1 ? 1 : 0;
+        r->h_st->cg_first = cg1 ? 1 : 0;
+        r->h_st->upd_part = r->part.get() + 4 * pcg_grid();
+        r->h_st->upd_n = cg_update_grid(3 * r->nloc);
+        FS_CUDA(cudaMemcpyAsync(r->st.get(), r->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, r->stream));
+      }
+    };
+    // (Re)start from x_full (x0 = 0 or the current iterate): r = f - K x, z = D^-1 r, p = z.
+    auto start = [&](bool x_is_zero) {
+      for (fsfem_ctx* r : cs) {
+        const double* q0 = nullptr;
+        if (!x_is_zero) {
+          spmv_of(r, r->x_full.get(), r->q.get(), false);
+          q0 = r->q.get();
+        }
+        if (det)
+          launch_det_dots(0, r->n_lo, r->nloc, r->f.get(), q0, r->dinv.get(), r->r.get(), own_p(r), nullptr,
+                          r->st.get(), r->dpart.get(), r->stream);
+        else
+          launch_init(r->f.get(), q0, r->dinv.get(), r->r.get(), own_p(r), 3 * r->nloc, r->st.get(), r->part.get(),
+                      r->stream);
+      }
+      if (det) {
+        coll_dpart(cs);
+        for (fsfem_ctx* r : cs) launch_det_finish(r->st.get(), r->dpart.get(), nchg, 0, r->stream);
+      } else {
+        coll_partials(cs, 0);
+      }
+      coll_full(cs, &fsfem_ctx::p_full);
+      if (cg1) {  // p = s = 0, then w = K u and the first alpha (u = D^-1 r is in p_full)
+        for (fsfem_ctx* r : cs) {
+          FS_CUDA(cudaMemsetAsync(r->cg_p.get(), 0, sizeof(double) * std::max<int64_t>(3 * r->nloc, 1), r->stream));
+          FS_CUDA(cudaMemsetAsync(r->cg_s.get(), 0, sizeof(double) * std::max<int64_t>(3 * r->nloc, 1), r->stream));
+          spmv_of(r, r->p_full.get(), r->q.get(), true);
+        }
+        coll_partials(cs, 4);
+      }
+    };
+    auto read_state = [&]() {
+      FS_CUDA(cudaMemcpyAsync(c0->h_st, c0->st.get(), sizeof(PcgState), cudaMemcpyDeviceToHost, c0->stream));
+      FS_CUDA(cudaStreamSynchronize(c0->stream));
+    };
 
     FS_CUDA(cudaEventRecord(c->ev0, c->stream));
-    FS_CUDA(cudaMemcpyAsync(st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
-    FS_CUDA(cudaMemsetAsync(c->x_full.get(), 0, sizeof(double) * nfull, c->stream));
-    FS_CUDA(cudaMemsetAsync(c->p_full.get(), 0, sizeof(double) * nfull, c->stream));
-    double* own_x = c->x_full.get() + 3 * c->n_lo;
-    double* own_p = c->p_full.get() + 3 * c->n_lo;
-    const double* q0 = nullptr;
-    if (!u0_is_zero) {
-      node_in(c, u, 3, c->x_full.get());
-      launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
-      q0 = c->q.get();
+    set_state(max_iter);
+    for (fsfem_ctx* r : cs) {
+      FS_CUDA(cudaMemsetAsync(r->x_full.get(), 0, sizeof(double) * nglob, r->stream));
+      FS_CUDA(cudaMemsetAsync(r->p_full.get(), 0, sizeof(double) * nglob, r->stream));
+      if (!u0_is_zero) node_in(r, u, 3, r->x_full.get());
     }
-    launch_init(c->f.get(), q0, c->dinv.get(), c->r.get(), own_p, n, st, c->part.get(), c->stream);
-    if (c->nranks > 1) {
-      combine(c, 0);
-      gather_full(c, c->p_full.get());
-    }
-    if (cg1) {  // p = s = 0, then w = K u and the first alpha (u = D^-1 r is in p_full)
-      FS_CUDA(cudaMemsetAsync(c->cg_p.get(), 0, sizeof(double) * std::max<int64_t>(n, 1), c->stream));
-      FS_CUDA(cudaMemsetAsync(c->cg_s.get(), 0, sizeof(double) * std::max<int64_t>(n, 1), c->stream));
-      launch_spmv(c->pat, c->vals.get(), c->p_full.get(), 3 * c->n_lo, c->q.get(), st, c->part.get(), true, c->stream);
-      if (c->nranks > 1) combine(c, 4);
-    }
-    FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
-    FS_CUDA(cudaStreamSynchronize(c->stream));
+    start(u0_is_zero != 0);
+    read_state();
 
-    // graph of kBatch iterations with event pairs around each SpMV
-    const void* key[4] = {c->vals.get(), c->x_full.get(), c->p_full.get(), c->r.get()};
-    if (!c->graph || std::memcmp(key, c->graph_key, sizeof(key)) != 0) {
+    // graph of kBatch iterations with event pairs around the first SpMV
+    const std::vector<uintptr_t> key = graph_key_of(cs);
+    if (!c->graph || key != c->graph_key) {
       drop_graph(c);
       cudaGraph_t g;
       FS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -887,7 +1162,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
         // One SpMV per batch is bracketed by events (a live per-launch sample for the roofline);
         // an event pair around every SpMV would cost ~14 us per iteration at cfg4.
         for (int it = 0; it < kBatch; ++it)
-          pcg_iteration(c, it == 0 ? c->spmv_ev[0] : nullptr, it == 0 ? c->spmv_ev[1] : nullptr);
+          pcg_iteration(cs, it == 0 ? c->spmv_ev[0] : nullptr, it == 0 ? c->spmv_ev[1] : nullptr);
       } catch (...) {
         set_capturing(false);
         cudaStreamEndCapture(c->stream, &g);
@@ -897,46 +1172,89 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       FS_CUDA(cudaStreamEndCapture(c->stream, &g));
       FS_CUDA(cudaGraphInstantiate(&c->graph, g, 0));
       cudaGraphDestroy(g);
-      std::memcpy(c->graph_key, key, sizeof(key));
+      c->graph_key = key;
+      c->graph_launches = captured_launches();
     }
+    const long long launches_per_batch = c->graph_launches;
     double spmv_ms = 0.0;
-    int64_t spmv_n = 0;
-    while (c->h_st->done_d == 0.0) {
-      const long long before = c->h_st->iters;
-      FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
-      count_launch((c->nranks > 1 ? (cg1 ? 3 : 5) : 2) * kBatch);
-      FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
-      FS_CUDA(cudaStreamSynchronize(c->stream));
-      const long long ran = std::min<long long>(kBatch, c->h_st->iters - before);
-      if (ran > 0) {  // the sampled SpMV ran (iteration 0 of the batch)
-        spmv_ms += elapsed(c->spmv_ev[0], c->spmv_ev[1]);
-        ++spmv_n;
+    int64_t spmv_n = 0, total_iters = 0;
+    int restarts = 0;
+    double true_rel = 0.0, floor_rel = 0.0;
+    for (;;) {
+      while (c0->h_st->done_d == 0.0) {
+        const long long before = c0->h_st->iters;
+        FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
+        count_launch(launches_per_batch);
+        read_state();
+        const long long ran = std::min<long long>(kBatch, c0->h_st->iters - before);
+        if (ran > 0) {  // the sampled SpMV ran (iteration 0 of the batch)
+          spmv_ms += elapsed(c->spmv_ev[0], c->spmv_ev[1]);
+          ++spmv_n;
+        }
+        if (c0->h_st->iters == before && c0->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg made no progress");
       }
-      if (c->h_st->iters == before && c->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg made no progress");
+      total_iters += c0->h_st->iters;
+      // true residual ||f - K x|| / ||f|| and its rounding floor eps ||K||_F ||x|| / ||f||
+      coll_allgatherv(cs, &fsfem_ctx::x_full);  // every rank holds the whole iterate
+      for (fsfem_ctx* r : cs) {
+        spmv_of(r, r->x_full.get(), r->q.get(), false);
+        launch_sumsq(r->vals.get(), 9 * r->pat.nsb, r->st.get(), r->part.get(), r->stream);
+      }
+      if (det) {
+        coll_partials(cs, 5);  // ||K||_F^2 bound: sum over ranks (no effect with one rank)
+        for (fsfem_ctx* r : cs)
+          launch_det_dots(3, r->n_lo, r->nloc, r->f.get(), r->q.get(), nullptr, nullptr, nullptr, own_x(r), r->st.get(),
+                          r->dpart.get(), r->stream);
+        coll_dpart(cs);
+        for (fsfem_ctx* r : cs) launch_det_finish(r->st.get(), r->dpart.get(), nchg, 3, r->stream);
+      } else {
+        for (fsfem_ctx* r : cs) launch_resid(r->f.get(), r->q.get(), own_x(r), 3 * r->nloc, r->st.get(), r->part.get(), r->stream);
+        coll_partials(cs, 3);
+      }
+      read_state();
+      const PcgState& h = *c0->h_st;
+      const double ff = h.ff;
+      true_rel = ff > 0 ? std::sqrt(h.local[3] / ff) : 0.0;
+      floor_rel = ff > 0 ? std::ldexp(1.0, -52) * std::sqrt(h.local[2]) * std::sqrt(h.local[1]) / std::sqrt(ff) : 0.0;
+      const bool miss = h.status == FSFEM_OK && true_rel > std::max(rel_tol, floor_rel);
+      if (!miss || restarts >= c->max_restarts || total_iters >= max_iter) {
+        if (miss) {  // the recurrence converged but the true residual did not follow
+          for (fsfem_ctx* r : cs) r->h_st->status = FSFEM_ERR_NOT_CONVERGED;
+        }
+        break;
+      }
+      // residual replacement: restart the recurrence from the current iterate
+      ++restarts;
+      set_state(max_iter - total_iters);
+      for (fsfem_ctx* r : cs) FS_CUDA(cudaMemsetAsync(r->p_full.get(), 0, sizeof(double) * nglob, r->stream));
+      start(false);
+      read_state();
     }
     FS_CUDA(cudaEventRecord(c->ev1, c->stream));
-    // true residual ||f - K x|| / ||f||
-    allgather_full(c, c->x_full.get());  // every rank returns the whole solution
-    launch_spmv(c->pat, c->vals.get(), c->x_full.get(), 3 * c->n_lo, c->q.get(), nullptr, nullptr, false, c->stream);
-    launch_resid(c->f.get(), c->q.get(), n, st, c->part.get(), c->stream);
-    if (c->nranks > 1) combine(c, 3);
-    node_out(c, u, c->x_full.get(), 0, c->nn, 3);
-    FS_CUDA(cudaMemcpyAsync(c->h_st, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    node_out(c0, u, c0->x_full.get(), 0, c->nn, 3);
     FS_CUDA(cudaStreamSynchronize(c->stream));
-    (void)own_x;
-    const PcgState& h = *c->h_st;
-    c->rep.iterations = h.iters;
-    c->rep.converged = (h.status == FSFEM_OK) ? 1 : 0;
-    c->rep.rel_residual = h.ff > 0 ? std::sqrt(h.rr / h.ff) : 0.0;
-    c->rep.true_rel_residual = h.ff > 0 ? std::sqrt(h.local[3] / h.ff) : 0.0;
-    c->rep.t_pcg_ms = elapsed(c->ev0, c->ev1);
-    c->rep.t_spmv_ms = spmv_ms;
-    c->rep.spmv_launches = spmv_n;
-    c->rep.kernel_launches = launch_count();
+    const PcgState& h = *c0->h_st;
+    const int status = h.status;
+    for (fsfem_ctx* r : cs) {
+      r->rep.iterations = total_iters;
+      r->rep.converged = (status == FSFEM_OK) ? 1 : 0;
+      r->rep.rel_residual = h.ff > 0 ? std::sqrt(h.rr / h.ff) : 0.0;
+      r->rep.true_rel_residual = true_rel;
+      r->rep.residual_floor = floor_rel;
+      r->rep.restarts = restarts;
+      r->rep.t_pcg_ms = elapsed(c->ev0, c->ev1);
+      r->rep.t_spmv_ms = spmv_ms;
+      r->rep.spmv_launches = spmv_n;
+      r->rep.kernel_launches = launch_count();
+    }
     if (rep) *rep = c->rep;
-    if (h.status == FSFEM_ERR_BREAKDOWN) return fail(c, FSFEM_ERR_BREAKDOWN, "pcg breakdown (p.q <= 0 or non-finite)");
-    if (h.status == FSFEM_ERR_NOT_CONVERGED)
-      return fail(c, FSFEM_ERR_NOT_CONVERGED, "pcg reached max_iter=" + std::to_string(max_iter));
+    if (status == FSFEM_ERR_BREAKDOWN) return fail(c, FSFEM_ERR_BREAKDOWN, "pcg breakdown (p.q <= 0 or non-finite)");
+    if (status == FSFEM_ERR_NOT_CONVERGED) {
+      if (total_iters >= max_iter) return fail(c, FSFEM_ERR_NOT_CONVERGED, "pcg reached max_iter=" + std::to_string(max_iter));
+      return fail(c, FSFEM_ERR_NOT_CONVERGED,
+                  "true residual " + std::to_string(true_rel) + " above max(tol, rounding floor " +
+                      std::to_string(floor_rel) + ") after " + std::to_string(restarts) + " restarts");
+    }
     return FSFEM_OK;
   });
 }
@@ -960,6 +1278,14 @@ fsfem_status fsfem_recover_stress(fsfem_ctx* c, const double* u, double* strain,
     if (node_stress) d_nodes = c->rec_nodes.ensure(std::max<int64_t>(6 * c->nloc, 1));
     double* d_vm = nullptr;
     if (node_vm) d_vm = c->rec_vm.ensure(std::max<int64_t>(c->nloc, 1));
+    // per-domain records s_K, V (the assembly keeps them on chip; recovery recomputes them)
+    c->face_s.ensure(16 * std::max(c->nf, c->nt));
+    c->face_V.ensure(std::max(c->nf, c->nt));
+    if (tet)
+      tet_s_device(c->xyz.get(), c->tets.get(), c->nt, c->face_s.get(), c->face_V.get(), c->stream);
+    else
+      face_s_device(c->xyz.get(), c->tets.get(), c->face_nodes.get(), c->face_tet.get(), c->face_opp.get(), c->nf,
+                    c->face_s.get(), c->face_V.get(), c->stream);
     recover_device(tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(), tet, c->face_s.get(),
                    c->face_V.get(), nd,
                    c->pat.nf_ptr.get(), c->pat.nf_idx.get(), c->nloc, c->rec_u.get(), lam, mu, d_strain, d_stress,

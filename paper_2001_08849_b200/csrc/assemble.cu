@@ -177,254 +177,570 @@ __global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, c
   }
 }
 
-// Generic path (rows with more than 32 stored blocks; none in the Kuhn beams): warp per own
-// node i; lane = stored block slot (j >= i, or halo j < n_lo; pattern.cuh), in chunks of 32.
-// For every face of F(i) in ascending order, lanes whose neighbour j is in the face's field add
-// s_i s_j^T.
+// =============================================================================================
+// Tile assembly (S2-S4 + S6 in one kernel; DESIGN.md §6 "assembly").
+//
+// The own nodes are ordered along a Morton curve of their coordinates and cut into tiles of
+// <= kTileRows rows.  The union U of the tile rows' domain lists F(i) (faces -- tets for FEM-T4 --
+// whose field holds a tile row) is the only geometry a tile needs: the kernel computes
+// s_K = (V b_K)/sqrt(V) of every domain of U ONCE into shared memory from the coordinates of the
+// tile's vertices (staged in shared memory too), then sums every stored block of the tile rows
+// from shared memory and writes the rows' values.  No per-domain record goes to HBM.
+//
+// Warp specialisation, one CTA per SM, two tile buffers: producer warps stage tile j+1 (blob,
+// vertex coordinates, s records) while consumer warps sum and write tile j.
+//
+// Summation order (reading Q26) -- a function of the block alone, not of the tile, the rank's
+// range or the row length, so results are bitwise reproducible AND partition-invariant:
+//   off-diagonal block (i, j): the domains of F(i) n F(j) in ascending id, in sequence;
+//   diagonal block (i, i): the domains of F(i) in ascending id split into kDiagSplit strided
+//     sub-lists (entries q, q + kDiagSplit, ...), each summed in sequence, then the sub-list sums
+//     added in q order.
+// Each block is then K_ij = lam M + mu M^T + mu tr(M) I (M-form, reading Q25).
+//
+// Per-tile blob (built once per pattern by k_tile_build, read once per assembly):
+//   TileHdr | rows [nrows] (P = first stored block of the row, il) | verts int32 [nverts] (tile
+//   rows first) | fv u8 [ndom][5] (local vertex of field position p, 255 = none) |
+//   tasks [ntask] (entry start, slot, count, row, sub-list) | ent u16 [nent] ((local domain << 5)
+//   | 5 pos_i + pos_j), the entries of every stored block (rows in tile order, slots in order).
+// Local domain order = ascending domain id.  Tasks are stored longest first (load balance; which
+// thread runs a task does not change its sum).
+// =============================================================================================
+constexpr int kTileRows = 16;
+constexpr int kMaxDom = 640;      // domains per tile (shared-memory s records: 120 B each)
+constexpr int kMaxVerts = 254;    // u8 local vertex ids, 255 = none
+constexpr int kDiagCap = 2048;    // sum over the tile rows of |F(i)|
+constexpr int kMaxBlk = 767;      // stored blocks of the tile rows
+constexpr int kMaxTask = 1024;
+constexpr int kDiagSplit = 4;     // strided sub-lists of a diagonal block
+constexpr int kBlobCap = 16384;   // bytes of one tile blob
+constexpr int kAsmWarps = 16;     // 8 producer + 8 consumer warps
+constexpr int kAsmThreads = 32 * kAsmWarps;
+constexpr int kGroup = kAsmThreads / 2;
+
+struct TileHdr {
+  int32_t nrows, nverts, ndom, ntask, nent, pad0, pad1, pad2;
+};
+struct TileRow {
+  int64_t P;  // first stored block of the row (index into vals / 9)
+  int32_t il;
+  int32_t sdiag;  // slot of the diagonal block, -1 for a row without blocks (a node in no tet)
+};
+struct TileTask {
+  uint16_t estart, slot;
+  uint8_t count, row, sub, pad;  // sub = 255: off-diagonal block (stride 1); else diagonal sub-list
+};
+__host__ __device__ __forceinline__ constexpr int al16(int x) { return (x + 15) & ~15; }
+struct TileLayout {
+  int o_rows, o_verts, o_fv, o_task, o_ent, bytes;
+  __host__ __device__ TileLayout(int nrows, int nverts, int ndom, int ntask, int nent) {
+    o_rows = 32;
+    o_verts = al16(o_rows + 16 * nrows);
+    o_fv = al16(o_verts + 4 * nverts);
+    o_task = al16(o_fv + 5 * ndom);
+    o_ent = al16(o_task + 8 * ntask);
+    bytes = al16(o_ent + 2 * nent);
+  }
+};
+
+// ---- builder (once per pattern) ---------------------------------------------------------------
+constexpr int kBldThreads = 256;
+constexpr int kSortCap = 4096;
+
+// In-place ascending bitonic sort of a[0..n2) (n2 a power of two), whole CTA.
+__device__ void cta_bitonic(int32_t* a, int n2) {
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t x = a[i], y = a[l];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// Keep the first of every run of equal values of the sorted a[0..n) (ignoring `skip`) -> out;
+// returns the count.  Deterministic (CTA scan of the keep flags).
+__device__ int cta_unique(const int32_t* a, int n, int32_t skip, int32_t* out, int* sh_tot) {
+  int base = 0;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool keep = i < n && a[i] != skip && (i == 0 || a[i - 1] != a[i]);
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ int wsum[32];
+    if (lane == 0) wsum[w] = __popc(ball);
+    __syncthreads();
+    int off = base;
+    for (int k = 0; k < w; ++k) off += wsum[k];
+    if (keep) out[off + __popc(ball & ((1u << lane) - 1u))] = a[i];
+    int tot = 0;
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) tot += wsum[k];
+    __syncthreads();
+    base += tot;
+  }
+  if (threadIdx.x == 0) *sh_tot = base;
+  __syncthreads();
+  return base;
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One CTA per tile.  kFill = false: blob size (or -1 = too big for the caps: split the tile,
+// -2 = a single row that cannot fit: UNSUPPORTED) into size[t]; kFill = true: the blob at off[t].
+template <bool kFill>
+__global__ void __launch_bounds__(kBldThreads) k_tile_build(
+    const int32_t* __restrict__ order, const int32_t* __restrict__ tstart, int64_t ntiles,
+    const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a,
+    const int32_t* __restrict__ rec_b, bool tet, const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr,
+    const int32_t* __restrict__ sdiag, int64_t n_lo, int64_t* __restrict__ size, const int64_t* __restrict__ off,
+    unsigned char* __restrict__ blob) {
+  extern __shared__ __align__(16) unsigned char bsm[];
+  int32_t* A = reinterpret_cast<int32_t*>(bsm);          // [kSortCap] sort buffer
+  int32_t* U = A + kSortCap;                              // [kMaxDom] domains (ascending)
+  int32_t* F5 = U + kMaxDom;                              // [kMaxDom * 5] field nodes
+  int32_t* others = F5 + 5 * kMaxDom;                     // [kSortCap] other vertices (sorted)
+  int32_t* bcnt = others + kSortCap;                      // [kMaxBlk + 1] entries per block
+  int32_t* cur = bcnt + kMaxBlk + 1;                      // [kMaxBlk + 1] entry offsets / cursors
+  int32_t* tkey = cur + kMaxBlk + 1;                      // [kMaxTask] task keys (count, index)
+  int32_t* tinfo = tkey + kMaxTask;                       // [kMaxTask] row << 24 | sub-list << 16 | slot
+  __shared__ int32_t rnode[kTileRows], ril[kTileRows], rds[kTileRows], rsd[kTileRows], rbb[kTileRows + 1];
+  __shared__ int64_t rP[kTileRows], rF[kTileRows + 1];
+  __shared__ int sh_n, sh_flag;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int nrows = tstart[t + 1] - tstart[t];
+    if (threadIdx.x == 0) {
+      int64_t fsum = 0;
+      int bb = 0;
+      for (int r = 0; r < nrows; ++r) {
+        const int32_t il = order[tstart[t] + r];
+        ril[r] = il;
+        rnode[r] = static_cast<int32_t>(n_lo + il);
+        rP[r] = sptr[il];
+        rds[r] = static_cast<int32_t>(sptr[il + 1] - sptr[il]);
+        rsd[r] = rds[r] > 0 ? sdiag[il] : -1;
+        rbb[r] = bb;
+        bb += rds[r];
+        rF[r] = fsum;
+        fsum += nf_ptr[il + 1] - nf_ptr[il];
+      }
+      rbb[nrows] = bb;
+      rF[nrows] = fsum;
+      sh_flag = (fsum > kDiagCap || bb > kMaxBlk) ? 1 : 0;
+    }
+    __syncthreads();
+    if (sh_flag) {
+      if (!kFill && threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
+      __syncthreads();
+      continue;
+    }
+    // U = sorted unique union of the rows' domain lists
+    const int nA = static_cast<int>(rF[nrows]);
+    int n2 = 32;
+    while (n2 < nA) n2 <<= 1;
+    for (int r = 0; r < nrows; ++r) {
+      const int64_t b = nf_ptr[ril[r]];
+      const int len = static_cast<int>(rF[r + 1] - rF[r]);
+      for (int k = threadIdx.x; k < len; k += blockDim.x) A[rF[r] + k] = nf_idx[b + k];
+    }
+    for (int k = nA + threadIdx.x; k < n2; k += blockDim.x) A[k] = 0x7fffffff;
+    __syncthreads();
+    cta_bitonic(A, n2);
+    const int ndom = cta_unique(A, nA, 0x7fffffff, U, &sh_n);
+    if (ndom > kMaxDom) {
+      if (!kFill && threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
+      __syncthreads();
+      continue;
+    }
+    for (int k = threadIdx.x; k < ndom; k += blockDim.x) {
+      int32_t fld[5];
+      field_of(rec_a, rec_b, tet, U[k], fld);
+#pragma unroll
+      for (int p = 0; p < 5; ++p) F5[5 * k + p] = fld[p];
+    }
+    __syncthreads();
+    // other vertices: field nodes that are not tile rows, sorted unique
+    const int nc = 5 * ndom;
+    int m2 = 32;
+    while (m2 < nc) m2 <<= 1;
+    for (int k = threadIdx.x; k < m2; k += blockDim.x) {
+      int32_t v = 0x7fffffff;
+      if (k < nc) {
+        v = F5[k];
+        for (int r = 0; r < nrows; ++r)
+          if (v == rnode[r]) v = 0x7fffffff;
+        if (v < 0) v = 0x7fffffff;
+      }
+      A[k] = v;
+    }
+    __syncthreads();
+    cta_bitonic(A, m2);
+    const int no = cta_unique(A, nc, 0x7fffffff, others, &sh_n);
+    const int nverts = nrows + no;
+    // entries per stored block: off-diagonal (i, J): one per domain of F(i) holding J (stored J);
+    // diagonal: one per domain of F(i).  Warp per row, lane per domain.
+    for (int b = threadIdx.x; b <= kMaxBlk; b += blockDim.x) bcnt[b] = 0;
+    __syncthreads();
+    for (int r = w; r < nrows; r += kBldThreads / 32) {
+      const int32_t i = rnode[r];
+      const int64_t fb = nf_ptr[ril[r]];
+      const int len = static_cast<int>(rF[r + 1] - rF[r]);
+      const int64_t P = rP[r];
+      const int ds = rds[r];
+      for (int k0 = 0; k0 < len; k0 += 32) {
+        const int k = k0 + lane;
+        if (k < len) {
+          const int kl = lower_bound_i32(U, ndom, nf_idx[fb + k]);
+          int pi = 0;
+#pragma unroll
+          for (int p = 0; p < 5; ++p) pi = F5[5 * kl + p] == i ? p : pi;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            const int32_t J = F5[5 * kl + q];
+            if (J < 0 || (J < i && J >= n_lo)) continue;
+            const int slot = q == pi ? rsd[r] : lower_bound_i32(snbr + P, ds, J);
+            atomicAdd(&bcnt[rbb[r] + slot], 1);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // entry offsets and the number of tasks
+      int run = 0, nt = 0;
+      bool ok = true;
+      for (int r = 0; r < nrows; ++r)
+        for (int sl = 0; sl < rds[r]; ++sl) {
+          const int b = rbb[r] + sl;
+          cur[b] = run;
+          run += bcnt[b];
+          if (sl == rsd[r]) {
+            nt += kDiagSplit;
+            ok = ok && bcnt[b] <= 255 * kDiagSplit;
+          } else {
+            nt += 1;
+            ok = ok && bcnt[b] <= 255;
+          }
+        }
+      sh_n = run;
+      sh_flag = (!ok || nt > kMaxTask || run >= 65536) ? 1 : 0;
+      cur[kMaxBlk] = nt;
+    }
+    __syncthreads();
+    const int nent = sh_n, ntask = cur[kMaxBlk];
+    const TileLayout L(nrows, nverts, ndom, ntask, nent);
+    const bool ok = !sh_flag && nverts <= kMaxVerts && L.bytes <= kBlobCap;
+    if (!kFill) {
+      if (threadIdx.x == 0) size[t] = ok ? L.bytes : -(nrows > 1 ? 1 : 2);
+      __syncthreads();
+      continue;
+    }
+    unsigned char* bl = blob + off[t];
+    if (threadIdx.x == 0) {
+      TileHdr h{nrows, nverts, ndom, ntask, nent, 0, 0, 0};
+      *reinterpret_cast<TileHdr*>(bl) = h;
+    }
+    for (int r = threadIdx.x; r < nrows; r += blockDim.x)
+      reinterpret_cast<TileRow*>(bl + L.o_rows)[r] = TileRow{rP[r], ril[r], rsd[r]};
+    for (int v = threadIdx.x; v < nverts; v += blockDim.x)
+      reinterpret_cast<int32_t*>(bl + L.o_verts)[v] = v < nrows ? rnode[v] : others[v - nrows];
+    for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+      const int32_t v = F5[k];
+      int lv = 255;
+      if (v >= 0) {
+        lv = -1;
+        for (int r = 0; r < nrows; ++r)
+          if (v == rnode[r]) lv = r;
+        if (lv < 0) lv = nrows + lower_bound_i32(others, no, v);
+      }
+      bl[L.o_fv + k] = static_cast<unsigned char>(lv);
+    }
+    // tasks, longest first (ties: block order): key = (255 * kDiagSplit - count) << 20 | index
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int r = 0; r < nrows; ++r)
+        for (int sl = 0; sl < rds[r]; ++sl) {
+          const int b = rbb[r] + sl;
+          if (sl == rsd[r]) {
+            for (int q = 0; q < kDiagSplit; ++q) {
+              const int c = (bcnt[b] - q + kDiagSplit - 1) / kDiagSplit;
+              tkey[k] = ((1023 - c) << 20) | k;
+              tinfo[k] = (r << 24) | (q << 16) | sl;
+              ++k;
+            }
+          } else {
+            tkey[k] = ((1023 - bcnt[b]) << 20) | k;
+            tinfo[k] = (r << 24) | (255 << 16) | sl;
+            ++k;
+          }
+        }
+    }
+    __syncthreads();
+    {
+      TileTask* tasks = reinterpret_cast<TileTask*>(bl + L.o_task);
+      for (int a = threadIdx.x; a < ntask; a += blockDim.x) {  // rank sort (keys are distinct)
+        const int32_t key = tkey[a];
+        int rank = 0;
+        for (int c = 0; c < ntask; ++c) rank += tkey[c] < key ? 1 : 0;
+        const int r = tinfo[a] >> 24, q = (tinfo[a] >> 16) & 255, sl = tinfo[a] & 0xffff;
+        const int b = rbb[r] + sl;
+        TileTask tk;
+        tk.slot = static_cast<uint16_t>(sl);
+        tk.row = static_cast<uint8_t>(r);
+        tk.sub = static_cast<uint8_t>(q);
+        tk.pad = 0;
+        if (q == 255) {
+          tk.estart = static_cast<uint16_t>(cur[b]);
+          tk.count = static_cast<uint8_t>(bcnt[b]);
+        } else {
+          tk.estart = static_cast<uint16_t>(cur[b] + q);
+          tk.count = static_cast<uint8_t>((bcnt[b] - q + kDiagSplit - 1) / kDiagSplit);
+        }
+        tasks[rank] = tk;
+      }
+    }
+    __syncthreads();
+    // entries: per row, rounds of 32 domains in ascending order; slot by slot, the lanes holding
+    // the slot write in lane (= ascending domain) order
+    uint16_t* ent = reinterpret_cast<uint16_t*>(bl + L.o_ent);
+    for (int r = w; r < nrows; r += kBldThreads / 32) {
+      const int32_t i = rnode[r];
+      const int64_t fb = nf_ptr[ril[r]];
+      const int len = static_cast<int>(rF[r + 1] - rF[r]);
+      const int64_t P = rP[r];
+      const int ds = rds[r];
+      for (int k0 = 0; k0 < len; k0 += 32) {
+        const int k = k0 + lane;
+        int tslot[5] = {-1, -1, -1, -1, -1}, tcode[5] = {0, 0, 0, 0, 0}, kl = 0;
+        if (k < len) {
+          kl = lower_bound_i32(U, ndom, nf_idx[fb + k]);
+          int pi = 0;
+#pragma unroll
+          for (int p = 0; p < 5; ++p) pi = F5[5 * kl + p] == i ? p : pi;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            const int32_t J = F5[5 * kl + q];
+            if (J < 0 || (J < i && J >= n_lo)) continue;
+            tslot[q] = q == pi ? rsd[r] : lower_bound_i32(snbr + P, ds, J);
+            tcode[q] = 5 * pi + q;
+          }
+        }
+        for (int sl = 0; sl < ds; ++sl) {
+          int code = -1;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) code = tslot[q] == sl ? tcode[q] : code;
+          const unsigned m = __ballot_sync(0xffffffffu, code >= 0);
+          if (m == 0u) continue;
+          const int b = rbb[r] + sl;
+          if (code >= 0) ent[cur[b] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>((kl << 5) | code);
+          __syncwarp();
+          if (lane == 0) cur[b] += __popc(m);
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- numeric kernel ---------------------------------------------------------------------------
+constexpr int kSRecBytes = kMaxDom * 15 * 8;
+constexpr int kXBytes = al16(kMaxVerts * 3 * 8);
+constexpr int kAsmSmem = 2 * (kSRecBytes + kXBytes + kBlobCap) + kTileRows * kDiagSplit * 6 * 8 + 128;
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// s_K of domain k from the staged coordinates.  FS: field (a, b, c, d, e) -- the face nodes and
+// the vertices opposite the face in its tets (a, b, c, d) and (a, b, c, e); each tet's weights
+// w_K = (V_e / 4) grad N_K^e = sign(det) (cross product of two edges) / 24 land on known field
+// positions; s_K = (sum over the tets of w_K) / sqrt(V_f), V_f = sum |det| / 24 (closed form of
+// Eq. 7, reading Q24).  FEM-T4: s_I = sqrt(V_e) grad N_I (reading Q25).
 template <bool kTet>
-__global__ void __launch_bounds__(256) k_assemble_rows(
-    const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ nbr, const int64_t* __restrict__ nf_ptr,
-    const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ face_nodes, const int32_t* __restrict__ face_opp,
-    const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam, double mu, double* __restrict__ vals,
-    int min_deg) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t il = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; il < nloc;
-       il += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int32_t self = static_cast<int32_t>(n_lo + il);
-    const int64_t P = node_ptr[il];
-    const int deg = static_cast<int>(node_ptr[il + 1] - P);
-    if (deg <= min_deg) continue;  // handled by k_assemble_rows2
-    const int64_t f0 = nf_ptr[il], f1 = nf_ptr[il + 1];
-    double* blocks = vals + 9 * P;
-    for (int s0 = 0; s0 < deg; s0 += 32) {
-      const int s = s0 + lane;
-      const int32_t j = (s < deg) ? nbr[P + s] : -2;
+__device__ __forceinline__ void domain_s(const double* __restrict__ X, const unsigned char* fv, double* out) {
+  auto P = [&](int p, double& x, double& y, double& z) {
+    const double* q = X + 3 * fv[p];
+    x = q[0];
+    y = q[1];
+    z = q[2];
+  };
+  if (kTet) {
+    double x0, y0, z0, x1, y1, z1, x2, y2, z2, x3, y3, z3;
+    P(0, x0, y0, z0);
+    P(1, x1, y1, z1);
+    P(2, x2, y2, z2);
+    P(3, x3, y3, z3);
+    const double e1x = x1 - x0, e1y = y1 - y0, e1z = z1 - z0;
+    const double e2x = x2 - x0, e2y = y2 - y0, e2z = z2 - z0;
+    const double e3x = x3 - x0, e3y = y3 - y0, e3z = z3 - z0;
+    double g[4][3];
+    g[1][0] = e2y * e3z - e2z * e3y;
+    g[1][1] = e2z * e3x - e2x * e3z;
+    g[1][2] = e2x * e3y - e2y * e3x;
+    g[2][0] = e3y * e1z - e3z * e1y;
+    g[2][1] = e3z * e1x - e3x * e1z;
+    g[2][2] = e3x * e1y - e3y * e1x;
+    g[3][0] = e1y * e2z - e1z * e2y;
+    g[3][1] = e1z * e2x - e1x * e2z;
+    g[3][2] = e1x * e2y - e1y * e2x;
+    const double det = e1x * g[1][0] + e1y * g[1][1] + e1z * g[1][2];
+    const double V = fabs(det) * (1.0 / 6.0);
+    const double sc = sqrt(V) / det;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const double a = g[1][h] * sc, b = g[2][h] * sc, c = g[3][h] * sc;
+      out[3 + h] = a;
+      out[6 + h] = b;
+      out[9 + h] = c;
+      out[h] = -(a + b + c);
+      out[12 + h] = 0.0;
+    }
+    return;
+  }
+  double ax, ay, az, bx, by, bz, cx, cy, cz, dx, dy, dz;
+  P(0, ax, ay, az);
+  P(1, bx, by, bz);
+  P(2, cx, cy, cz);
+  P(3, dx, dy, dz);
+  const bool two = fv[4] != 255;
+  double ex = 0.0, ey = 0.0, ez = 0.0;
+  if (two) P(4, ex, ey, ez);
+  const double e1x = bx - ax, e1y = by - ay, e1z = bz - az;
+  const double e2x = cx - ax, e2y = cy - ay, e2z = cz - az;
+  const double c3x = e1y * e2z - e1z * e2y, c3y = e1z * e2x - e1x * e2z, c3z = e1x * e2y - e1y * e2x;
+  double g[5][3];
+  double Vf;
+  {  // tet (a, b, c, d)
+    const double e3x = dx - ax, e3y = dy - ay, e3z = dz - az;
+    const double c1x = e2y * e3z - e2z * e3y, c1y = e2z * e3x - e2x * e3z, c1z = e2x * e3y - e2y * e3x;
+    const double c2x = e3y * e1z - e3z * e1y, c2y = e3z * e1x - e3x * e1z, c2z = e3x * e1y - e3y * e1x;
+    const double det = e1x * c1x + e1y * c1y + e1z * c1z;
+    const double sc = (det > 0.0 ? 1.0 : -1.0) * (1.0 / 24.0);
+    g[1][0] = c1x * sc; g[1][1] = c1y * sc; g[1][2] = c1z * sc;
+    g[2][0] = c2x * sc; g[2][1] = c2y * sc; g[2][2] = c2z * sc;
+    g[3][0] = c3x * sc; g[3][1] = c3y * sc; g[3][2] = c3z * sc;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) g[0][h] = -(g[1][h] + g[2][h] + g[3][h]);
+    g[4][0] = g[4][1] = g[4][2] = 0.0;
+    Vf = fabs(det) * (1.0 / 24.0);
+  }
+  if (two) {  // tet (a, b, c, e)
+    const double e3x = ex - ax, e3y = ey - ay, e3z = ez - az;
+    const double c1x = e2y * e3z - e2z * e3y, c1y = e2z * e3x - e2x * e3z, c1z = e2x * e3y - e2y * e3x;
+    const double c2x = e3y * e1z - e3z * e1y, c2y = e3z * e1x - e3x * e1z, c2z = e3x * e1y - e3y * e1x;
+    const double det = e1x * c1x + e1y * c1y + e1z * c1z;
+    const double sc = (det > 0.0 ? 1.0 : -1.0) * (1.0 / 24.0);
+    const double w1[3] = {c1x * sc, c1y * sc, c1z * sc}, w2[3] = {c2x * sc, c2y * sc, c2z * sc},
+                 w3[3] = {c3x * sc, c3y * sc, c3z * sc};
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      g[0][h] += -(w1[h] + w2[h] + w3[h]);
+      g[1][h] += w1[h];
+      g[2][h] += w2[h];
+      g[4][h] = w3[h];
+    }
+    Vf += fabs(det) * (1.0 / 24.0);
+  }
+  const double rs = 1.0 / sqrt(Vf);
+#pragma unroll
+  for (int K = 0; K < 5; ++K) {
+    out[3 * K] = g[K][0] * rs;
+    out[3 * K + 1] = g[K][1] * rs;
+    out[3 * K + 2] = g[K][2] * rs;
+  }
+}
+
+// Warps 0-7 produce (blob, coordinates, s records of tile j into buffer j & 1), warps 8-15
+// consume (tasks, writes).  Named barriers: 1 + b "buffer b full" (producers arrive, consumers
+// sync), 3 + b "buffer b free" (consumers arrive, producers sync), 5 producers only, 6 consumers.
+template <bool kTet>
+__global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __restrict__ tile_off,
+                                                             const unsigned char* __restrict__ gblob, int64_t ntiles,
+                                                             const double* __restrict__ xyz, double lam, double mu,
+                                                             double* __restrict__ vals) {
+  extern __shared__ __align__(16) unsigned char asm_sm[];
+  double* dpart = reinterpret_cast<double*>(asm_sm + 2 * (kSRecBytes + kXBytes + kBlobCap));  // [rows][split][6]
+  const int tid = threadIdx.x;
+  const bool producer = tid < kGroup;
+  const int gt = producer ? tid : tid - kGroup;  // thread index inside the group
+  const int K = ntiles > blockIdx.x ? static_cast<int>((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto buf_S = [&](int b) { return reinterpret_cast<double*>(asm_sm + b * (kSRecBytes + kXBytes + kBlobCap)); };
+  auto buf_X = [&](int b) { return reinterpret_cast<double*>(asm_sm + b * (kSRecBytes + kXBytes + kBlobCap) + kSRecBytes); };
+  auto buf_B = [&](int b) {
+    return asm_sm + b * (kSRecBytes + kXBytes + kBlobCap) + kSRecBytes + kXBytes;
+  };
+  if (producer) {
+    for (int j = 0; j < K; ++j) {
+      const int b = j & 1;
+      if (j >= 2) named_sync(3 + b, kAsmThreads);  // consumers are done with buffer b
+      const int64_t t = blockIdx.x + static_cast<int64_t>(j) * gridDim.x;
+      unsigned char* blob = buf_B(b);
+      {
+        const int64_t o = tile_off[t];
+        const int n16 = static_cast<int>((tile_off[t + 1] - o) >> 4);
+        const int4* src = reinterpret_cast<const int4*>(gblob + o);
+        for (int k = gt; k < n16; k += kGroup) reinterpret_cast<int4*>(blob)[k] = __ldg(src + k);
+      }
+      named_sync(5, kGroup);
+      const TileHdr h = *reinterpret_cast<const TileHdr*>(blob);
+      const TileLayout L(h.nrows, h.nverts, h.ndom, h.ntask, h.nent);
+      const int32_t* verts = reinterpret_cast<const int32_t*>(blob + L.o_verts);
+      double* X = buf_X(b);
+      for (int k = gt; k < 3 * h.nverts; k += kGroup) {
+        const int v = k / 3, c = k - 3 * v;
+        X[k] = __ldg(xyz + 3 * static_cast<int64_t>(verts[v]) + c);
+      }
+      named_sync(5, kGroup);
+      const unsigned char* fv = blob + L.o_fv;
+      double* S = buf_S(b);
+      for (int k = gt; k < h.ndom; k += kGroup) domain_s<kTet>(X, fv + 5 * k, S + 15 * k);
+      __threadfence_block();
+      named_arrive(1 + b, kAsmThreads);  // buffer b full
+    }
+    for (int j = (K > 2 ? K - 2 : 0); j < K; ++j) named_sync(3 + (j & 1), kAsmThreads);  // match the last frees
+    return;
+  }
+  for (int j = 0; j < K; ++j) {
+    const int b = j & 1;
+    named_sync(1 + b, kAsmThreads);
+    const unsigned char* blob = buf_B(b);
+    const double* S = buf_S(b);
+    const TileHdr h = *reinterpret_cast<const TileHdr*>(blob);
+    const TileLayout L(h.nrows, h.nverts, h.ndom, h.ntask, h.nent);
+    const TileRow* rows = reinterpret_cast<const TileRow*>(blob + L.o_rows);
+    const TileTask* tasks = reinterpret_cast<const TileTask*>(blob + L.o_task);
+    const uint16_t* ent = reinterpret_cast<const uint16_t*>(blob + L.o_ent);
+    for (int a = gt; a < h.ntask; a += kGroup) {
+      const TileTask tk = tasks[a];
       double M[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) M[q] = 0.0;
-      for (int64_t k = f0; k < f1; ++k) {
-        const int32_t f = nf_idx[k];
-        const double* sf = face_s + kRec * static_cast<int64_t>(f);
-        int32_t fld[5];
-        field_of(face_nodes, face_opp, kTet, f, fld);
-        int pi = 0, pj = -1;
-#pragma unroll
-        for (int K = 0; K < 5; ++K) {
-          pi = (fld[K] == self) ? K : pi;
-          pj = (fld[K] == j) ? K : pj;
-        }
-        if (pj >= 0) {
-          const double si0 = sf[3 * pi], si1 = sf[3 * pi + 1], si2 = sf[3 * pi + 2];
-          const double sj0 = sf[3 * pj], sj1 = sf[3 * pj + 1], sj2 = sf[3 * pj + 2];
-          M[0] = fma(si0, sj0, M[0]);
-          M[1] = fma(si0, sj1, M[1]);
-          M[2] = fma(si0, sj2, M[2]);
-          M[3] = fma(si1, sj0, M[3]);
-          M[4] = fma(si1, sj1, M[4]);
-          M[5] = fma(si1, sj2, M[5]);
-          M[6] = fma(si2, sj0, M[6]);
-          M[7] = fma(si2, sj1, M[7]);
-          M[8] = fma(si2, sj2, M[8]);
-        }
-      }
-      if (s < deg) {
-        const double tr = M[0] + M[4] + M[8];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double v = fma(lam, M[3 * a + c], mu * M[3 * c + a]);
-            if (a == c) v = fma(mu, tr, v);
-            blocks[9 * s + 3 * a + c] = v;
-          }
-      }
-    }
-  }
-}
-
-
-// Assembly program (once per pattern; thread per own node, faces of F(i) in ascending order):
-// nf_pi[k] = field position of i in the k-th face; for every other field node v that is a
-// stored column of row i (v > i, or a halo column v < n_lo) the entry k | (position of v) << 13
-// is appended to the list of v's stored block, so every list is ascending in k.
-constexpr int kProgMaxFaces = 8000;  // k < 8192 - 32 keeps the 0xffff sentinel above every round
-
-// Warp per own node; the faces of F(i) in rounds of 32 (lane = face).  Count pass: nf_pi and the
-// number of entries of every stored block (shared counters; order irrelevant).  Fill pass: per
-// round, slot by slot, the lanes holding the slot's column write in lane (= ascending face) order.
-constexpr int kProgWarps = 8;
-template <bool kFill>
-__global__ void __launch_bounds__(kProgWarps * 32) k_prog(
-    const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
-    const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a, const int32_t* __restrict__ rec_b, bool tet,
-    int64_t n_lo, int64_t nloc, uint8_t* __restrict__ nf_pi, int32_t* __restrict__ cnt,
-    const int32_t* __restrict__ blk_ent, uint16_t* __restrict__ prog, unsigned long long* __restrict__ err) {
-  __shared__ int32_t sh_cols[kProgWarps][32];
-  __shared__ int32_t sh_cnt[kProgWarps][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t il = blockIdx.x * (int64_t)kProgWarps + w; il < nloc; il += (int64_t)gridDim.x * kProgWarps) {
-    const int32_t i = static_cast<int32_t>(n_lo + il);
-    const int64_t P = sptr[il];
-    const int ds = static_cast<int>(sptr[il + 1] - P);
-    if (ds > 32) continue;  // generic path (no program)
-    const int64_t f0 = nf_ptr[il];
-    const int nfc = static_cast<int>(nf_ptr[il + 1] - f0);
-    if (nfc >= kProgMaxFaces) {
-      if (!kFill && lane == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, i);
-      continue;
-    }
-    sh_cols[w][lane] = lane < ds ? snbr[P + lane] : 0x7fffffff;
-    sh_cnt[w][lane] = (kFill && lane < ds) ? blk_ent[P + lane] : 0;
-    __syncwarp();
-    for (int rb = 0; rb < nfc; rb += 32) {
-      const int k = rb + lane;
-      int tslot[4] = {-1, -1, -1, -1}, tk[4] = {0, 0, 0, 0};
-      if (k < nfc) {
-        int32_t fld[5];
-        field_of(rec_a, rec_b, tet, nf_idx[f0 + k], fld);
-        int pi = 0;
-#pragma unroll
-        for (int K = 0; K < 5; ++K) pi = (fld[K] == i) ? K : pi;
-        if (!kFill) nf_pi[f0 + k] = static_cast<uint8_t>(pi);
-        int t = 0;
-#pragma unroll
-        for (int K = 0; K < 5; ++K) {
-          const int32_t v = fld[K];
-          if (K == pi || v < 0 || (v < i && v >= n_lo)) continue;
-          int lo = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1)
-            if (sh_cols[w][lo + step - 1] < v) lo += step;
-          tslot[t] = lo;
-          tk[t] = K;
-          ++t;
-          if (!kFill) atomicAdd(&sh_cnt[w][lo], 1);
-        }
-      }
-      if (kFill) {
-        for (int sl = 0; sl < ds; ++sl) {  // warp-uniform: lane order = ascending face order
-          int K = -1;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) K = (tslot[t] == sl) ? tk[t] : K;
-          const unsigned m = __ballot_sync(0xffffffffu, K >= 0);
-          if (K >= 0) prog[sh_cnt[w][sl] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(k | (K << 13));
-          __syncwarp();
-          if (lane == 0) sh_cnt[w][sl] += __popc(m);
-          __syncwarp();
-        }
-      }
-    }
-    __syncwarp();
-    if (!kFill && lane < ds) cnt[P + lane] = sh_cnt[w][lane];
-    __syncwarp();
-  }
-}
-
-// Fast path, warp per own node i with <= 32 stored blocks (diagonal + j > i + halo j < n_lo),
-// driven by the assembly program.  Rounds of 32 records (faces of F(i), or tets for FEM-T4;
-// ascending):
-//   load: the warp copies the round's 32 records (128 B each) into shared memory with coalesced
-//      16-byte cp.async (8 warp instructions);
-//   diagonal: lane = face, s_i s_i^T into the lane's partial sum (fixed warp tree at the end);
-//   off-diagonal: lane = stored slot walks its program entries of the round (ascending face),
-//      adding s_i s_K^T; rows with <= 16 stored blocks give every slot two lanes, one for the
-//      even and one for the odd entries, combined at the end in that order.
-// Summation order is fixed by the program: results do not depend on timing.
-constexpr int kRowWarps = 4;
-#ifndef FSFEM_ASM_MINB
-#define FSFEM_ASM_MINB 8
-#endif
-// Shared-memory record stride (doubles).  128-B records at a 128-B stride put every record's
-// s_K in the same banks (32-way conflicts when the lanes of a warp read the same K of different
-// records).  18 doubles (144 B) spreads them over 8 bank offsets with 16-B copies: 581 us vs
-// 806 us at 16 and 654 us at 17 (odd stride: conflict-free reads but 8-B copies), cfg4.
-#ifndef FSFEM_ASM_STRIDE
-#define FSFEM_ASM_STRIDE 18
-#endif
-constexpr int kSh = FSFEM_ASM_STRIDE;
-
-__global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_rows3(
-    const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr, const int64_t* __restrict__ nf_ptr,
-    const int32_t* __restrict__ nf_idx, const uint8_t* __restrict__ nf_pi, const int32_t* __restrict__ blk_ent,
-    const uint16_t* __restrict__ prog, const double* __restrict__ face_s, int64_t n_lo, int64_t nloc, double lam,
-    double mu, double* __restrict__ vals) {
-  __shared__ __align__(16) double sh_rec[kRowWarps][32][kSh];
-  __shared__ uint8_t sh_pi[kRowWarps][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t il = blockIdx.x * (int64_t)kRowWarps + w; il < nloc; il += (int64_t)gridDim.x * kRowWarps) {
-    const int32_t self = static_cast<int32_t>(n_lo + il);
-    const int64_t P = sptr[il];
-    const int ds = static_cast<int>(sptr[il + 1] - P);
-    if (ds > 32) continue;  // generic path
-    const bool split = ds <= 16;
-    const int slot = split ? (lane & 15) : lane;
-    const int step = split ? 2 : 1;
-    int e = 0, e_end = 0;
-    if (slot < ds) {
-      e = blk_ent[P + slot] + (split ? (lane >> 4) : 0);
-      e_end = blk_ent[P + slot + 1];
-    }
-    uint32_t ent = e < e_end ? prog[e] : 0xffffu;
-    const int32_t my_col = lane < ds ? snbr[P + lane] : -1;
-    const int64_t f0 = nf_ptr[il];
-    const int nfc = static_cast<int>(nf_ptr[il + 1] - f0);
-    double d[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // diagonal partial: xx yy zz xy xz yz
-    double M[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) M[q] = 0.0;
-    for (int rb = 0; rb < nfc; rb += 32) {
-      const int nact = min(32, nfc - rb);
-      const int32_t myr = lane < nact ? nf_idx[f0 + rb + lane] : 0;
-      const int mypi = lane < nact ? nf_pi[f0 + rb + lane] : 0;
-      if (kSh % 2 == 0) {  // 16-B pieces (record slots 16-B aligned)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int c = lane + 32 * q;
-          const int k = c >> 3, part = c & 7;
-          const int32_t r = __shfl_sync(0xffffffffu, myr, k);
-          if (k < nact) {
-            const double2* src = reinterpret_cast<const double2*>(face_s + kRec * static_cast<int64_t>(r)) + part;
-            const uint32_t dst =
-                static_cast<uint32_t>(__cvta_generic_to_shared(&sh_rec[w][k][0])) + 16u * static_cast<uint32_t>(part);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-          }
-        }
-      } else {  // 8-B pieces (odd stride)
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int c = lane + 32 * q;
-          const int k = c >> 4, part = c & 15;
-          const int32_t r = __shfl_sync(0xffffffffu, myr, k);
-          if (k < nact) {
-            const double* src = face_s + kRec * static_cast<int64_t>(r) + part;
-            const uint32_t dst =
-                static_cast<uint32_t>(__cvta_generic_to_shared(&sh_rec[w][k][0])) + 8u * static_cast<uint32_t>(part);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-          }
-        }
-      }
-      sh_pi[w][lane] = static_cast<uint8_t>(mypi);
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
-      if (lane < nact) {
-        const double* sf = sh_rec[w][lane];
-        const double s0 = sf[3 * mypi], s1 = sf[3 * mypi + 1], s2 = sf[3 * mypi + 2];
-        d[0] = fma(s0, s0, d[0]);
-        d[1] = fma(s1, s1, d[1]);
-        d[2] = fma(s2, s2, d[2]);
-        d[3] = fma(s0, s1, d[3]);
-        d[4] = fma(s0, s2, d[4]);
-        d[5] = fma(s1, s2, d[5]);
-      }
-      const uint32_t kend = static_cast<uint32_t>(rb + 32);
-      while ((ent & 0x1fffu) < kend) {  // (0xffff: no more entries; its k = 8191 >= any kend)
-        const int kl = static_cast<int>(ent & 0x1fffu) - rb, K = static_cast<int>(ent >> 13);
-        e += step;
-        const uint32_t nxt = e < e_end ? prog[e] : 0xffffu;
-        const double* rf = sh_rec[w][kl];
-        const int pb = sh_pi[w][kl];
-        const double a0 = rf[3 * pb], a1 = rf[3 * pb + 1], a2 = rf[3 * pb + 2];
-        const double c0 = rf[3 * K], c1 = rf[3 * K + 1], c2 = rf[3 * K + 2];
+      const int stride = tk.sub == 255 ? 1 : kDiagSplit;
+      int e = tk.estart;
+      for (int c = 0; c < tk.count; ++c, e += stride) {
+        const int en = ent[e];
+        const int code = en & 31;
+        const int pi = code / 5, pj = code - 5 * pi;
+        const double* sd = S + 15 * (en >> 5);
+        const double a0 = sd[3 * pi], a1 = sd[3 * pi + 1], a2 = sd[3 * pi + 2];
+        const double c0 = sd[3 * pj], c1 = sd[3 * pj + 1], c2 = sd[3 * pj + 2];
         M[0] = fma(a0, c0, M[0]);
         M[1] = fma(a0, c1, M[1]);
         M[2] = fma(a0, c2, M[2]);
@@ -434,111 +750,170 @@ __global__ void __launch_bounds__(kRowWarps * 32, FSFEM_ASM_MINB) k_assemble_row
         M[6] = fma(a2, c0, M[6]);
         M[7] = fma(a2, c1, M[7]);
         M[8] = fma(a2, c2, M[8]);
-        ent = nxt;
       }
-      __syncwarp();
-    }
-    if (split) {  // slot s = (even entries) + (odd entries): lane s adds lane s+16's partial
+      if (tk.sub == 255) {
+        const double tr = M[0] + M[4] + M[8];
+        double* out = vals + 9 * (rows[tk.row].P + tk.slot);
 #pragma unroll
-      for (int q = 0; q < 9; ++q) M[q] += __shfl_down_sync(0xffffffffu, M[q], 16);
-    }
-    // diagonal block: fixed warp tree of the per-lane partial sums
+        for (int aa = 0; aa < 3; ++aa)
 #pragma unroll
-    for (int q = 0; q < 6; ++q) d[q] = warp_sum(d[q]);
-    double* blocks = vals + 9 * P;
-    if (lane < ds && my_col == self) {
+          for (int cc = 0; cc < 3; ++cc) {
+            double v = fma(lam, M[3 * aa + cc], mu * M[3 * cc + aa]);
+            if (aa == cc) v = fma(mu, tr, v);
+            out[3 * aa + cc] = v;
+          }
+      } else {  // diagonal sub-list: the 6 independent entries of the symmetric partial
+        double* dp = dpart + 6 * (kDiagSplit * tk.row + tk.sub);
+        dp[0] = M[0];
+        dp[1] = M[4];
+        dp[2] = M[8];
+        dp[3] = M[1];
+        dp[4] = M[2];
+        dp[5] = M[5];
+      }
+    }
+    named_sync(6, kGroup);
+    if (gt < h.nrows && rows[gt].sdiag >= 0) {  // diagonal blocks: sub-list sums in order
+      const int r = gt;
+      double d[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int q = 0; q < kDiagSplit; ++q)
+#pragma unroll
+        for (int v = 0; v < 6; ++v) d[v] += dpart[6 * (kDiagSplit * r + q) + v];
       const double Md[9] = {d[0], d[3], d[4], d[3], d[1], d[5], d[4], d[5], d[2]};
+      const double tr = Md[0] + Md[4] + Md[8];
+      double* out = vals + 9 * (rows[r].P + rows[r].sdiag);
 #pragma unroll
-      for (int q = 0; q < 9; ++q) M[q] = Md[q];
-    }
-    if (lane < ds) {
-      const double tr = M[0] + M[4] + M[8];
+      for (int aa = 0; aa < 3; ++aa)
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double v = fma(lam, M[3 * a + c], mu * M[3 * c + a]);
-          if (a == c) v = fma(mu, tr, v);
-          blocks[9 * lane + 3 * a + c] = v;
+        for (int cc = 0; cc < 3; ++cc) {
+          double v = fma(lam, Md[3 * aa + cc], mu * Md[3 * cc + aa]);
+          if (aa == cc) v = fma(mu, tr, v);
+          out[3 * aa + cc] = v;
         }
     }
-    __syncwarp();
+    named_sync(6, kGroup);              // dpart reused by the next tile
+    named_arrive(3 + b, kAsmThreads);   // buffer b free
   }
 }
+
 }  // namespace
 
 void face_s_device(const double* xyz, const int32_t* tets, const int32_t* face_nodes, const int32_t* face_tet,
                    const int32_t* face_opp, int64_t nf, double* face_s, double* face_V, cudaStream_t s) {
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nf, 256), 16LL * num_sms()));
-  k_face_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, face_nodes, face_tet, face_opp, nf, face_s, face_V);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nf, 256), 16LL * num_sms())));
+  k_face_s<<<grid, 256, 0, s>>>(xyz, tets, face_nodes, face_tet, face_opp, nf, face_s, face_V);
   FS_LAUNCH_CHECK();
-}
-
-// Assembly program of the pattern (once; pattern.cuh).  rec_a/rec_b: FS face_nodes/face_opp,
-// FEM-T4 tets/unused.  Returns the error word (kNoError if fine).
-void build_assembly_program(Pattern& pat, const int32_t* rec_a, const int32_t* rec_b, bool tet,
-                            DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s) {
-  const int64_t nloc = pat.nloc, nsb = pat.nsb;
-  pat.nf_pi.ensure(std::max<int64_t>(pat.nfi, 1));
-  pat.blk_ent.ensure(nsb + 1);
-  const size_t tb = scan_tmp_bytes(nsb + 1);
-  const size_t o_cnt = 0, o_flags = (sizeof(int32_t) * (nsb + 1) + 255) & ~size_t(255),
-               o_tmp = o_flags + 256;
-  unsigned char* base = scratch.ensure(o_tmp + tb);
-  int32_t* cnt = reinterpret_cast<int32_t*>(base + o_cnt);
-  unsigned long long* flags = reinterpret_cast<unsigned long long*>(base + o_flags);
-  FS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nsb + 1), s));
-  FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
-  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kProgWarps), 32LL * num_sms())));
-  if (nloc > 0) {
-    k_prog<false><<<g, kProgWarps * 32, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
-                                    tet, pat.n_lo, nloc, pat.nf_pi.get(), cnt, nullptr, nullptr, flags);
-    FS_LAUNCH_CHECK();
-  }
-  exclusive_scan_i32(cnt, pat.blk_ent.get(), nsb, s, base + o_tmp, tb);
-  int32_t total = 0;
-  FS_CUDA(cudaMemcpyAsync(&total, pat.blk_ent.get() + nsb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaStreamSynchronize(s));
-  if (h_flags[0] != kNoError) return;
-  pat.prog.ensure(std::max<int64_t>(total, 1));
-  if (nloc > 0) {
-    k_prog<true><<<g, kProgWarps * 32, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(), rec_a, rec_b,
-                                   tet, pat.n_lo, nloc, nullptr, nullptr, pat.blk_ent.get(), pat.prog.get(), flags);
-    FS_LAUNCH_CHECK();
-  }
-  pat.have_prog = true;
-}
-
-// rec_a/rec_b: FS (kTet = false) face_nodes/face_opp; FEM-T4 (tet = true) tets/unused.
-void assemble_rows_device(const Pattern& pat, const int32_t* face_nodes, const int32_t* face_opp,
-                          const double* face_s, double lam, double mu, double* vals, bool tet, cudaStream_t s) {
-  const int64_t nloc = pat.nloc;
-  if (nloc == 0) return;
-  // Persistent grid of exactly the resident CTAs: warp w takes nodes w, w + W, ... so the nodes in
-  // flight form one contiguous window that slides forward; the field nodes of a face (which span
-  // less than two windows in a banded numbering) are then assembled close together in time and
-  // the face's record is re-read from L2, not DRAM.
-  static int per_sm = 0;
-  if (per_sm == 0) FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assemble_rows3, kRowWarps * 32, 0));
-  const int g2 = static_cast<int>(
-      std::min<int64_t>(ceil_div(nloc, kRowWarps), static_cast<int64_t>(std::max(1, per_sm)) * num_sms()));
-  k_assemble_rows3<<<std::max(g2, 1), kRowWarps * 32, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(),
-                                                              pat.nf_idx.get(), pat.nf_pi.get(), pat.blk_ent.get(),
-                                                              pat.prog.get(), face_s, pat.n_lo, nloc, lam, mu, vals);
-  FS_LAUNCH_CHECK();
-  if (pat.max_row_blocks > 32) {
-    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nloc * 32, 256), 32LL * num_sms()));
-    auto k1 = tet ? k_assemble_rows<true> : k_assemble_rows<false>;
-    k1<<<std::max(grid, 1), 256, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.nf_ptr.get(), pat.nf_idx.get(),
-                                         face_nodes, face_opp, face_s, pat.n_lo, nloc, lam, mu, vals, 32);
-    FS_LAUNCH_CHECK();
-  }
 }
 
 void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s) {
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(nt, 256), 16LL * num_sms()));
-  k_tet_s<<<std::max(grid, 1), 256, 0, s>>>(xyz, tets, nt, tet_s, tet_V);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nt, 256), 16LL * num_sms())));
+  k_tet_s<<<grid, 256, 0, s>>>(xyz, tets, nt, tet_s, tet_V);
+  FS_LAUNCH_CHECK();
+}
+
+void morton_order_device(const double* d_xyz, int64_t nn, int32_t* iperm, int32_t* perm, DevBuf<unsigned char>& scratch,
+                         cudaStream_t s);
+
+// Assembly tiles of the pattern (once per pattern; pattern.cuh).  rec_a / rec_b: FS
+// face_nodes / face_opp, FEM-T4 tets / unused.  xyz: node coordinates (the tiles follow a Morton
+// curve of the own nodes).  Returns an error word in h_flags[0] (kNoError if fine).
+void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a, const int32_t* rec_b, bool tet,
+                          DevBuf<unsigned char>& scratch, unsigned long long* h_flags, cudaStream_t s) {
+  const int64_t nloc = pat.nloc;
+  h_flags[0] = kNoError;
+  pat.ntiles = 0;
+  if (nloc <= 0) {
+    pat.tile_off.ensure(1);
+    FS_CUDA(cudaMemsetAsync(pat.tile_off.get(), 0, sizeof(int64_t), s));
+    return;
+  }
+  DevBuf<int32_t> order, inv;
+  order.ensure(nloc);
+  inv.ensure(nloc);
+  morton_order_device(xyz + 3 * pat.n_lo, nloc, order.get(), inv.get(), scratch, s);
+  std::vector<int32_t> ts;
+  for (int64_t a = 0; a < nloc; a += kTileRows) ts.push_back(static_cast<int32_t>(a));
+  ts.push_back(static_cast<int32_t>(nloc));
+  static bool attr = false;
+  const int bsmem =
+      static_cast<int>(sizeof(int32_t) * (2 * kSortCap + kMaxDom + 5 * kMaxDom + 2 * (kMaxBlk + 1) + 2 * kMaxTask));
+  if (!attr) {
+    FS_CUDA(cudaFuncSetAttribute(k_tile_build<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+    FS_CUDA(cudaFuncSetAttribute(k_tile_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+    FS_CUDA(cudaFuncSetAttribute(k_asm_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
+    FS_CUDA(cudaFuncSetAttribute(k_asm_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
+    attr = true;
+  }
+  DevBuf<int32_t> d_ts;
+  DevBuf<int64_t> d_size;
+  std::vector<int64_t> sz;
+  for (int pass = 0;; ++pass) {
+    const int64_t nt = static_cast<int64_t>(ts.size()) - 1;
+    d_ts.ensure(nt + 1);
+    d_size.ensure(nt);
+    FS_CUDA(cudaMemcpyAsync(d_ts.get(), ts.data(), sizeof(int32_t) * (nt + 1), cudaMemcpyHostToDevice, s));
+    const int g = static_cast<int>(std::min<int64_t>(nt, 8LL * num_sms()));
+    k_tile_build<false><<<g, kBldThreads, bsmem, s>>>(order.get(), d_ts.get(), nt, pat.nf_ptr.get(), pat.nf_idx.get(),
+                                                     rec_a, rec_b, tet, pat.sptr.get(), pat.snbr.get(), pat.sdiag.get(),
+                                                     pat.n_lo, d_size.get(), nullptr, nullptr);
+    FS_LAUNCH_CHECK();
+    sz.resize(nt);
+    FS_CUDA(cudaMemcpyAsync(sz.data(), d_size.get(), sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> nts;
+    bool split = false;
+    for (int64_t k = 0; k < nt; ++k) {
+      nts.push_back(ts[k]);
+      if (sz[k] == -2) {  // one row whose domains exceed the tile caps
+        std::vector<int32_t> hord(1);
+        FS_CUDA(cudaMemcpy(hord.data(), order.get() + ts[k], sizeof(int32_t), cudaMemcpyDeviceToHost));
+        h_flags[0] = (static_cast<unsigned long long>(FSFEM_ERR_UNSUPPORTED) << 56) |
+                     static_cast<unsigned long long>(pat.n_lo + hord[0]);
+        return;
+      }
+      if (sz[k] == -1) {
+        nts.push_back((ts[k] + ts[k + 1]) / 2);
+        split = true;
+      }
+    }
+    nts.push_back(ts[nt]);
+    if (!split) break;
+    ts.swap(nts);
+  }
+  const int64_t nt = static_cast<int64_t>(ts.size()) - 1;
+  std::vector<int64_t> off(nt + 1, 0);
+  int64_t mx = 0;
+  for (int64_t k = 0; k < nt; ++k) {
+    off[k + 1] = off[k] + sz[k];
+    mx = std::max(mx, sz[k]);
+  }
+  pat.ntiles = nt;
+  pat.tile_blob_max = mx;
+  pat.tile_off.ensure(nt + 1);
+  pat.tile_blob.ensure(std::max<int64_t>(off[nt], 16));
+  FS_CUDA(cudaMemcpyAsync(pat.tile_off.get(), off.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, s));
+  const int g = static_cast<int>(std::min<int64_t>(nt, 8LL * num_sms()));
+  k_tile_build<true><<<g, kBldThreads, bsmem, s>>>(order.get(), d_ts.get(), nt, pat.nf_ptr.get(), pat.nf_idx.get(),
+                                                  rec_a, rec_b, tet, pat.sptr.get(), pat.snbr.get(), pat.sdiag.get(),
+                                                  pat.n_lo, nullptr, pat.tile_off.get(), pat.tile_blob.get());
+  FS_LAUNCH_CHECK();
+  FS_CUDA(cudaStreamSynchronize(s));  // the host vectors above must outlive the copies
+}
+
+// Numeric assembly of the own rows into the stored blocks (S2-S4 + S6).
+void assemble_tiles_device(const Pattern& pat, const double* xyz, double lam, double mu, double* vals, bool tet,
+                           cudaStream_t s) {
+  if (pat.ntiles <= 0) return;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    FS_CUDA(cudaFuncSetAttribute(k_asm_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
+    FS_CUDA(cudaFuncSetAttribute(k_asm_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
+    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_tile<false>, kAsmThreads, kAsmSmem));
+    per_sm = std::max(1, per_sm);
+  }
+  const int g = static_cast<int>(std::min<int64_t>(pat.ntiles, static_cast<int64_t>(per_sm) * num_sms()));
+  auto k = tet ? k_asm_tile<true> : k_asm_tile<false>;
+  k<<<g, kAsmThreads, kAsmSmem, s>>>(pat.tile_off.get(), pat.tile_blob.get(), pat.ntiles, xyz, lam, mu, vals);
   FS_LAUNCH_CHECK();
 }
 

@@ -33,6 +33,7 @@ struct Error : std::runtime_error {
 void count_launch(long long n = 1);
 long long launch_count();
 void set_capturing(bool on);
+long long captured_launches();
 
 #define FS_LAUNCH_CHECK()              \
   do {                                 \

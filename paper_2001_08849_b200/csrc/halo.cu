@@ -8,6 +8,8 @@
 // grouped by owner rank) and the pack / unpack kernels; the exchange itself is NCCL send/recv
 // in api.cu.
 #include "common.cuh"
+#include <algorithm>
+#include <vector>
 #include "pattern.cuh"
 
 namespace fsfem {
@@ -48,9 +50,10 @@ int grid_n(int64_t n) {
 }  // namespace
 
 // Halo list of the rank (pat.halo, ascending global ids) and its size; per-owner counts on the
-// host (owner q holds nodes [q * chunk, (q + 1) * chunk)).
-void build_halo_device(Pattern& pat, int64_t nn, int64_t chunk, int nranks, std::vector<int64_t>& need,
+// host (owner q holds nodes [ranges[q], ranges[q + 1])).
+void build_halo_device(Pattern& pat, int64_t nn, const std::vector<int64_t>& ranges, std::vector<int64_t>& need,
                        DevBuf<unsigned char>& scratch, cudaStream_t s) {
+  const int nranks = static_cast<int>(ranges.size()) - 1;
   const int64_t n_hi = pat.n_lo + pat.nloc;
   const size_t tb = scan_tmp_bytes(nn + 1);
   const size_t o_flag = 0, o_pos = (sizeof(int32_t) * (nn + 1) + 255) & ~size_t(255),
@@ -75,7 +78,11 @@ void build_halo_device(Pattern& pat, int64_t nn, int64_t chunk, int nranks, std:
   if (nh > 0) FS_CUDA(cudaMemcpyAsync(h.data(), pat.halo.get(), sizeof(int32_t) * nh, cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
   need.assign(nranks, 0);
-  for (int32_t j : h) need[std::min<int64_t>(nranks - 1, j / chunk)] += 1;
+  for (int32_t j : h) {
+    const int q = static_cast<int>(std::upper_bound(ranges.begin(), ranges.end(), static_cast<int64_t>(j)) -
+                                   ranges.begin()) - 1;
+    need[std::min(nranks - 1, std::max(0, q))] += 1;
+  }
 }
 
 void halo_pack_device(const double* full, const int32_t* nodes, int64_t n, double* buf, cudaStream_t s) {

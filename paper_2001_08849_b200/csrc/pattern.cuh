@@ -58,20 +58,20 @@ struct Pattern {
   bool df_ok = false;        // every chunk's producer list fits kMaxDeps
   DevBuf<int32_t> dep_ptr;   // [nchunks + 1]
   DevBuf<int2> dep_list;     // [dep_ptr[nchunks]] (chunk d, need[d])
-  DevBuf<uint32_t> cnt;      // [nchunks] arrival counters (mod need)
+  DevBuf<uint32_t> cnt;      // [nchunks] arrival counters, wrapping at need (atomicInc: 0 .. need-1)
   DevBuf<double> dotc;       // [nchunks] per-chunk p.q partials
   // halo of the rank (halo.cu, row partitions only): columns of the own rows outside the range
   int64_t nhalo = 0;
   DevBuf<int32_t> halo;      // [nhalo] global node ids, ascending (grouped by owner rank)
   DevBuf<int64_t> nf_ptr;    // [nloc+1]
   DevBuf<int32_t> nf_idx;    // [nfi] faces whose field holds node i, ascending
-  // Assembly program (assemble.cu, built once per pattern): for the k-th face of F(i) the field
-  // position of i (nf_pi), and per stored block (i, j) the faces of F(i) holding j with j's field
-  // position, ascending: prog[blk_ent[b] .. blk_ent[b+1]) = k | (position << 13).
-  bool have_prog = false;
-  DevBuf<uint8_t> nf_pi;     // [nfi]
-  DevBuf<int32_t> blk_ent;   // [nsb + 1]
-  DevBuf<uint16_t> prog;     // [blk_ent[nsb]]
+  // Assembly tiles (assemble.cu, built once per pattern): the own nodes in Morton order cut into
+  // tiles of <= kTileRows rows; per tile one contiguous blob (TileHdr + rows, vertices, field
+  // positions, per-block entry counts, program entries), tile t at blob + tile_off[t].
+  int64_t ntiles = 0;
+  int64_t tile_blob_max = 0;  // largest tile blob (bytes)
+  DevBuf<int64_t> tile_off;   // [ntiles + 1] byte offsets (16-B aligned)
+  DevBuf<unsigned char> tile_blob;
 };
 
 }  // namespace fsfem

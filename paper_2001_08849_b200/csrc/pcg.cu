@@ -650,11 +650,12 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
 #pragma unroll
       for (int b = 0; b < kDfBatch; ++b)
 #pragma unroll
-        for (int r = 0; r < R; ++r) old[b][r] = e[b][r].x >= 0 ? atomicAdd(cnt + e[b][r].x, 1u) : 0u;
+        for (int r = 0; r < R; ++r)
+          old[b][r] = e[b][r].x >= 0 ? atomicInc(cnt + e[b][r].x, static_cast<uint32_t>(e[b][r].y) - 1u) : 0u;
       for (int b = 0; b < jd - j; ++b)  // dependants beyond R * 32 (rare)
         for (int q = qq0[b] + 32 * R + lane; q < qq1[b]; q += 32) {
           const int2 ee = dep_list[q];
-          if ((atomicAdd(cnt + ee.x, 1u) + 1u) % static_cast<uint32_t>(ee.y) == 0u) {
+          if (atomicInc(cnt + ee.x, static_cast<uint32_t>(ee.y) - 1u) == static_cast<uint32_t>(ee.y) - 1u) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
             asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ready + ee.x), "r"(epoch) : "memory");
           }
@@ -666,7 +667,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       for (int b = 0; b < kDfBatch; ++b)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (e[b][r].x >= 0 && (old[b][r] + 1u) % static_cast<uint32_t>(e[b][r].y) == 0u) {
+          if (e[b][r].x >= 0 && old[b][r] == static_cast<uint32_t>(e[b][r].y) - 1u) {
             my_ready[nready++] = e[b][r].x;
             any_last = true;
           }
@@ -1213,24 +1214,29 @@ __global__ void __launch_bounds__(kThreads) k_init(const double* __restrict__ f,
   }
 }
 
-// ||f - q||^2 over own rows -> st->local[3] (true residual check).
-__global__ void __launch_bounds__(kThreads) k_resid(const double* __restrict__ f, const double* __restrict__ q, int64_t n,
-                                                    PcgState* st, double* part) {
-  double s = 0.0;
+// ||f - q||^2 over own rows -> st->local[3] (true residual check), ||x||^2 -> st->local[1].
+__global__ void __launch_bounds__(kThreads) k_resid(const double* __restrict__ f, const double* __restrict__ q,
+                                                    const double* __restrict__ x, int64_t n, PcgState* st,
+                                                    double* part) {
+  double s = 0.0, xx = 0.0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const double d = f[k] - q[k];
     s = fma(d, d, s);
+    xx = fma(x[k], x[k], xx);
   }
-  const double mine[1] = {s};
-  double out[1];
-  if (grid_reduce<1>(mine, part, &st->ticket[3], out) && threadIdx.x == 0) st->local[3] = out[0];
+  const double mine[2] = {s, xx};
+  double out[2];
+  if (grid_reduce<2>(mine, part, &st->ticket[3], out) && threadIdx.x == 0) {
+    st->local[3] = out[0];
+    st->local[1] = out[1];
+  }
 }
 
 // Multi-rank: combine per-rank partials gathered in `all[nranks*4]` in rank order.
-__global__ void k_combine(PcgState* st, const double* __restrict__ all, int stage) {
+__global__ void k_combine(PcgState* st, const double* __restrict__ all, int stage, int nranks) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s[4] = {0, 0, 0, 0};
-  for (int r = 0; r < st->nranks; ++r)
+  for (int r = 0; r < nranks; ++r)
     for (int v = 0; v < 4; ++v) s[v] += all[4 * r + v];
   if (stage == 0) finish_init(st, s[0], s[1], s[2]);
   if (stage == 1) {
@@ -1241,7 +1247,12 @@ __global__ void k_combine(PcgState* st, const double* __restrict__ all, int stag
     if (ld_cg(&st->done_d) != 0.0) return;
     finish_beta(st, s[1], s[2]);
   }
-  if (stage == 3) st->local[3] = s[3];
+  if (stage == 3) {  // true residual, ||x||^2, ||K||_F^2 bound
+    st->local[1] = s[1];
+    st->local[2] = s[2];
+    st->local[3] = s[3];
+  }
+  if (stage == 5) st->local[2] = s[2];  // ||K||_F^2 bound only (deterministic mode)
   if (stage == 4) {  // single-reduction variant: (u.w, gamma', r.r) in one collective
     if (ld_cg(&st->done_d) != 0.0) return;
     finish_cg(st, s[0], s[1], s[2]);
@@ -1396,8 +1407,9 @@ void launch_init(const double* f, const double* q, const double* dinv, double* r
   FS_LAUNCH_CHECK();
 }
 
-void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s) {
-  k_resid<<<vec_grid(n), kThreads, 0, s>>>(f, q, n, st, part);
+void launch_resid(const double* f, const double* q, const double* x, int64_t n, PcgState* st, double* part,
+                  cudaStream_t s) {
+  k_resid<<<vec_grid(n), kThreads, 0, s>>>(f, q, x, n, st, part);
   FS_LAUNCH_CHECK();
 }
 
@@ -1409,8 +1421,8 @@ void launch_cg_update(double* x, double* r, double* u, double* p, double* sv, co
   FS_LAUNCH_CHECK();
 }
 
-void launch_combine(PcgState* st, const double* all, int stage, cudaStream_t s) {
-  k_combine<<<1, 32, 0, s>>>(st, all, stage);
+void launch_combine(PcgState* st, const double* all, int stage, int nranks, cudaStream_t s) {
+  k_combine<<<1, 32, 0, s>>>(st, all, stage, nranks);
   FS_LAUNCH_CHECK();
 }
 

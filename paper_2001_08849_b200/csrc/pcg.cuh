@@ -1,6 +1,7 @@
 // Device-resident PCG scalars and the scalar steps of the recurrence.
 #pragma once
 #include "common.cuh"
+#include <vector>
 #include "pattern.cuh"
 
 namespace fsfem {
@@ -118,6 +119,26 @@ __device__ __forceinline__ void finish_cg(PcgState* st, double delta, double gam
   }
 }
 
+// Deterministic dots (det.cu): fixed global chunks of this many nodes; partition ranges are
+// aligned to it in deterministic mode.
+constexpr int64_t kDetChunkNodes = 256;
+int64_t det_nchunks(int64_t nn);
+// kind 0 init (r.z, r.r, f.f), 1 p.q, 2 update x, r (r.r, r.z), 3 true residual (|f-q|^2, x.x);
+// partials of the own rows' chunks into dpart[3 * chunk + v].
+void launch_det_dots(int kind, int64_t n_lo, int64_t nloc, const double* f, const double* q, const double* dinv,
+                     double* r, double* p, double* x, PcgState* st, double* dpart, cudaStream_t s);
+// Sum of all chunk partials in chunk order, then the scalar step (0 init, 1 alpha, 2 beta, 3 resid).
+void launch_det_finish(PcgState* st, const double* dpart, int64_t nchg, int stage, cudaStream_t s);
+// Canonical-order SpMV (no fused dot): bitwise independent of the partition.
+void launch_spmv_canon(const Pattern& pat, const double* vals, const double* x_full, double* y, const PcgState* st,
+                       cudaStream_t s);
+// 2 * sum of squares of the stored values (bound of ||K||_F^2 of the rank's rows) -> st->local[2].
+void launch_sumsq(const double* vals, int64_t n, PcgState* st, double* part, cudaStream_t s);
+// Node ranges of the ranks (det.cu), balanced by node-face incidences, aligned to `align`.
+void partition_ranges_device(const int32_t* face_nodes, const int32_t* face_opp, int64_t nf, int64_t nn, int nranks,
+                             int64_t align, DevBuf<unsigned char>& scratch, cudaStream_t s,
+                             std::vector<int64_t>& ranges);
+
 int pcg_grid();
 int spmv_kind(const Pattern& pat);  // 0 small, 1 gather, 2 dataflow (pcg.cu)
 // y (own rows) = K x_full; own_off = 3 * n_lo, the offset of the own rows in x_full (the dataflow
@@ -132,8 +153,12 @@ void launch_update_direction(double* x, double* r, double* p, const double* q, c
                              PcgState* st, double* part, cudaStream_t s);
 void launch_init(const double* f, const double* q, const double* dinv, double* r, double* p, int64_t n, PcgState* st,
                  double* part, cudaStream_t s);
-void launch_resid(const double* f, const double* q, int64_t n, PcgState* st, double* part, cudaStream_t s);
-void launch_combine(PcgState* st, const double* all, int stage, cudaStream_t s);
+// ||f - q||^2 -> st->local[3] and ||x||^2 (own rows) -> st->local[1].
+void launch_resid(const double* f, const double* q, const double* x, int64_t n, PcgState* st, double* part,
+                  cudaStream_t s);
+// Multi-rank: per-rank partials all[4 * nranks] summed in rank order, then the scalar step
+// (stage 0 init, 1 alpha, 2 beta, 3 true residual, 4 single-reduction, 5 ||K||_F^2 bound).
+void launch_combine(PcgState* st, const double* all, int stage, int nranks, cudaStream_t s);
 // Single-reduction variant: p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s,
 // u = dinv r; per-CTA partials of r.u and r.r into upd_part (no grid-wide step).
 void launch_cg_update(double* x, double* r, double* u, double* p, double* sv, const double* w, const double* dinv,

@@ -382,7 +382,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   exclusive_scan_i32(cnt, ptr, nloc, s, tmp, tb);
   k_scatter_node_tets<<<g4, 256, 0, s>>>(d_tets, 4 * nt, n_lo, n_lo + nloc, ptr, cur, idx);
   FS_LAUNCH_CHECK();
-  const int gw = static_cast<int>(std::min<int64_t>(ceil_div(nloc, kPatWarps), 32LL * sms));
+  const int gw = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kPatWarps), 32LL * sms)));
   k_sort_segments<<<gw, kPatWarps * 32, 0, s>>>(ptr, nloc, idx, flags);
   FS_LAUNCH_CHECK();
   k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc, deg,
@@ -474,7 +474,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
     FS_LAUNCH_CHECK();
   }
   if (pat.nchunks > 0) {
-    const int gd = static_cast<int>(std::min<int64_t>(ceil_div(pat.nchunks, kDepWarps), 16LL * sms));
+    const int gd = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pat.nchunks, kDepWarps), 16LL * sms)));
     k_chunk_deps<<<gd, kDepWarps * 32, 0, s>>>(pat.chunks.get(), static_cast<int>(pat.nchunks), pat.tlist.get(), n_lo,
                                                pat.deps.get(), pat.ndeps.get());
     FS_LAUNCH_CHECK();

@@ -25,7 +25,8 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
 # Every symbol include/fsfem.h declares (checked by tests/test_abi.py).
 METHOD_FS, METHOD_FEM_T4 = 0, 1
 
-EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
+EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init",
+           "fsfem_comm_init_loopback", "fsfem_get_partition", "fsfem_set_deterministic", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
            "fsfem_surface_loads"]
@@ -39,7 +40,9 @@ class FsfemReport(ctypes.Structure):
                 ("t_spmv_ms", ctypes.c_double), ("spmv_launches", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("stored_blocks", ctypes.c_int64),
                 ("transposed_blocks", ctypes.c_int64), ("spmv_bytes", ctypes.c_int64),
-                ("assembly_bytes", ctypes.c_int64), ("spmv_kernel", ctypes.c_int64)]
+                ("assembly_bytes", ctypes.c_int64), ("spmv_kernel", ctypes.c_int64),
+                ("residual_floor", ctypes.c_double), ("restarts", ctypes.c_int64),
+                ("assembly_aux_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -70,6 +73,9 @@ def load_library(path: str = LIB_PATH):
         "fsfem_destroy": (I, [P]),
         "fsfem_last_error": (ctypes.c_char_p, [P]),
         "fsfem_comm_init": (I, [P, P, I, I]),
+        "fsfem_comm_init_loopback": (I, [P, I]),
+        "fsfem_get_partition": (I, [P, P]),
+        "fsfem_set_deterministic": (I, [P, I]),
         "fsfem_set_method": (I, [P, I]),
         "fsfem_set_reorder": (I, [P, I]),
         "fsfem_set_pcg_variant": (I, [P, I]),
@@ -159,13 +165,31 @@ def fsfem_comm_init(ctx, unique_id: bytes | None, rank: int, nranks: int) -> Non
     _raise(ctx, load_library().fsfem_comm_init(ctx, buf, rank, nranks))
 
 
+def fsfem_comm_init_loopback(ctxs) -> None:
+    """Make the contexts ctxs[0..n) ranks 0..n-1 of one in-process loopback group (include/fsfem.h)."""
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.value if isinstance(c, ctypes.c_void_p) else c for c in ctxs])
+    st = load_library().fsfem_comm_init_loopback(arr, len(ctxs))
+    if st != 0:
+        _raise(ctxs[0], st)
+
+
+def fsfem_get_partition(ctx, nranks: int) -> np.ndarray:
+    out = np.zeros(nranks + 1, np.int64)
+    _raise(ctx, load_library().fsfem_get_partition(ctx, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def fsfem_set_deterministic(ctx, on: bool) -> None:
+    _raise(ctx, load_library().fsfem_set_deterministic(ctx, 1 if on else 0))
+
+
 def fsfem_set_method(ctx, method: int) -> None:
     _raise(ctx, load_library().fsfem_set_method(ctx, int(method)))
 
 
 def fsfem_set_pcg_variant(ctx, variant: int) -> None:
     """0: standard PCG recurrence, 1: single reduction per iteration (Chronopoulos-Gear),
-    2: auto (default: single reduction with several ranks, standard on one GPU)."""
+    2: auto (default: the standard recurrence)."""
     _raise(ctx, load_library().fsfem_set_pcg_variant(ctx, int(variant)))
 
 
@@ -286,6 +310,13 @@ class FsFem:
 
     def comm_init(self, unique_id: bytes | None, rank: int, nranks: int):
         fsfem_comm_init(self.ctx, unique_id, rank, nranks)
+        self.nranks = nranks
+
+    def partition(self) -> np.ndarray:
+        return fsfem_get_partition(self.ctx, getattr(self, "nranks", 1))
+
+    def set_deterministic(self, on: bool = True):
+        fsfem_set_deterministic(self.ctx, on)
 
     def set_reorder(self, mode: int):
         fsfem_set_reorder(self.ctx, mode)

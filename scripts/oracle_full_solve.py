@@ -3,7 +3,9 @@
 Writes tests/golden/oracle_cfg<N>.json: faces, nnz, PCG iterations, residuals, tip deflection
 and a deterministic sample of displacement entries.  Calls only oracle/ and fsfem_inputs/
 (never the CUDA path).  Used by tests (parity at full size) and by bench.py's CPU baseline
-(iteration count of the full solve).  Usage: python scripts/oracle_full_solve.py 4
+(iteration count of the full solve).  Usage: python scripts/oracle_full_solve.py 4 [chunks] [--fem]
+--fem: the oracle's FEM-T4 companion (O8) instead of FS-FEM ->
+tests/golden/oracle_cfg<N>_fem.json (the FS >= FEM tip-deflection pin).
 """
 import json
 import os
@@ -20,7 +22,7 @@ from oracle import Oracle  # noqa: E402
 E, NU = 1.0e6, 0.3
 
 
-def main(cfg: int, chunks: int = 4):
+def main(cfg: int, chunks: int = 4, fem: bool = False):
     m = config_mesh(cfg)
     o = Oracle(m.xyz, m.tets)
     t = {}
@@ -32,7 +34,7 @@ def main(cfg: int, chunks: int = 4):
     off = 0
     t0 = time.perf_counter()
     for a, b in zip(bounds[:-1], bounds[1:]):
-        lo, rp, ci, va = o.assemble_fs(E, NU, int(a), int(b))
+        lo, rp, ci, va = (o.assemble_fem if fem else o.assemble_fs)(E, NU, int(a), int(b))
         rps.append(rp[:-1] + off)
         off += rp[-1]
         cis.append(ci)
@@ -55,13 +57,16 @@ def main(cfg: int, chunks: int = 4):
                nnz=int(rp[-1]), pcg=rep, tip_mean_uz=float(u.reshape(-1, 3)[m.tip, 2].mean()),
                u_norm=float(np.linalg.norm(u)), u_sample_idx=idx.tolist(), u_sample=u[idx].tolist(),
                f_dot_u=float(m.loads.reshape(-1) @ u), timings_s=t, threads=int(os.environ.get("OMP_NUM_THREADS", "0")),
+               method="FEM-T4" if fem else "FS-FEM",
                note="written by scripts/oracle_full_solve.py from oracle/ only")
-    path = os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}.json")
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}{'_fem' if fem else ''}.json")
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)
-    np.save(os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}_u.npy"), u) if cfg <= 3 else None
+    if cfg <= 4 and not fem:
+        np.save(os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}_u.npy"), u)
     print(json.dumps({k: v for k, v in out.items() if not k.startswith("u_sample")}, indent=1))
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]), int(sys.argv[2]) if len(sys.argv) > 2 else 4)
+    pos = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(int(pos[0]), int(pos[1]) if len(pos) > 1 else 4, fem="--fem" in sys.argv)

@@ -34,8 +34,12 @@ def main():
     loads = torch.from_numpy(m.loads.reshape(-1).copy()).to(dev)
     u = torch.zeros(3 * m.n_nodes, dtype=torch.float64, device=dev)
     fsfem_build_faces(g.ctx, xyz, tets)
+    t_num = []
     for _ in range(1 + a.reassemble):
         fsfem_assemble_csr(g.ctx, 1.0e6, 0.3)
+        t_num.append(round(g.report()["t_numeric_ms"], 4))
+    print("numeric assembly ms per call:", t_num, "aux bytes", g.report()["assembly_aux_bytes"],
+          "alg bytes", g.report()["assembly_bytes"])
     fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
     try:
         rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)

@@ -32,13 +32,13 @@ def fs():
 
 def _check(fs, m, nranks):
     x = np.random.default_rng(nranks).standard_normal(3 * m.n_nodes)
-    chunk = -(-m.n_nodes // nranks)
     for r in range(nranks):
-        lo, hi = min(m.n_nodes, r * chunk), min(m.n_nodes, (r + 1) * chunk)
         g = fs()
         g.comm_init(None, r, nranks)
         g.set_exchange(1)
         g.build_faces(m.xyz, m.tets)
+        rng = g.partition()
+        lo, hi = int(rng[r]), int(rng[r + 1])
         g.assemble_csr(E, NU)
         halo = g.halo()
         cols = np.unique(g.get_csr().col_idx // 3)

@@ -227,7 +227,10 @@ def test_full_size_faces_and_sampled_rows(fs, cfg):
     g.assemble_csr(E, NU)
     assert g.nnz == c["nnz_fs"]
     o = Oracle(m.xyz, m.tets)
-    o.build_faces()
+    ofn, oft, ofo = o.build_faces()
+    # bit-exact against the oracle's map-based face table at full size
+    assert np.array_equal(fn, ofn) and np.array_equal(ft, oft) and np.array_equal(fo, ofo)
+    del ofn, oft, ofo
     rng = np.random.default_rng(cfg)
     for lo in [0, m.n_nodes - 400, *rng.integers(0, m.n_nodes - 300, 2)]:
         check_csr(g, o, int(lo), int(lo) + 257)
@@ -266,12 +269,13 @@ def test_row_partition_contexts(fs, nranks):
     x = np.random.default_rng(nranks).standard_normal(3 * m.n_nodes)
     q_ref = o.spmv(x)
     orp_bc, oci_bc, ova_bc, _ = o.apply_bc(m.dirichlet, m.loads, 0)
-    chunk = -(-m.n_nodes // nranks)
     for r in range(nranks):
-        lo, hi = min(m.n_nodes, r * chunk), min(m.n_nodes, (r + 1) * chunk)
         g = fs()
         g.comm_init(None, r, nranks)
         g.build_faces(m.xyz, m.tets)
+        rng = g.partition()
+        assert rng[0] == 0 and rng[-1] == m.n_nodes and np.all(np.diff(rng) > 0)
+        lo, hi = int(rng[r]), int(rng[r + 1])
         rb, nr, nnz = g.assemble_csr(E, NU)
         assert (rb, nr) == (3 * lo, 3 * (hi - lo))
         c = g.get_csr()
@@ -323,12 +327,16 @@ def test_cfg3_displacements_match_oracle(fs):
 
 
 def test_cfg4_displacements_match_oracle(fs):
-    """cfg4 (bench workload): compliance, tip deflection and 4096 sampled dofs against the
-    oracle's full solve (tests/golden/oracle_cfg4.json)."""
+    """cfg4 (bench workload): the WHOLE u against the oracle's full solve
+    (tests/golden/oracle_cfg4_u.npy, written by scripts/oracle_full_solve.py 4 from oracle/ only:
+    ||u - u_ora||_2 <= 1e-7 ||u_ora||_2), plus compliance, tip deflection and the json samples."""
+    import os
     m = config_mesh(4)
     g, u, rep = _gpu_solve(fs, m)
     gold = _golden(4)
     assert rep["converged"] == 1
+    uo = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_cfg4_u.npy"))
+    assert np.linalg.norm(u - uo) <= U_TOL * np.linalg.norm(uo)
     f = m.loads.reshape(-1)
     assert abs(f @ u - gold["f_dot_u"]) <= 1e-8 * abs(gold["f_dot_u"])
     tip = u.reshape(-1, 3)[m.tip, 2].mean()

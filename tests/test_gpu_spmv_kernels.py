@@ -92,12 +92,13 @@ g.assemble_csr(1.0e6, 0.3)
 full = g.spmv(x)
 res = {{"full": full}}
 for nranks in (2, 3):
-    chunk = -(-m.n_nodes // nranks)
     for r in range(nranks):
-        lo, hi = min(m.n_nodes, r * chunk), min(m.n_nodes, (r + 1) * chunk)
         h = FsFem()
         h.comm_init(None, r, nranks)
         h.build_faces(m.xyz, m.tets)
+        rng = h.partition()
+        lo, hi = int(rng[r]), int(rng[r + 1])
+        res[f"r{{nranks}}"] = rng
         h.assemble_csr(1.0e6, 0.3)
         res[f"q{{nranks}}_{{r}}"] = h.spmv(x)[3 * lo:3 * hi]
         res[f"k{{nranks}}_{{r}}"] = np.array([h.report()["spmv_kernel"]])
@@ -117,9 +118,9 @@ def test_spmv_kernel_row_partition(kernel, tmp_path):
     n_nodes = full.size // 3
     want = 1 if kernel == "gather" else 2
     for nranks in (2, 3):
-        chunk = -(-n_nodes // nranks)
+        rng = r[f"r{nranks}"]
         for k in range(nranks):
-            lo, hi = min(n_nodes, k * chunk), min(n_nodes, (k + 1) * chunk)
+            lo, hi = int(rng[k]), int(rng[k + 1])
             q = r[f"q{nranks}_{k}"]
             assert np.abs(q - full[3 * lo:3 * hi]).max() <= 1e-12 * np.abs(full).max()
             assert int(r[f"k{nranks}_{k}"][0]) in (0, want)  # small partitions may fall back to warp per node

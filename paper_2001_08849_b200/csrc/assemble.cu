@@ -213,7 +213,7 @@ constexpr int kDiagCap = 2048;    // sum over the tile rows of |F(i)|
 constexpr int kMaxBlk = 767;      // stored blocks of the tile rows
 constexpr int kMaxTask = 1024;
 constexpr int kDiagSplit = 4;     // strided sub-lists of a diagonal block
-constexpr int kBlobCap = 16384;   // bytes of one tile blob
+constexpr int kBlobCap = 14336;   // bytes of one tile blob
 constexpr int kAsmWarps = 16;     // 8 producer + 8 consumer warps
 constexpr int kAsmThreads = 32 * kAsmWarps;
 constexpr int kGroup = kAsmThreads / 2;
@@ -561,7 +561,9 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
 // ---- numeric kernel ---------------------------------------------------------------------------
 constexpr int kSRecBytes = kMaxDom * 15 * 8;
 constexpr int kXBytes = al16(kMaxVerts * 3 * 8);
-constexpr int kAsmSmem = 2 * (kSRecBytes + kXBytes + kBlobCap) + kTileRows * kDiagSplit * 6 * 8 + 128;
+constexpr int kBlobSlots = 4;
+constexpr int kAsmSmem = 2 * (kSRecBytes + kXBytes) + kBlobSlots * kBlobCap + kTileRows * kDiagSplit * 6 * 8 +
+                         8 * kBlobSlots + 128;
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) {
@@ -667,50 +669,112 @@ __device__ __forceinline__ void domain_s(const double* __restrict__ X, const uns
   }
 }
 
-// Warps 0-7 produce (blob, coordinates, s records of tile j into buffer j & 1), warps 8-15
+// Warps 0-7 produce tile j into S/X buffer j & 1 (s records from the coordinates; the blob of
+// tile j + 2 is bulk-copied (TMA) into blob slot (j + 2) % 4 and the coordinates of tile j + 1
+// gathered with cp.async meanwhile, so neither latency is on the producer's path), warps 8-15
 // consume (tasks, writes).  Named barriers: 1 + b "buffer b full" (producers arrive, consumers
 // sync), 3 + b "buffer b free" (consumers arrive, producers sync), 5 producers only, 6 consumers.
+__device__ __forceinline__ uint32_t sm_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void tma_blob(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm_u32(dst)), "l"(src), "r"(bytes), "r"(sm_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
+                   sm_u32(bar)), "r"(parity)
+               : "memory");
+}
+
 template <bool kTet>
 __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __restrict__ tile_off,
                                                              const unsigned char* __restrict__ gblob, int64_t ntiles,
                                                              const double* __restrict__ xyz, double lam, double mu,
                                                              double* __restrict__ vals) {
-  extern __shared__ __align__(16) unsigned char asm_sm[];
-  double* dpart = reinterpret_cast<double*>(asm_sm + 2 * (kSRecBytes + kXBytes + kBlobCap));  // [rows][split][6]
+  extern __shared__ __align__(128) unsigned char asm_sm[];
+  double* Sb = reinterpret_cast<double*>(asm_sm);                                   // [2][kMaxDom * 15]
+  double* Xb = reinterpret_cast<double*>(asm_sm + 2 * kSRecBytes);                  // [2][kXBytes / 8]
+  unsigned char* Bb = asm_sm + 2 * kSRecBytes + 2 * kXBytes;                        // [kBlobSlots][kBlobCap]
+  double* dpart = reinterpret_cast<double*>(Bb + kBlobSlots * kBlobCap);           // [rows][split][6]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dpart + kTileRows * kDiagSplit * 6);  // [kBlobSlots]
   const int tid = threadIdx.x;
   const bool producer = tid < kGroup;
   const int gt = producer ? tid : tid - kGroup;  // thread index inside the group
   const int K = ntiles > blockIdx.x ? static_cast<int>((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  auto buf_S = [&](int b) { return reinterpret_cast<double*>(asm_sm + b * (kSRecBytes + kXBytes + kBlobCap)); };
-  auto buf_X = [&](int b) { return reinterpret_cast<double*>(asm_sm + b * (kSRecBytes + kXBytes + kBlobCap) + kSRecBytes); };
-  auto buf_B = [&](int b) {
-    return asm_sm + b * (kSRecBytes + kXBytes + kBlobCap) + kSRecBytes + kXBytes;
-  };
+  auto tile = [&](int j) { return blockIdx.x + static_cast<int64_t>(j) * gridDim.x; };
+  auto blob_of = [&](int j) { return Bb + (j % kBlobSlots) * kBlobCap; };
   if (producer) {
-    for (int j = 0; j < K; ++j) {
-      const int b = j & 1;
-      if (j >= 2) named_sync(3 + b, kAsmThreads);  // consumers are done with buffer b
-      const int64_t t = blockIdx.x + static_cast<int64_t>(j) * gridDim.x;
-      unsigned char* blob = buf_B(b);
-      {
-        const int64_t o = tile_off[t];
-        const int n16 = static_cast<int>((tile_off[t + 1] - o) >> 4);
-        const int4* src = reinterpret_cast<const int4*>(gblob + o);
-        for (int k = gt; k < n16; k += kGroup) reinterpret_cast<int4*>(blob)[k] = __ldg(src + k);
-      }
-      named_sync(5, kGroup);
+    auto issue_blob = [&](int j) {  // one thread
+      const int64_t t = tile(j);
+      const int64_t o = tile_off[t];
+      tma_blob(blob_of(j), gblob + o, static_cast<uint32_t>(tile_off[t + 1] - o), &bars[j % kBlobSlots]);
+    };
+    auto wait_blob = [&](int j) { mbar_wait_parity(&bars[j % kBlobSlots], (j / kBlobSlots) & 1); };
+    auto issue_x = [&](int j) {  // all producers: cp.async of the tile's vertex coordinates
+      const unsigned char* blob = blob_of(j);
       const TileHdr h = *reinterpret_cast<const TileHdr*>(blob);
       const TileLayout L(h.nrows, h.nverts, h.ndom, h.ntask, h.nent);
       const int32_t* verts = reinterpret_cast<const int32_t*>(blob + L.o_verts);
-      double* X = buf_X(b);
+      double* X = Xb + (j & 1) * (kXBytes / 8);
       for (int k = gt; k < 3 * h.nverts; k += kGroup) {
         const int v = k / 3, c = k - 3 * v;
-        X[k] = __ldg(xyz + 3 * static_cast<int64_t>(verts[v]) + c);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sm_u32(X + k)),
+                     "l"(xyz + 3 * static_cast<int64_t>(verts[v]) + c)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (gt == 0) {
+      for (int k = 0; k < kBlobSlots; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&bars[k])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (K > 0) issue_blob(0);
+      if (K > 1) issue_blob(1);
+    }
+    named_sync(5, kGroup);
+    if (K > 0) {
+      wait_blob(0);
+      issue_x(0);
+    }
+    for (int j = 0; j < K; ++j) {
+      const int b = j & 1;
+      if (j >= 2) named_sync(3 + b, kAsmThreads);  // consumers are done with tile j - 2
+      if (gt == 0 && j + 2 < K) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_blob(j + 2);  // slot (j + 2) % 4 held tile j - 2
+      }
+      if (j + 1 < K) {
+        wait_blob(j + 1);
+        issue_x(j + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // tile j's coordinates landed
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       named_sync(5, kGroup);
+      const unsigned char* blob = blob_of(j);
+      const TileHdr h = *reinterpret_cast<const TileHdr*>(blob);
+      const TileLayout L(h.nrows, h.nverts, h.ndom, h.ntask, h.nent);
       const unsigned char* fv = blob + L.o_fv;
-      double* S = buf_S(b);
-      for (int k = gt; k < h.ndom; k += kGroup) domain_s<kTet>(X, fv + 5 * k, S + 15 * k);
+      const double* X = Xb + b * (kXBytes / 8);
+      double* S = Sb + b * (kSRecBytes / 8);
+#ifndef FSFEM_ASM_SKIP
+#define FSFEM_ASM_SKIP 0
+#endif
+      if (FSFEM_ASM_SKIP != 1) {
+        // two domains per thread and pass (independent FP64 chains interleave)
+        for (int k = gt; k < h.ndom; k += 2 * kGroup) {
+          const int k2 = k + kGroup;
+          double o1[15], o2[15];
+          domain_s<kTet>(X, fv + 5 * k, o1);
+          domain_s<kTet>(X, fv + 5 * min(k2, h.ndom - 1), o2);
+#pragma unroll
+          for (int q = 0; q < 15; ++q) S[15 * k + q] = o1[q];
+          if (k2 < h.ndom)
+#pragma unroll
+            for (int q = 0; q < 15; ++q) S[15 * k2 + q] = o2[q];
+        }
+      }
       __threadfence_block();
       named_arrive(1 + b, kAsmThreads);  // buffer b full
     }
@@ -720,36 +784,52 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
   for (int j = 0; j < K; ++j) {
     const int b = j & 1;
     named_sync(1 + b, kAsmThreads);
-    const unsigned char* blob = buf_B(b);
-    const double* S = buf_S(b);
+    const unsigned char* blob = blob_of(j);
+    const double* S = Sb + b * (kSRecBytes / 8);
     const TileHdr h = *reinterpret_cast<const TileHdr*>(blob);
     const TileLayout L(h.nrows, h.nverts, h.ndom, h.ntask, h.nent);
     const TileRow* rows = reinterpret_cast<const TileRow*>(blob + L.o_rows);
     const TileTask* tasks = reinterpret_cast<const TileTask*>(blob + L.o_task);
     const uint16_t* ent = reinterpret_cast<const uint16_t*>(blob + L.o_ent);
-    for (int a = gt; a < h.ntask; a += kGroup) {
+    for (int a = gt; a < (FSFEM_ASM_SKIP == 2 ? 0 : h.ntask); a += kGroup) {
       const TileTask tk = tasks[a];
       double M[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) M[q] = 0.0;
-      const int stride = tk.sub == 255 ? 1 : kDiagSplit;
       int e = tk.estart;
-      for (int c = 0; c < tk.count; ++c, e += stride) {
-        const int en = ent[e];
-        const int code = en & 31;
-        const int pi = code / 5, pj = code - 5 * pi;
-        const double* sd = S + 15 * (en >> 5);
-        const double a0 = sd[3 * pi], a1 = sd[3 * pi + 1], a2 = sd[3 * pi + 2];
-        const double c0 = sd[3 * pj], c1 = sd[3 * pj + 1], c2 = sd[3 * pj + 2];
-        M[0] = fma(a0, c0, M[0]);
-        M[1] = fma(a0, c1, M[1]);
-        M[2] = fma(a0, c2, M[2]);
-        M[3] = fma(a1, c0, M[3]);
-        M[4] = fma(a1, c1, M[4]);
-        M[5] = fma(a1, c2, M[5]);
-        M[6] = fma(a2, c0, M[6]);
-        M[7] = fma(a2, c1, M[7]);
-        M[8] = fma(a2, c2, M[8]);
+      if (tk.sub == 255) {  // off-diagonal block: s_i s_J^T, 6 doubles per entry
+#pragma unroll 2
+        for (int c = 0; c < tk.count; ++c, ++e) {
+          const int en = ent[e];
+          const int code = en & 31;
+          const int pi = code / 5, pj = code - 5 * pi;
+          const double* sd = S + 15 * (en >> 5);
+          const double a0 = sd[3 * pi], a1 = sd[3 * pi + 1], a2 = sd[3 * pi + 2];
+          const double c0 = sd[3 * pj], c1 = sd[3 * pj + 1], c2 = sd[3 * pj + 2];
+          M[0] = fma(a0, c0, M[0]);
+          M[1] = fma(a0, c1, M[1]);
+          M[2] = fma(a0, c2, M[2]);
+          M[3] = fma(a1, c0, M[3]);
+          M[4] = fma(a1, c1, M[4]);
+          M[5] = fma(a1, c2, M[5]);
+          M[6] = fma(a2, c0, M[6]);
+          M[7] = fma(a2, c1, M[7]);
+          M[8] = fma(a2, c2, M[8]);
+        }
+      } else {  // diagonal sub-list: s_i s_i^T, 3 doubles per entry (upper triangle)
+#pragma unroll 2
+        for (int c = 0; c < tk.count; ++c, e += kDiagSplit) {
+          const int en = ent[e];
+          const int pi = (en & 31) / 6;  // code = 5 pi + pi
+          const double* sd = S + 15 * (en >> 5) + 3 * pi;
+          const double a0 = sd[0], a1 = sd[1], a2 = sd[2];
+          M[0] = fma(a0, a0, M[0]);
+          M[1] = fma(a0, a1, M[1]);
+          M[2] = fma(a0, a2, M[2]);
+          M[4] = fma(a1, a1, M[4]);
+          M[5] = fma(a1, a2, M[5]);
+          M[8] = fma(a2, a2, M[8]);
+        }
       }
       if (tk.sub == 255) {
         const double tr = M[0] + M[4] + M[8];
@@ -792,7 +872,7 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
         }
     }
     named_sync(6, kGroup);              // dpart reused by the next tile
-    named_arrive(3 + b, kAsmThreads);   // buffer b free
+    named_arrive(3 + b, kAsmThreads);   // buffer b free (S, X and the blob slot of tile j)
   }
 }
 

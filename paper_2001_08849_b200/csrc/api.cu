@@ -958,11 +958,7 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
                         (c->rep.spmv_kernel == 2 ? 4 * c->pat.nsb : 8 * c->pat.ntb) + 16 * (c->nloc + 1) +
                         24 * c->nn + 24 * c->nloc;
     c->rep.assembly_bytes = 24 * c->nn + 16 * c->nt + 72 * c->pat.nsb;
-    {
-      int64_t blob = 0;
-      FS_CUDA(cudaMemcpy(&blob, c->pat.tile_off.get() + c->pat.ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
-      c->rep.assembly_aux_bytes = blob;
-    }
+    c->rep.assembly_aux_bytes = c->pat.tile_blob_bytes;
     if (row_begin) *row_begin = 3 * c->n_lo;
     if (n_rows) *n_rows = 3 * c->nloc;
     if (nnz) *nnz = 9 * c->pat.nblk;

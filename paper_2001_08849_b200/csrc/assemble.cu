@@ -245,50 +245,49 @@ struct TileLayout {
 
 // ---- builder (once per pattern) ---------------------------------------------------------------
 constexpr int kBldThreads = 256;
-constexpr int kSortCap = 4096;
+constexpr int kHashD = 2048;  // domain hash slots (>= 2 x the tile's list entries cap kDiagCap / 1)
+constexpr int kHashV = 1024;  // vertex hash slots (>= 4 x kMaxVerts)
 
-// In-place ascending bitonic sort of a[0..n2) (n2 a power of two), whole CTA.
-__device__ void cta_bitonic(int32_t* a, int n2) {
-  for (int k = 2; k <= n2; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const int32_t x = a[i], y = a[l];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            a[i] = y;
-            a[l] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
+__device__ __forceinline__ unsigned hslot(int32_t x, unsigned mask) {
+  return (static_cast<unsigned>(x) * 2654435761u >> 7) & mask;
+}
+// Insert x into the open-addressing set keys[0..mask] (empty = -1); duplicates collapse.
+// Returns true if x was new.
+__device__ __forceinline__ bool hinsert(int32_t* keys, unsigned mask, int32_t x) {
+  unsigned h = hslot(x, mask);
+  for (;;) {
+    const int32_t old = atomicCAS(&keys[h], -1, x);
+    if (old == -1) return true;
+    if (old == x) return false;
+    h = (h + 1) & mask;
+  }
+}
+__device__ __forceinline__ int hfind(const int32_t* keys, const int32_t* idx, unsigned mask, int32_t x) {
+  unsigned h = hslot(x, mask);
+  while (keys[h] != x) h = (h + 1) & mask;
+  return idx[h];
 }
 
-// Keep the first of every run of equal values of the sorted a[0..n) (ignoring `skip`) -> out;
-// returns the count.  Deterministic (CTA scan of the keep flags).
-__device__ int cta_unique(const int32_t* a, int n, int32_t skip, int32_t* out, int* sh_tot) {
-  int base = 0;
-  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
-    const int i = c0 + threadIdx.x;
-    const bool keep = i < n && a[i] != skip && (i == 0 || a[i - 1] != a[i]);
-    const unsigned ball = __ballot_sync(0xffffffffu, keep);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __shared__ int wsum[32];
-    if (lane == 0) wsum[w] = __popc(ball);
-    __syncthreads();
-    int off = base;
-    for (int k = 0; k < w; ++k) off += wsum[k];
-    if (keep) out[off + __popc(ball & ((1u << lane) - 1u))] = a[i];
-    int tot = 0;
-    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) tot += wsum[k];
-    __syncthreads();
-    base += tot;
+// Exclusive CTA scan of one int per thread (kBldThreads threads); *total = sum.
+__device__ int cta_excl_scan(int v, int* total) {
+  __shared__ int ws[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
-  if (threadIdx.x == 0) *sh_tot = base;
+  if (lane == 31) ws[w] = inc;
   __syncthreads();
-  return base;
+  int base = 0, tot = 0;
+  for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) {
+    if (k < w) base += ws[k];
+    tot += ws[k];
+  }
+  __syncthreads();
+  *total = tot;
+  return base + inc - v;
 }
 
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t v) {
@@ -301,27 +300,31 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t 
   return lo;
 }
 
-// One CTA per tile.  kFill = false: blob size (or -1 = too big for the caps: split the tile,
-// -2 = a single row that cannot fit: UNSUPPORTED) into size[t]; kFill = true: the blob at off[t].
-template <bool kFill>
+// One CTA per tile, one pass: the blob at blob + t * kBlobCap and its size into size[t] (or
+// -1 = too big for the caps: split the tile, -2 = a single row that cannot fit: UNSUPPORTED).
+// The tile's domains and vertices are collected in shared-memory hash sets: their local numbering
+// is arbitrary (it only names shared-memory slots), while every summation order is fixed by the
+// rows' ascending domain lists F(i).
 __global__ void __launch_bounds__(kBldThreads) k_tile_build(
     const int32_t* __restrict__ order, const int32_t* __restrict__ tstart, int64_t ntiles,
     const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a,
     const int32_t* __restrict__ rec_b, bool tet, const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr,
-    const int32_t* __restrict__ sdiag, int64_t n_lo, int64_t* __restrict__ size, const int64_t* __restrict__ off,
-    unsigned char* __restrict__ blob) {
+    const int32_t* __restrict__ sdiag, int64_t n_lo, int64_t* __restrict__ size, unsigned char* __restrict__ blob) {
   extern __shared__ __align__(16) unsigned char bsm[];
-  int32_t* A = reinterpret_cast<int32_t*>(bsm);          // [kSortCap] sort buffer
-  int32_t* U = A + kSortCap;                              // [kMaxDom] domains (ascending)
-  int32_t* F5 = U + kMaxDom;                              // [kMaxDom * 5] field nodes
-  int32_t* others = F5 + 5 * kMaxDom;                     // [kSortCap] other vertices (sorted)
-  int32_t* bcnt = others + kSortCap;                      // [kMaxBlk + 1] entries per block
-  int32_t* cur = bcnt + kMaxBlk + 1;                      // [kMaxBlk + 1] entry offsets / cursors
-  int32_t* tkey = cur + kMaxBlk + 1;                      // [kMaxTask] task keys (count, index)
-  int32_t* tinfo = tkey + kMaxTask;                       // [kMaxTask] row << 24 | sub-list << 16 | slot
+  int32_t* HK = reinterpret_cast<int32_t*>(bsm);  // [kHashD] domain keys
+  int32_t* HI = HK + kHashD;                       // [kHashD] local domain index
+  int32_t* U = HI + kHashD;                        // [kMaxDom] local -> domain id
+  int32_t* F5 = U + kMaxDom;                       // [kMaxDom * 5] field nodes
+  int32_t* VK = F5 + 5 * kMaxDom;                  // [kHashV] vertex keys
+  int32_t* VI = VK + kHashV;                       // [kHashV] local vertex index
+  int32_t* VL = VI + kHashV;                       // [kMaxVerts + kTileRows] local -> node id
+  int32_t* bcnt = VL + kMaxVerts + kTileRows;      // [kMaxBlk + 1] entries per block
+  int32_t* cur = bcnt + kMaxBlk + 1;               // [kMaxBlk + 1] entry offsets / cursors
+  int32_t* tkey = cur + kMaxBlk + 1;               // [kMaxTask] task keys (count, index)
+  int32_t* tinfo = tkey + kMaxTask;                // [kMaxTask] row << 24 | sub-list << 16 | slot
   __shared__ int32_t rnode[kTileRows], ril[kTileRows], rds[kTileRows], rsd[kTileRows], rbb[kTileRows + 1];
   __shared__ int64_t rP[kTileRows], rF[kTileRows + 1];
-  __shared__ int sh_n, sh_flag;
+  __shared__ int sh_flag, sh_ntask, sh_nent, sh_nv;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int nrows = tstart[t + 1] - tstart[t];
@@ -343,28 +346,42 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       rbb[nrows] = bb;
       rF[nrows] = fsum;
       sh_flag = (fsum > kDiagCap || bb > kMaxBlk) ? 1 : 0;
+      sh_nv = 0;
     }
+    for (int k = threadIdx.x; k < kHashD; k += blockDim.x) HK[k] = -1;
+    for (int k = threadIdx.x; k < kHashV; k += blockDim.x) VK[k] = -1;
     __syncthreads();
     if (sh_flag) {
-      if (!kFill && threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
+      if (threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
       __syncthreads();
       continue;
     }
-    // U = sorted unique union of the rows' domain lists
+    // domains: hash set of the rows' lists, then a local numbering of the occupied slots
     const int nA = static_cast<int>(rF[nrows]);
-    int n2 = 32;
-    while (n2 < nA) n2 <<= 1;
-    for (int r = 0; r < nrows; ++r) {
-      const int64_t b = nf_ptr[ril[r]];
-      const int len = static_cast<int>(rF[r + 1] - rF[r]);
-      for (int k = threadIdx.x; k < len; k += blockDim.x) A[rF[r] + k] = nf_idx[b + k];
+    for (int k = threadIdx.x; k < nA; k += blockDim.x) {
+      int r = 0;
+      while (rF[r + 1] <= k) ++r;
+      hinsert(HK, kHashD - 1, nf_idx[nf_ptr[ril[r]] + (k - rF[r])]);
     }
-    for (int k = nA + threadIdx.x; k < n2; k += blockDim.x) A[k] = 0x7fffffff;
     __syncthreads();
-    cta_bitonic(A, n2);
-    const int ndom = cta_unique(A, nA, 0x7fffffff, U, &sh_n);
+    int ndom = 0;
+    {
+      constexpr int per = kHashD / kBldThreads;
+      int c = 0;
+      for (int q = 0; q < per; ++q) c += HK[threadIdx.x * per + q] >= 0 ? 1 : 0;
+      int base = cta_excl_scan(c, &ndom);
+      for (int q = 0; q < per; ++q) {
+        const int h = threadIdx.x * per + q;
+        if (HK[h] >= 0) {
+          HI[h] = base;
+          if (base < kMaxDom) U[base] = HK[h];
+          ++base;
+        }
+      }
+    }
+    __syncthreads();
     if (ndom > kMaxDom) {
-      if (!kFill && threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
+      if (threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
       __syncthreads();
       continue;
     }
@@ -372,27 +389,52 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       int32_t fld[5];
       field_of(rec_a, rec_b, tet, U[k], fld);
 #pragma unroll
-      for (int p = 0; p < 5; ++p) F5[5 * k + p] = fld[p];
-    }
-    __syncthreads();
-    // other vertices: field nodes that are not tile rows, sorted unique
-    const int nc = 5 * ndom;
-    int m2 = 32;
-    while (m2 < nc) m2 <<= 1;
-    for (int k = threadIdx.x; k < m2; k += blockDim.x) {
-      int32_t v = 0x7fffffff;
-      if (k < nc) {
-        v = F5[k];
-        for (int r = 0; r < nrows; ++r)
-          if (v == rnode[r]) v = 0x7fffffff;
-        if (v < 0) v = 0x7fffffff;
+      for (int p = 0; p < 5; ++p) {
+        F5[5 * k + p] = fld[p];
+        // the set stays at most half full (a tile with more vertices is split anyway)
+        if (fld[p] >= 0 && sh_nv < kHashV / 2 && hinsert(VK, kHashV - 1, fld[p])) atomicAdd(&sh_nv, 1);
       }
-      A[k] = v;
     }
+    for (int r = threadIdx.x; r < nrows; r += blockDim.x)
+      if (hinsert(VK, kHashV - 1, rnode[r])) atomicAdd(&sh_nv, 1);
     __syncthreads();
-    cta_bitonic(A, m2);
-    const int no = cta_unique(A, nc, 0x7fffffff, others, &sh_n);
-    const int nverts = nrows + no;
+    if (sh_nv >= kHashV / 2) {
+      if (threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
+      __syncthreads();
+      continue;
+    }
+    // vertices: tile rows first (local r), the others after them
+    int nverts = 0;
+    {
+      constexpr int per = kHashV / kBldThreads;
+      int c = 0;
+      auto row_of = [&](int32_t v) {
+        for (int r = 0; r < nrows; ++r)
+          if (rnode[r] == v) return r;
+        return -1;
+      };
+      for (int q = 0; q < per; ++q) {
+        const int32_t v = VK[threadIdx.x * per + q];
+        c += (v >= 0 && row_of(v) < 0) ? 1 : 0;
+      }
+      int no = 0;
+      int base = nrows + cta_excl_scan(c, &no);
+      for (int q = 0; q < per; ++q) {
+        const int h = threadIdx.x * per + q;
+        const int32_t v = VK[h];
+        if (v < 0) continue;
+        const int r = row_of(v);
+        if (r >= 0) {
+          VI[h] = r;
+        } else {
+          VI[h] = base;
+          if (base < kMaxVerts + kTileRows) VL[base] = v;
+          ++base;
+        }
+      }
+      for (int r = threadIdx.x; r < nrows; r += blockDim.x) VL[r] = rnode[r];
+      nverts = nrows + no;
+    }
     // entries per stored block: off-diagonal (i, J): one per domain of F(i) holding J (stored J);
     // diagonal: one per domain of F(i).  Warp per row, lane per domain.
     for (int b = threadIdx.x; b <= kMaxBlk; b += blockDim.x) bcnt[b] = 0;
@@ -406,7 +448,7 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       for (int k0 = 0; k0 < len; k0 += 32) {
         const int k = k0 + lane;
         if (k < len) {
-          const int kl = lower_bound_i32(U, ndom, nf_idx[fb + k]);
+          const int kl = hfind(HK, HI, kHashD - 1, nf_idx[fb + k]);
           int pi = 0;
 #pragma unroll
           for (int p = 0; p < 5; ++p) pi = F5[5 * kl + p] == i ? p : pi;
@@ -421,76 +463,77 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // entry offsets and the number of tasks
-      int run = 0, nt = 0;
+    {  // entry offsets and tasks (longest first; ties in block order): CTA scans over the blocks
+      const int nblk = rbb[nrows];
+      constexpr int per = (kMaxBlk + 1) / kBldThreads;  // 3 blocks per thread
+      int ce = 0, ct = 0;
       bool ok = true;
-      for (int r = 0; r < nrows; ++r)
-        for (int sl = 0; sl < rds[r]; ++sl) {
-          const int b = rbb[r] + sl;
-          cur[b] = run;
-          run += bcnt[b];
-          if (sl == rsd[r]) {
-            nt += kDiagSplit;
-            ok = ok && bcnt[b] <= 255 * kDiagSplit;
-          } else {
-            nt += 1;
-            ok = ok && bcnt[b] <= 255;
-          }
+      int rr[per], ss[per];
+      for (int q = 0; q < per; ++q) {
+        const int b = threadIdx.x * per + q;
+        rr[q] = -1;
+        ss[q] = 0;
+        if (b < nblk) {
+          int r = 0;
+          while (rbb[r + 1] <= b) ++r;
+          rr[q] = r;
+          ss[q] = b - rbb[r];
+          ce += bcnt[b];
+          const bool dg = ss[q] == rsd[r];
+          ct += dg ? kDiagSplit : 1;
+          ok = ok && bcnt[b] <= (dg ? 255 * kDiagSplit : 255);
         }
-      sh_n = run;
-      sh_flag = (!ok || nt > kMaxTask || run >= 65536) ? 1 : 0;
-      cur[kMaxBlk] = nt;
+      }
+      int tot_e = 0, tot_t = 0;
+      int e0 = cta_excl_scan(ce, &tot_e);
+      int t0 = cta_excl_scan(ct, &tot_t);
+      ok = __syncthreads_and(ok) && tot_t <= kMaxTask && tot_e < 65536;
+      for (int q = 0; q < per; ++q) {
+        const int b = threadIdx.x * per + q;
+        if (rr[q] < 0) continue;
+        cur[b] = e0;
+        e0 += bcnt[b];
+        if (!ok) continue;
+        if (ss[q] == rsd[rr[q]]) {
+          for (int qq = 0; qq < kDiagSplit; ++qq) {
+            const int c = (bcnt[b] - qq + kDiagSplit - 1) / kDiagSplit;
+            tkey[t0] = ((1023 - c) << 20) | t0;
+            tinfo[t0] = (rr[q] << 24) | (qq << 16) | ss[q];
+            ++t0;
+          }
+        } else {
+          tkey[t0] = ((1023 - bcnt[b]) << 20) | t0;
+          tinfo[t0] = (rr[q] << 24) | (255 << 16) | ss[q];
+          ++t0;
+        }
+      }
+      if (threadIdx.x == 0) {
+        sh_nent = tot_e;
+        sh_ntask = tot_t;
+        sh_flag = ok ? 0 : 1;
+      }
     }
     __syncthreads();
-    const int nent = sh_n, ntask = cur[kMaxBlk];
+    const int nent = sh_nent, ntask = sh_ntask;
     const TileLayout L(nrows, nverts, ndom, ntask, nent);
     const bool ok = !sh_flag && nverts <= kMaxVerts && L.bytes <= kBlobCap;
-    if (!kFill) {
-      if (threadIdx.x == 0) size[t] = ok ? L.bytes : -(nrows > 1 ? 1 : 2);
+    if (threadIdx.x == 0) size[t] = ok ? L.bytes : -(nrows > 1 ? 1 : 2);
+    if (!ok) {
       __syncthreads();
       continue;
     }
-    unsigned char* bl = blob + off[t];
+    unsigned char* bl = blob + t * static_cast<int64_t>(kBlobCap);
     if (threadIdx.x == 0) {
       TileHdr h{nrows, nverts, ndom, ntask, nent, 0, 0, 0};
       *reinterpret_cast<TileHdr*>(bl) = h;
     }
     for (int r = threadIdx.x; r < nrows; r += blockDim.x)
       reinterpret_cast<TileRow*>(bl + L.o_rows)[r] = TileRow{rP[r], ril[r], rsd[r]};
-    for (int v = threadIdx.x; v < nverts; v += blockDim.x)
-      reinterpret_cast<int32_t*>(bl + L.o_verts)[v] = v < nrows ? rnode[v] : others[v - nrows];
-    for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+    for (int v = threadIdx.x; v < nverts; v += blockDim.x) reinterpret_cast<int32_t*>(bl + L.o_verts)[v] = VL[v];
+    for (int k = threadIdx.x; k < 5 * ndom; k += blockDim.x) {
       const int32_t v = F5[k];
-      int lv = 255;
-      if (v >= 0) {
-        lv = -1;
-        for (int r = 0; r < nrows; ++r)
-          if (v == rnode[r]) lv = r;
-        if (lv < 0) lv = nrows + lower_bound_i32(others, no, v);
-      }
-      bl[L.o_fv + k] = static_cast<unsigned char>(lv);
+      bl[L.o_fv + k] = static_cast<unsigned char>(v >= 0 ? hfind(VK, VI, kHashV - 1, v) : 255);
     }
-    // tasks, longest first (ties: block order): key = (255 * kDiagSplit - count) << 20 | index
-    if (threadIdx.x == 0) {
-      int k = 0;
-      for (int r = 0; r < nrows; ++r)
-        for (int sl = 0; sl < rds[r]; ++sl) {
-          const int b = rbb[r] + sl;
-          if (sl == rsd[r]) {
-            for (int q = 0; q < kDiagSplit; ++q) {
-              const int c = (bcnt[b] - q + kDiagSplit - 1) / kDiagSplit;
-              tkey[k] = ((1023 - c) << 20) | k;
-              tinfo[k] = (r << 24) | (q << 16) | sl;
-              ++k;
-            }
-          } else {
-            tkey[k] = ((1023 - bcnt[b]) << 20) | k;
-            tinfo[k] = (r << 24) | (255 << 16) | sl;
-            ++k;
-          }
-        }
-    }
-    __syncthreads();
     {
       TileTask* tasks = reinterpret_cast<TileTask*>(bl + L.o_task);
       for (int a = threadIdx.x; a < ntask; a += blockDim.x) {  // rank sort (keys are distinct)
@@ -515,8 +558,8 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       }
     }
     __syncthreads();
-    // entries: per row, rounds of 32 domains in ascending order; slot by slot, the lanes holding
-    // the slot write in lane (= ascending domain) order
+    // entries: per row, rounds of 32 domains in ascending id; slot by slot, the lanes holding the
+    // slot write in lane (= ascending domain) order
     uint16_t* ent = reinterpret_cast<uint16_t*>(bl + L.o_ent);
     for (int r = w; r < nrows; r += kBldThreads / 32) {
       const int32_t i = rnode[r];
@@ -528,7 +571,7 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
         const int k = k0 + lane;
         int tslot[5] = {-1, -1, -1, -1, -1}, tcode[5] = {0, 0, 0, 0, 0}, kl = 0;
         if (k < len) {
-          kl = lower_bound_i32(U, ndom, nf_idx[fb + k]);
+          kl = hfind(HK, HI, kHashD - 1, nf_idx[fb + k]);
           int pi = 0;
 #pragma unroll
           for (int p = 0; p < 5; ++p) pi = F5[5 * kl + p] == i ? p : pi;
@@ -540,18 +583,36 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
             tcode[q] = 5 * pi + q;
           }
         }
-        for (int sl = 0; sl < ds; ++sl) {
+        // slots touched by this round, lowest first (warp-uniform loop over the union)
+        unsigned long long lo_mask = 0ull;  // slots < 64 as a bit set; others via the slow loop
+        bool big = false;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          if (tslot[q] >= 64) big = true;
+          else if (tslot[q] >= 0) lo_mask |= 1ull << tslot[q];
+        }
+        unsigned long long all = lo_mask;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) all |= __shfl_xor_sync(0xffffffffu, all, o);
+        const bool any_big = __any_sync(0xffffffffu, big);
+        auto emit = [&](int sl) {
           int code = -1;
 #pragma unroll
           for (int q = 0; q < 5; ++q) code = tslot[q] == sl ? tcode[q] : code;
           const unsigned m = __ballot_sync(0xffffffffu, code >= 0);
-          if (m == 0u) continue;
           const int b = rbb[r] + sl;
           if (code >= 0) ent[cur[b] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>((kl << 5) | code);
           __syncwarp();
           if (lane == 0) cur[b] += __popc(m);
           __syncwarp();
+        };
+        while (all) {
+          const int sl = __ffsll(static_cast<long long>(all)) - 1;
+          all &= all - 1ull;
+          emit(sl);
         }
+        if (any_big)
+          for (int sl = 64; sl < ds; ++sl) emit(sl);
       }
     }
     __syncthreads();
@@ -688,7 +749,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 }
 
 template <bool kTet>
-__global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __restrict__ tile_off,
+__global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __restrict__ tile_bytes,
                                                              const unsigned char* __restrict__ gblob, int64_t ntiles,
                                                              const double* __restrict__ xyz, double lam, double mu,
                                                              double* __restrict__ vals) {
@@ -707,8 +768,8 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
   if (producer) {
     auto issue_blob = [&](int j) {  // one thread
       const int64_t t = tile(j);
-      const int64_t o = tile_off[t];
-      tma_blob(blob_of(j), gblob + o, static_cast<uint32_t>(tile_off[t + 1] - o), &bars[j % kBlobSlots]);
+      tma_blob(blob_of(j), gblob + t * static_cast<int64_t>(kBlobCap), static_cast<uint32_t>(tile_bytes[t]),
+               &bars[j % kBlobSlots]);
     };
     auto wait_blob = [&](int j) { mbar_wait_parity(&bars[j % kBlobSlots], (j / kBlobSlots) & 1); };
     auto issue_x = [&](int j) {  // all producers: cp.async of the tile's vertex coordinates
@@ -775,7 +836,9 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
             for (int q = 0; q < 15; ++q) S[15 * k2 + q] = o2[q];
         }
       }
-      __threadfence_block();
+      // every producer is done reading X[b] before the next iteration gathers tile j + 2's
+      // coordinates into it (and before the consumers are released)
+      named_sync(5, kGroup);
       named_arrive(1 + b, kAsmThreads);  // buffer b full
     }
     for (int j = (K > 2 ? K - 2 : 0); j < K; ++j) named_sync(3 + (j & 1), kAsmThreads);  // match the last frees
@@ -902,12 +965,10 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
   const int64_t nloc = pat.nloc;
   h_flags[0] = kNoError;
   pat.ntiles = 0;
-  if (nloc <= 0) {
-    pat.tile_off.ensure(1);
-    FS_CUDA(cudaMemsetAsync(pat.tile_off.get(), 0, sizeof(int64_t), s));
-    return;
-  }
-  DevBuf<int32_t> order, inv;
+  pat.tile_blob_bytes = 0;
+  if (nloc <= 0) return;
+  DevBuf<int32_t>& order = pat.tile_order;
+  DevBuf<int32_t>& inv = pat.tile_tmp;
   order.ensure(nloc);
   inv.ensure(nloc);
   morton_order_device(xyz + 3 * pat.n_lo, nloc, order.get(), inv.get(), scratch, s);
@@ -915,40 +976,39 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
   for (int64_t a = 0; a < nloc; a += kTileRows) ts.push_back(static_cast<int32_t>(a));
   ts.push_back(static_cast<int32_t>(nloc));
   static bool attr = false;
-  const int bsmem =
-      static_cast<int>(sizeof(int32_t) * (2 * kSortCap + kMaxDom + 5 * kMaxDom + 2 * (kMaxBlk + 1) + 2 * kMaxTask));
+  const int bsmem = static_cast<int>(sizeof(int32_t) * (2 * kHashD + kMaxDom + 5 * kMaxDom + 2 * kHashV + kMaxVerts +
+                                                       kTileRows + 2 * (kMaxBlk + 1) + 2 * kMaxTask));
   if (!attr) {
-    FS_CUDA(cudaFuncSetAttribute(k_tile_build<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
-    FS_CUDA(cudaFuncSetAttribute(k_tile_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+    FS_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
     FS_CUDA(cudaFuncSetAttribute(k_asm_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
     FS_CUDA(cudaFuncSetAttribute(k_asm_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
     attr = true;
   }
-  DevBuf<int32_t> d_ts;
-  DevBuf<int64_t> d_size;
+  DevBuf<int32_t>& d_ts = pat.tile_start;
   std::vector<int64_t> sz;
-  for (int pass = 0;; ++pass) {
+  for (;;) {  // build every tile; split the tiles that exceed a cap and rebuild (rare)
     const int64_t nt = static_cast<int64_t>(ts.size()) - 1;
     d_ts.ensure(nt + 1);
-    d_size.ensure(nt);
+    pat.tile_bytes.ensure(nt);
+    pat.tile_blob.ensure(nt * static_cast<int64_t>(kBlobCap));
     FS_CUDA(cudaMemcpyAsync(d_ts.get(), ts.data(), sizeof(int32_t) * (nt + 1), cudaMemcpyHostToDevice, s));
     const int g = static_cast<int>(std::min<int64_t>(nt, 8LL * num_sms()));
-    k_tile_build<false><<<g, kBldThreads, bsmem, s>>>(order.get(), d_ts.get(), nt, pat.nf_ptr.get(), pat.nf_idx.get(),
-                                                     rec_a, rec_b, tet, pat.sptr.get(), pat.snbr.get(), pat.sdiag.get(),
-                                                     pat.n_lo, d_size.get(), nullptr, nullptr);
+    k_tile_build<<<g, kBldThreads, bsmem, s>>>(order.get(), d_ts.get(), nt, pat.nf_ptr.get(), pat.nf_idx.get(), rec_a,
+                                               rec_b, tet, pat.sptr.get(), pat.snbr.get(), pat.sdiag.get(), pat.n_lo,
+                                               pat.tile_bytes.get(), pat.tile_blob.get());
     FS_LAUNCH_CHECK();
     sz.resize(nt);
-    FS_CUDA(cudaMemcpyAsync(sz.data(), d_size.get(), sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaMemcpyAsync(sz.data(), pat.tile_bytes.get(), sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
     std::vector<int32_t> nts;
     bool split = false;
     for (int64_t k = 0; k < nt; ++k) {
       nts.push_back(ts[k]);
       if (sz[k] == -2) {  // one row whose domains exceed the tile caps
-        std::vector<int32_t> hord(1);
-        FS_CUDA(cudaMemcpy(hord.data(), order.get() + ts[k], sizeof(int32_t), cudaMemcpyDeviceToHost));
+        int32_t hord = 0;
+        FS_CUDA(cudaMemcpy(&hord, order.get() + ts[k], sizeof(int32_t), cudaMemcpyDeviceToHost));
         h_flags[0] = (static_cast<unsigned long long>(FSFEM_ERR_UNSUPPORTED) << 56) |
-                     static_cast<unsigned long long>(pat.n_lo + hord[0]);
+                     static_cast<unsigned long long>(pat.n_lo + hord);
         return;
       }
       if (sz[k] == -1) {
@@ -961,23 +1021,14 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
     ts.swap(nts);
   }
   const int64_t nt = static_cast<int64_t>(ts.size()) - 1;
-  std::vector<int64_t> off(nt + 1, 0);
-  int64_t mx = 0;
+  int64_t tot = 0, mx = 0;
   for (int64_t k = 0; k < nt; ++k) {
-    off[k + 1] = off[k] + sz[k];
+    tot += sz[k];
     mx = std::max(mx, sz[k]);
   }
   pat.ntiles = nt;
   pat.tile_blob_max = mx;
-  pat.tile_off.ensure(nt + 1);
-  pat.tile_blob.ensure(std::max<int64_t>(off[nt], 16));
-  FS_CUDA(cudaMemcpyAsync(pat.tile_off.get(), off.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, s));
-  const int g = static_cast<int>(std::min<int64_t>(nt, 8LL * num_sms()));
-  k_tile_build<true><<<g, kBldThreads, bsmem, s>>>(order.get(), d_ts.get(), nt, pat.nf_ptr.get(), pat.nf_idx.get(),
-                                                  rec_a, rec_b, tet, pat.sptr.get(), pat.snbr.get(), pat.sdiag.get(),
-                                                  pat.n_lo, nullptr, pat.tile_off.get(), pat.tile_blob.get());
-  FS_LAUNCH_CHECK();
-  FS_CUDA(cudaStreamSynchronize(s));  // the host vectors above must outlive the copies
+  pat.tile_blob_bytes = tot;
 }
 
 // Numeric assembly of the own rows into the stored blocks (S2-S4 + S6).
@@ -993,7 +1044,7 @@ void assemble_tiles_device(const Pattern& pat, const double* xyz, double lam, do
   }
   const int g = static_cast<int>(std::min<int64_t>(pat.ntiles, static_cast<int64_t>(per_sm) * num_sms()));
   auto k = tet ? k_asm_tile<true> : k_asm_tile<false>;
-  k<<<g, kAsmThreads, kAsmSmem, s>>>(pat.tile_off.get(), pat.tile_blob.get(), pat.ntiles, xyz, lam, mu, vals);
+  k<<<g, kAsmThreads, kAsmSmem, s>>>(pat.tile_bytes.get(), pat.tile_blob.get(), pat.ntiles, xyz, lam, mu, vals);
   FS_LAUNCH_CHECK();
 }
 

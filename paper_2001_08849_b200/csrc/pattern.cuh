@@ -40,6 +40,7 @@ struct Pattern {
   DevBuf<int64_t> sptr;      // [nloc+1] stored block offsets
   DevBuf<int32_t> snbr;      // [nsb] column node of each stored block (ascending per row)
   DevBuf<int32_t> sdiag;     // [nloc] slot of the diagonal block inside the stored row
+  DevBuf<int32_t> diag_full; // [nloc] slot of the diagonal inside the full neighbour list
   DevBuf<int64_t> tptr;      // [nloc+1] transposed block offsets
   DevBuf<int2> tlist;        // [ntb] (stored block index of K_ji, node j), ascending j
   int64_t nchunks = 0;
@@ -67,10 +68,12 @@ struct Pattern {
   DevBuf<int32_t> nf_idx;    // [nfi] faces whose field holds node i, ascending
   // Assembly tiles (assemble.cu, built once per pattern): the own nodes in Morton order cut into
   // tiles of <= kTileRows rows; per tile one contiguous blob (TileHdr + rows, vertices, field
-  // positions, per-block entry counts, program entries), tile t at blob + tile_off[t].
+  // positions, tasks, program entries), tile t at tile_blob + t * kBlobCap, tile_bytes[t] long.
   int64_t ntiles = 0;
-  int64_t tile_blob_max = 0;  // largest tile blob (bytes)
-  DevBuf<int64_t> tile_off;   // [ntiles + 1] byte offsets (16-B aligned)
+  int64_t tile_blob_max = 0;    // largest tile blob (bytes)
+  int64_t tile_blob_bytes = 0;  // sum of the blob sizes (read once per numeric assembly)
+  DevBuf<int64_t> tile_bytes;   // [ntiles]
+  DevBuf<int32_t> tile_order, tile_tmp, tile_start;  // builder scratch (kept: no cudaFree per mesh)
   DevBuf<unsigned char> tile_blob;
 };
 

@@ -344,7 +344,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   DevBuf<int32_t>& nbr = pat.nbr;
   DevBuf<int64_t>& nf_ptr = pat.nf_ptr;
   DevBuf<int32_t>& nf_idx = pat.nf_idx;
-  DevBuf<int32_t> diag_slot;
+  DevBuf<int32_t>& diag_slot = pat.diag_full;
   pat.n_lo = n_lo;
   pat.nloc = nloc;
   const int sms = num_sms();

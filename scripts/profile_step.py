@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--reassemble", type=int, default=2)
     ap.add_argument("--reorder", type=int, default=0, help="0 auto, 1 always, 2 never")
     ap.add_argument("--pcg-variant", type=int, default=0, help="0 standard, 1 single reduction")
+    ap.add_argument("--rebuild", type=int, default=0, help="extra faces + symbolic passes (steady-state timing)")
     a = ap.parse_args()
     import torch
     from fsfem_inputs import config_mesh
@@ -33,6 +34,11 @@ def main():
     dirichlet = torch.from_numpy(m.dirichlet).to(dev)
     loads = torch.from_numpy(m.loads.reshape(-1).copy()).to(dev)
     u = torch.zeros(3 * m.n_nodes, dtype=torch.float64, device=dev)
+    for _ in range(a.rebuild):
+        fsfem_build_faces(g.ctx, xyz, tets)
+        fsfem_assemble_csr(g.ctx, 1.0e6, 0.3)
+        r = g.report()
+        print(f"rebuild: faces {r['t_faces_ms']:.3f} ms, symbolic {r['t_symbolic_ms']:.3f} ms")
     fsfem_build_faces(g.ctx, xyz, tets)
     t_num = []
     for _ in range(1 + a.reassemble):

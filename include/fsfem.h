@@ -67,9 +67,9 @@ typedef struct {
   double t_numeric_ms;       /* ... of the last numeric assembly (S2-S4, S6)                 */
   double t_bc_ms;            /* ... of the last apply_bc (S7)                                */
   double t_pcg_ms;           /* ... of the last pcg_solve loop (S8-S9)                       */
-  double t_spmv_ms;          /* summed device time of the sampled SpMV launches of that loop
-                                (the first SpMV of every CUDA-graph batch of iterations)      */
-  int64_t spmv_launches;     /* number of SpMV launches sampled in t_spmv_ms                 */
+  double t_spmv_ms;          /* summed duration of the PCG SpMV launches of that solve, timed on
+                                the device (%globaltimer: first CTA start to last CTA end)     */
+  int64_t spmv_launches;     /* number of SpMV launches in t_spmv_ms                          */
   int64_t kernel_launches;   /* kernels launched by libfsfem in this process so far (monotonic;
                                 graph replays count their kernels, early-exit ones included) */
   /* Storage and algorithmic traffic of the assembled operator.  K is stored as
@@ -178,6 +178,14 @@ fsfem_status fsfem_set_reorder(fsfem_ctx* ctx, int mode);
  * counts may differ by a few percent.  Takes effect at the next pcg_solve.  Errors: INVALID_ARG. */
 enum { FSFEM_PCG_STANDARD = 0, FSFEM_PCG_SINGLE_REDUCTION = 1, FSFEM_PCG_AUTO = 2 };
 fsfem_status fsfem_set_pcg_variant(fsfem_ctx* ctx, int variant);
+
+/* PCG loop control.  FSFEM_LOOP_DEVICE (default): the whole solve is ONE CUDA-graph launch whose
+ * while node repeats a body of 8 iterations until the device-side recurrence stops -- no host
+ * synchronisation inside the solve.  FSFEM_LOOP_HOST: graph batches of 32 iterations, the host
+ * polls the state between batches (also used with NCCL ranks, whose collectives are not
+ * conditional-body nodes).  Results are identical.  Errors: INVALID_ARG. */
+enum { FSFEM_LOOP_DEVICE = 0, FSFEM_LOOP_HOST = 1 };
+fsfem_status fsfem_set_loop(fsfem_ctx* ctx, int mode);
 
 /* S1: extract the unique faces of the mesh.
  *   xyz  [3*n_nodes] double, node coordinates (x, y, z per node)            (Node matrix)

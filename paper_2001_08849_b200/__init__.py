@@ -18,6 +18,7 @@ from .fsfem import (  # noqa: F401
     fsfem_comm_init_loopback,
     fsfem_get_partition,
     fsfem_set_deterministic,
+    fsfem_set_loop,
     fsfem_create,
     fsfem_destroy,
     fsfem_get_csr,

@@ -203,12 +203,20 @@ struct fsfem_ctx {
   cudaGraphExec_t graph = nullptr;
   std::vector<uintptr_t> graph_key;
   long long graph_launches = 0;  // kernels per replay of the graph (counted at capture)
+  // device-side loop (default): one graph whose while node repeats a body of kDevBatch iterations
+  // until the recurrence stops -- no host synchronisation inside the solve
+  int loop_mode = FSFEM_LOOP_DEVICE;
+  cudaGraphExec_t dgraph = nullptr;
+  std::vector<uintptr_t> dgraph_key;
+  long long dgraph_body_launches = 0;
+  bool dgraph_failed = false;  // instantiation refused (e.g. collectives inside the body): host batches
   int max_restarts = 2;  // residual-replacement restarts when the true residual misses (fsfem_pcg_solve)
 };
 
 namespace {
 
-constexpr int kBatch = 32;  // PCG iterations per CUDA graph launch
+constexpr int kBatch = 32;     // PCG iterations per CUDA graph launch (host-polled loop)
+constexpr int kDevBatch = 8;   // PCG iterations per body of the device-side while loop
 
 bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -316,6 +324,9 @@ void drop_graph(fsfem_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   c->graph = nullptr;
   c->graph_key.clear();
+  if (c->dgraph) cudaGraphExecDestroy(c->dgraph);
+  c->dgraph = nullptr;
+  c->dgraph_key.clear();
 }
 
 // ---- collectives over the ranks of one solve ---------------------------------------------------
@@ -742,6 +753,15 @@ fsfem_status fsfem_comm_init_loopback(fsfem_ctx** ctxs, int nranks) {
   return FSFEM_OK;
 }
 
+fsfem_status fsfem_set_loop(fsfem_ctx* c, int mode) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (mode != FSFEM_LOOP_DEVICE && mode != FSFEM_LOOP_HOST)
+      return fail(c, FSFEM_ERR_INVALID_ARG, "loop mode must be 0 (device) or 1 (host batches)");
+    c->loop_mode = mode;
+    return FSFEM_OK;
+  });
+}
+
 fsfem_status fsfem_set_deterministic(fsfem_ctx* c, int on) {
   return guarded(c, [&]() -> fsfem_status {
     if (c->stage != kCreated) return fail(c, FSFEM_ERR_STATE, "set_deterministic must precede build_faces");
@@ -1098,6 +1118,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
         r->h_st->cg_first = cg1 ? 1 : 0;
         r->h_st->upd_part = r->part.get() + 4 * pcg_grid();
         r->h_st->upd_n = cg_update_grid(3 * r->nloc);
+        r->h_st->spmv_t0 = ~0ull;
         FS_CUDA(cudaMemcpyAsync(r->st.get(), r->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, r->stream));
       }
     };
@@ -1147,18 +1168,58 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     start(u0_is_zero != 0);
     read_state();
 
-    // graph of kBatch iterations with event pairs around the first SpMV
+    // The loop: device-side while node (default) or host-polled batches of kBatch iterations.
     const std::vector<uintptr_t> key = graph_key_of(cs);
-    if (!c->graph || key != c->graph_key) {
-      drop_graph(c);
+    bool device_loop = c->loop_mode == FSFEM_LOOP_DEVICE && !c->dgraph_failed && !(c0->nranks > 1 && !c0->loop);
+    if (device_loop && (!c->dgraph || key != c->dgraph_key)) {
+      if (c->dgraph) cudaGraphExecDestroy(c->dgraph);
+      c->dgraph = nullptr;
+      cudaGraph_t g;
+      FS_CUDA(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle handle;
+      FS_CUDA(cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = handle;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      FS_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      FS_CUDA(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      set_capturing(true);
+      try {
+        for (int it = 0; it < kDevBatch; ++it) pcg_iteration(cs, nullptr, nullptr);
+        launch_loop_cond(handle, c0->st.get(), c->stream);
+      } catch (...) {
+        set_capturing(false);
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(c->stream, &dummy);
+        cudaGraphDestroy(g);
+        throw;
+      }
+      set_capturing(false);
+      cudaGraph_t captured;
+      FS_CUDA(cudaStreamEndCapture(c->stream, &captured));
+      c->dgraph_body_launches = captured_launches();
+      if (cudaGraphInstantiate(&c->dgraph, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        c->dgraph = nullptr;
+        c->dgraph_failed = true;  // fall back to host-polled batches from now on
+        device_loop = false;
+      } else {
+        c->dgraph_key = key;
+      }
+      cudaGraphDestroy(g);
+    }
+    if (!device_loop && (!c->graph || key != c->graph_key)) {
+      if (c->graph) cudaGraphExecDestroy(c->graph);
+      c->graph = nullptr;
       cudaGraph_t g;
       FS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       set_capturing(true);
       try {
-        // One SpMV per batch is bracketed by events (a live per-launch sample for the roofline);
-        // an event pair around every SpMV would cost ~14 us per iteration at cfg4.
-        for (int it = 0; it < kBatch; ++it)
-          pcg_iteration(cs, it == 0 ? c->spmv_ev[0] : nullptr, it == 0 ? c->spmv_ev[1] : nullptr);
+        for (int it = 0; it < kBatch; ++it) pcg_iteration(cs, nullptr, nullptr);
       } catch (...) {
         set_capturing(false);
         cudaStreamEndCapture(c->stream, &g);
@@ -1171,24 +1232,25 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       c->graph_key = key;
       c->graph_launches = captured_launches();
     }
-    const long long launches_per_batch = c->graph_launches;
-    double spmv_ms = 0.0;
-    int64_t spmv_n = 0, total_iters = 0;
+    int64_t total_iters = 0;
     int restarts = 0;
     double true_rel = 0.0, floor_rel = 0.0;
     for (;;) {
-      while (c0->h_st->done_d == 0.0) {
-        const long long before = c0->h_st->iters;
-        FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
-        count_launch(launches_per_batch);
+      if (device_loop) {
+        FS_CUDA(cudaGraphLaunch(c->dgraph, c->stream));
         read_state();
-        const long long ran = std::min<long long>(kBatch, c0->h_st->iters - before);
-        if (ran > 0) {  // the sampled SpMV ran (iteration 0 of the batch)
-          spmv_ms += elapsed(c->spmv_ev[0], c->spmv_ev[1]);
-          ++spmv_n;
+        const long long bodies = std::max<long long>(1, (c0->h_st->iters + kDevBatch - 1) / kDevBatch);
+        count_launch(bodies * c->dgraph_body_launches);
+      } else {
+        while (c0->h_st->done_d == 0.0) {
+          const long long before = c0->h_st->iters;
+          FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
+          count_launch(c->graph_launches);
+          read_state();
+          if (c0->h_st->iters == before && c0->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg made no progress");
         }
-        if (c0->h_st->iters == before && c0->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg made no progress");
       }
+      if (c0->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg loop ended before the recurrence stopped");
       total_iters += c0->h_st->iters;
       // true residual ||f - K x|| / ||f|| and its rounding floor eps ||K||_F ||x|| / ||f||
       coll_allgatherv(cs, &fsfem_ctx::x_full);  // every rank holds the whole iterate
@@ -1219,9 +1281,15 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
         }
         break;
       }
-      // residual replacement: restart the recurrence from the current iterate
+      // residual replacement: restart the recurrence from the current iterate (timers carry over)
       ++restarts;
+      const unsigned long long tns = c0->h_st->spmv_ns, tcnt = c0->h_st->spmv_cnt;
       set_state(max_iter - total_iters);
+      for (fsfem_ctx* r : cs) {
+        r->h_st->spmv_ns = tns;
+        r->h_st->spmv_cnt = tcnt;
+        FS_CUDA(cudaMemcpyAsync(r->st.get(), r->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, r->stream));
+      }
       for (fsfem_ctx* r : cs) FS_CUDA(cudaMemsetAsync(r->p_full.get(), 0, sizeof(double) * nglob, r->stream));
       start(false);
       read_state();
@@ -1239,8 +1307,8 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       r->rep.residual_floor = floor_rel;
       r->rep.restarts = restarts;
       r->rep.t_pcg_ms = elapsed(c->ev0, c->ev1);
-      r->rep.t_spmv_ms = spmv_ms;
-      r->rep.spmv_launches = spmv_n;
+      r->rep.t_spmv_ms = static_cast<double>(h.spmv_ns) * 1e-6;  // device timer, every PCG SpMV of the solve
+      r->rep.spmv_launches = static_cast<int64_t>(h.spmv_cnt);
       r->rep.kernel_launches = launch_count();
     }
     if (rep) *rep = c->rep;

@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   if (kPcg) {
     double unused;
     if (cta_scalars(st, nullptr, unused)) return;
+    spmv_time_start(st);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // chunk walk: grid-strided (contiguous ranges per CTA were slower)
@@ -436,7 +437,10 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   if (!kPcg) return;
   const double mine[1] = {dot};
   double out[1];
-  if (grid_reduce<1>(mine, part, &st->ticket[0], out)) spmv_finish(st, out[0]);
+  if (grid_reduce<1>(mine, part, &st->ticket[0], out)) {
+    spmv_finish(st, out[0]);
+    if (threadIdx.x == 0) spmv_time_end(st);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -582,6 +586,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   }
   __syncthreads();
   if (sh_done) return;  // uniform over the grid
+  if (kPcg) spmv_time_start(st);
   const uint32_t epoch = sh_epoch;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* xown = x + own_off;
@@ -871,6 +876,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
     }
     const double pq = block_sum(a, sh);
     spmv_finish(st, pq);
+    if (threadIdx.x == 0) spmv_time_end(st);
   }
   if (threadIdx.x == 0) {
     sync[1] = 0u;
@@ -894,6 +900,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_small(const int64_t* __restri
   if (kPcg) {
     double unused;
     if (cta_scalars(st, nullptr, unused)) return;
+    spmv_time_start(st);
   }
   const int lane = threadIdx.x & 31;
   double dot = 0.0;
@@ -944,7 +951,10 @@ __global__ void __launch_bounds__(kThreads) k_spmv_small(const int64_t* __restri
   if (!kPcg) return;
   const double mine[1] = {dot};
   double out[1];
-  if (grid_reduce<1>(mine, part, &st->ticket[0], out)) spmv_finish(st, out[0]);
+  if (grid_reduce<1>(mine, part, &st->ticket[0], out)) {
+    spmv_finish(st, out[0]);
+    if (threadIdx.x == 0) spmv_time_end(st);
+  }
 }
 
 // Vector kernels: each thread takes kVec elements per pass at stride gridDim*blockDim (coalesced)
@@ -1418,6 +1428,17 @@ int cg_update_grid(int64_t n) { return vec_grid(n); }
 void launch_cg_update(double* x, double* r, double* u, double* p, double* sv, const double* w, const double* dinv,
                       int64_t n, PcgState* st, double* upd_part, cudaStream_t s) {
   k_cg_update<<<cg_update_grid(n), kThreads, 0, s>>>(x, r, u, p, sv, w, dinv, n, st, upd_part);
+  FS_LAUNCH_CHECK();
+}
+
+// Device-side PCG loop (api.cu): the body of the graph's while node ends with this kernel, which
+// keeps the loop running while the recurrence has not stopped.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const PcgState* st) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, __ldcg(&st->done_d) == 0.0 ? 1u : 0u);
+}
+
+void launch_loop_cond(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s) {
+  k_loop_cond<<<1, 32, 0, s>>>(h, st);
   FS_LAUNCH_CHECK();
 }
 

@@ -29,7 +29,30 @@ struct PcgState {
   const double* upd_part;  // [2 * upd_n]: gamma partials, then r.r partials
   int upd_n;
   int pad_;
+  // device timing of the PCG SpMV launches (%globaltimer, ns): earliest CTA start of the launch
+  // in flight, summed durations (first CTA start -> last CTA end) and their number
+  unsigned long long spmv_t0;
+  unsigned long long spmv_ns;
+  unsigned long long spmv_cnt;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// SpMV launch timing: every CTA marks its start; the launch's last CTA closes the interval.
+__device__ __forceinline__ void spmv_time_start(PcgState* st) {
+  if (st && threadIdx.x == 0) atomicMin(&st->spmv_t0, global_ns());
+}
+__device__ __forceinline__ void spmv_time_end(PcgState* st) {  // one thread of the last CTA
+  const unsigned long long t1 = global_ns();
+  const unsigned long long t0 = atomicExch(&st->spmv_t0, ~0ull);
+  if (t0 != ~0ull && t1 > t0) {
+    st->spmv_ns += t1 - t0;
+    st->spmv_cnt += 1;
+  }
+}
 
 __device__ __forceinline__ void pcg_stop(PcgState* st, int status) {
   st->status = status;
@@ -138,6 +161,9 @@ void launch_sumsq(const double* vals, int64_t n, PcgState* st, double* part, cud
 void partition_ranges_device(const int32_t* face_nodes, const int32_t* face_opp, int64_t nf, int64_t nn, int nranks,
                              int64_t align, DevBuf<unsigned char>& scratch, cudaStream_t s,
                              std::vector<int64_t>& ranges);
+
+// Device-side loop: sets the while-node condition to "not done" (pcg.cu).
+void launch_loop_cond(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s);
 
 int pcg_grid();
 int spmv_kind(const Pattern& pat);  // 0 small, 1 gather, 2 dataflow (pcg.cu)

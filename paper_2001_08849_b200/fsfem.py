@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
 METHOD_FS, METHOD_FEM_T4 = 0, 1
 
 EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init",
-           "fsfem_comm_init_loopback", "fsfem_get_partition", "fsfem_set_deterministic", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
+           "fsfem_comm_init_loopback", "fsfem_get_partition", "fsfem_set_deterministic", "fsfem_set_loop", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
            "fsfem_surface_loads"]
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_comm_init_loopback": (I, [P, I]),
         "fsfem_get_partition": (I, [P, P]),
         "fsfem_set_deterministic": (I, [P, I]),
+        "fsfem_set_loop": (I, [P, I]),
         "fsfem_set_method": (I, [P, I]),
         "fsfem_set_reorder": (I, [P, I]),
         "fsfem_set_pcg_variant": (I, [P, I]),
@@ -177,6 +178,11 @@ def fsfem_get_partition(ctx, nranks: int) -> np.ndarray:
     out = np.zeros(nranks + 1, np.int64)
     _raise(ctx, load_library().fsfem_get_partition(ctx, out.ctypes.data_as(ctypes.c_void_p)))
     return out
+
+
+def fsfem_set_loop(ctx, mode: int) -> None:
+    """0: device-side while loop (default), 1: host-polled graph batches."""
+    _raise(ctx, load_library().fsfem_set_loop(ctx, int(mode)))
 
 
 def fsfem_set_deterministic(ctx, on: bool) -> None:
@@ -317,6 +323,9 @@ class FsFem:
 
     def set_deterministic(self, on: bool = True):
         fsfem_set_deterministic(self.ctx, on)
+
+    def set_loop(self, mode: int):
+        fsfem_set_loop(self.ctx, mode)
 
     def set_reorder(self, mode: int):
         fsfem_set_reorder(self.ctx, mode)

@@ -205,7 +205,7 @@ struct fsfem_ctx {
   long long graph_launches = 0;  // kernels per replay of the graph (counted at capture)
   // device-side loop (default): one graph whose while node repeats a body of kDevBatch iterations
   // until the recurrence stops -- no host synchronisation inside the solve
-  int loop_mode = FSFEM_LOOP_DEVICE;
+  int loop_mode = FSFEM_LOOP_HOST;  // device loop: same speed measured, not ncu-visible
   cudaGraphExec_t dgraph = nullptr;
   std::vector<uintptr_t> dgraph_key;
   long long dgraph_body_launches = 0;

@@ -23,7 +23,10 @@ namespace fsfem {
 #endif
 constexpr int kChunkNodes = FSFEM_CHUNK_NODES;
 constexpr int kCapBlocks = FSFEM_CAP_BLOCKS;
-constexpr int kMaxDeps = 48;
+#ifndef FSFEM_MAX_DEPS
+#define FSFEM_MAX_DEPS 48
+#endif
+constexpr int kMaxDeps = FSFEM_MAX_DEPS;
 struct SpmvChunk {
   int32_t n0, n1, Ps0, Ps1, Pt0, Pt1, pad0, pad1;
 };

@@ -22,6 +22,19 @@ constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+// Programmatic dependent launch (PDL, FSFEM_PDL): a kernel launched with the programmatic
+// serialization attribute may start before its predecessor finished; it waits here before it
+// touches anything the predecessor wrote, and the predecessor lets it launch early.
+#ifndef FSFEM_PDL
+#define FSFEM_PDL 0
+#endif
+__device__ __forceinline__ void pdl_wait() {
+  if (FSFEM_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  if (FSFEM_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // One thread per CTA reads the device-resident PCG scalars (every thread reading the same
 // address through L2 would serialise on one L2 slice); the CTA gets them from shared memory.
 __device__ __forceinline__ bool cta_scalars(const PcgState* st, const double* field, double& value) {
@@ -550,7 +563,14 @@ static_assert(P2Layout::kY % 16 == 0 && P2Layout::kT % 16 == 0 && P2Layout::kByt
 struct P2Info {
   int n0, nn, Pt0, Pt1, dptr, dy, dt, pad;
 };
-constexpr int kDfSmem = 128 + 192 + 2 * PushLayout::kBytes + 2 * P2Layout::kBytes;
+#ifndef FSFEM_DF_STAGES
+#define FSFEM_DF_STAGES 2
+#endif
+constexpr int kDfStages = FSFEM_DF_STAGES;  // phase-1 TMA ring depth
+static_assert(kDfStages >= 2 && kDfStages <= 7, "mbarrier header holds 2 * stages + 2 barriers");
+constexpr int kDfHdr = 128 + 32 * kDfStages + 64;  // barriers, stage infos, phase-2 infos
+constexpr int kDfPst = (kDfHdr + 127) / 128 * 128;
+constexpr int kDfSmem = 128 + kDfPst + kDfStages * PushLayout::kBytes + 2 * P2Layout::kBytes;
 
 template <bool kPcg>
 __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
@@ -563,26 +583,30 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   static_assert(kChunkNodes <= 32, "phase 2: one lane per node");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [2] P1 stage loaded
-  uint64_t* empty = full + 2;                                 // [2] P1 stage consumed (8 warps)
-  uint64_t* p2full = full + 4;                                // [2] phase-2 buffer loaded
-  PushInfo* pinfo = reinterpret_cast<PushInfo*>(smem + 64);   // [2]
-  P2Info* qinfo = reinterpret_cast<P2Info*>(smem + 128);      // [2]
-  unsigned char* pst = smem + 192;                            // 2 P1 stages
-  unsigned char* qst = pst + 2 * PushLayout::kBytes;          // 2 phase-2 buffers
+  pdl_trigger();
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);                     // [kDfStages] P1 stage loaded
+  uint64_t* empty = full + kDfStages;                                      // [kDfStages] P1 stage consumed
+  uint64_t* p2full = full + 2 * kDfStages;                                 // [2] phase-2 buffer loaded
+  PushInfo* pinfo = reinterpret_cast<PushInfo*>(smem + 128);               // [kDfStages]
+  P2Info* qinfo = reinterpret_cast<P2Info*>(smem + 128 + 32 * kDfStages);  // [2]
+  unsigned char* pst = smem + kDfPst;                                      // kDfStages P1 stages
+  unsigned char* qst = pst + kDfStages * PushLayout::kBytes;               // 2 phase-2 buffers
   __shared__ uint32_t sh_epoch;
   __shared__ int sh_done;
   __shared__ int sh_p1done;  // chunks whose phase 1 the loader has seen complete
   if (threadIdx.x == 0) {
+    for (int k = 0; k < kDfStages; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kWarps);
+    }
+    for (int k = 0; k < 2; ++k) mbar_init(&p2full[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_wait();  // everything below may read what the previous kernel wrote
+  if (threadIdx.x == 0) {
     sh_p1done = 0;
     sh_epoch = __ldcg(sync) + 1u;
     sh_done = kPcg ? (ld_cg(&st->done_d) != 0.0) : 0;
-    for (int k = 0; k < 2; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kWarps);
-      mbar_init(&p2full[k], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (sh_done) return;  // uniform over the grid
@@ -601,22 +625,22 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
 #define DF_T(acc) if (FSFEM_DF_TIMING) { const long long tq1 = clock64(); acc += tq1 - tq0; tq0 = tq1; }
   if (warp == kWarps) {
     // ---------------- loader warp: P1 stages (TMA ring) ----------------
-    SpmvChunk nx = K > 2 ? chunks[blockIdx.x + 2 * gridDim.x] : SpmvChunk{};
-    for (int j = 0; j < 2 && j < K; ++j)
+    SpmvChunk nx = K > kDfStages ? chunks[blockIdx.x + kDfStages * gridDim.x] : SpmvChunk{};
+    for (int j = 0; j < kDfStages && j < K; ++j)
       if (lane == 0)
         issue_chunk_push(chunks[blockIdx.x + j * gridDim.x], sptr, snbr, tpos, vals, xown, pst + j * PushLayout::kBytes,
                          &full[j], &pinfo[j]);
     for (int j = 0; j < K; ++j) {
       const int c = blockIdx.x + j * gridDim.x;
+      const int sj = j % kDfStages;
       DF_T(tC)
-      mbar_wait(&empty[j & 1], (j >> 1) & 1);  // P1(c) done by every compute warp
+      mbar_wait(&empty[sj], (j / kDfStages) & 1);  // P1(c) done by every compute warp
       DF_T(tA)
-      if (lane == 0 && j + 2 < K) {
+      if (lane == 0 && j + kDfStages < K) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_chunk_push(nx, sptr, snbr, tpos, vals, xown, pst + (j & 1) * PushLayout::kBytes, &full[j & 1],
-                         &pinfo[j & 1]);
+        issue_chunk_push(nx, sptr, snbr, tpos, vals, xown, pst + sj * PushLayout::kBytes, &full[sj], &pinfo[sj]);
       }
-      if (j + 3 < K) nx = chunks[c + 3 * gridDim.x];
+      if (j + kDfStages + 1 < K) nx = chunks[c + (kDfStages + 1) * gridDim.x];
       if (lane == 0) st_release_cta_s32(&sh_p1done, j + 1);  // -> counter warp
     }
   } else if (warp == kWarps + 2) {
@@ -780,9 +804,9 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
     const int grp = lane / G, gl = lane % G;
     const int m = warp * NPW + grp;  // this group's node inside every chunk
     for (int j = 0; j < K; ++j) {
-      const int s = j & 1;
+      const int s = j % kDfStages;
       DF_T(tC)
-      mbar_wait(&full[s], (j >> 1) & 1);
+      mbar_wait(&full[s], (j / kDfStages) & 1);
       DF_T(tA)
       const unsigned char* stg = pst + s * PushLayout::kBytes;
       const PushInfo in = pinfo[s];
@@ -1122,6 +1146,8 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
                                                                PcgState* st, double* part) {
   __shared__ double sh[kWarps];
   __shared__ double sh_sc[4];
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) {
     sh_sc[0] = ld_cg(&st->done_d);
     sh_sc[1] = ld_cg(&st->alpha);
@@ -1337,11 +1363,13 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     cfg.blockDim = dim3(kDfThreads);
     cfg.dynamicSmemBytes = kDfSmem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;  // phase-2 waits need every CTA resident
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = FSFEM_PDL ? 2 : 1;
     const SpmvChunk* chp = pat.chunks.get();
     const int64_t* spp = pat.sptr.get();
     const int64_t* tpp = pat.tptr.get();
@@ -1385,8 +1413,29 @@ void launch_direction(double* p, const double* r, const double* dinv, int64_t n,
   FS_LAUNCH_CHECK();
 }
 
+// Every PCG kernel asks for the same L1/shared-memory split as the SpMV, so that the SMs do not
+// reconfigure the carve-out between the kernels of an iteration (FSFEM_CARVEOUT, percent).
+#ifndef FSFEM_CARVEOUT
+#define FSFEM_CARVEOUT -1
+#endif
+void set_pcg_carveouts() {
+  static bool done = false;
+  if (done || FSFEM_CARVEOUT < 0) return;
+  done = true;
+  const int c = FSFEM_CARVEOUT;
+  FS_CUDA(cudaFuncSetAttribute(k_update_direction, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_spmv_df<true>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_spmv_df<false>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_direction, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_cg_update, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_spmv<true>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+  FS_CUDA(cudaFuncSetAttribute(k_spmv_small<true>, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+}
+
 int update_direction_grid() {
   static int g = 0;
+  set_pcg_carveouts();
   if (g == 0) {
     int per_sm = 0;
     FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_direction, kThreads, 0));
@@ -1402,11 +1451,13 @@ void launch_update_direction(double* x, double* r, double* p, const double* q, c
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = FSFEM_PDL ? 2 : 1;
   FS_CUDA(cudaLaunchKernelEx(&cfg, k_update_direction, x, r, p, q, dinv, n, st, part));
   count_launch();
 }

@@ -19,7 +19,7 @@ def main():
     ap.add_argument("--reassemble", type=int, default=2)
     ap.add_argument("--reorder", type=int, default=0, help="0 auto, 1 always, 2 never")
     ap.add_argument("--pcg-variant", type=int, default=0, help="0 standard, 1 single reduction")
-    ap.add_argument("--loop", type=int, default=0, help="0 device while loop, 1 host-polled batches")
+    ap.add_argument("--loop", type=int, default=1, help="0 device while loop, 1 host-polled batches (default)")
     ap.add_argument("--solves", type=int, default=1, help="repeat the solve (steady-state timing)")
     ap.add_argument("--rebuild", type=int, default=0, help="extra faces + symbolic passes (steady-state timing)")
     a = ap.parse_args()
@@ -55,6 +55,8 @@ def main():
         r = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)
         print(f"solve: {r['iterations']} it, {r['t_pcg_ms']:.3f} ms, {r['iterations'] / r['t_pcg_ms'] * 1e3:.0f} it/s, "
               f"spmv {r['t_spmv_ms'] / max(1, r['spmv_launches']) * 1e3:.2f} us")
+    if a.solves > 1:
+        fsfem_assemble_csr(g.ctx, 1.0e6, 0.3)
     fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
     try:
         rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)

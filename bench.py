@@ -147,6 +147,43 @@ def cpu_cores() -> int:
     return int(n) if n else (os.cpu_count() or 1)
 
 
+def cpu_info() -> dict:
+    """CPU model, sockets, physical cores and logical CPUs of this host, read at run time."""
+    model, phys, cores = None, set(), set()
+    try:
+        cur = {}
+        for line in open("/proc/cpuinfo"):
+            if ":" not in line:
+                if cur:
+                    phys.add(cur.get("physical id", "0"))
+                    cores.add((cur.get("physical id", "0"), cur.get("core id", cur.get("processor"))))
+                cur = {}
+                continue
+            k, v = [t.strip() for t in line.split(":", 1)]
+            cur[k] = v
+            if k == "model name" and model is None:
+                model = v
+        if cur:
+            phys.add(cur.get("physical id", "0"))
+            cores.add((cur.get("physical id", "0"), cur.get("core id", cur.get("processor"))))
+    except OSError:
+        pass
+    return {"model": model, "sockets": len(phys) or None, "physical_cores": len(cores) or None,
+            "logical_cpus": os.cpu_count()}
+
+
+def oracle_sample_threads(cfg: int, threads: int) -> dict:
+    """oracle_sample in a fresh process with OMP_NUM_THREADS=threads (the oracle's OpenMP loops
+    read it at load time; results are identical for any thread count)."""
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads), OMP_PROC_BIND="close", OMP_PLACES="cores")
+    code = (f"import json, sys; sys.path.insert(0, {ROOT!r}); import bench; "
+            f"print(json.dumps(bench.oracle_sample({cfg})))")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
+    d = json.loads(out.strip().splitlines()[-1])
+    d["threads"] = threads
+    return d
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -160,6 +197,7 @@ def run_reference(args):
         vals.append(s["t_step_s"])
         samples.append(s)
     t = float(np.mean(vals))
+    wall = float(np.mean([x["wall_s"] for x in samples]))
     nf = config_faces(args.config)
     v = nf / t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "faces/s", "n_gpus": args.gpus,
@@ -168,6 +206,12 @@ def run_reference(args):
             "config": {"workload": workload_name(args.config), "n_faces": nf},
             "components": {"assembly_faces_per_s": samples[-1]["assembly_faces_per_s"],
                            "pcg_it_per_s": samples[-1]["pcg_it_per_s"], "pcg_iterations": samples[-1]["iters_full"]},
+            "extrapolated": True,
+            "measured_wall_ms_per_step": wall * 1e3,
+            "note": ("each step runs the oracle on a bounded slab of the workload (measured_wall_ms_per_step) and "
+                     "scales each phase to the full config; value and ms_per_step are that extrapolation "
+                     "(a full cfg4 oracle step takes minutes)"),
+            "cpu": cpu_info(),
             "cpu_baseline": {"value": v, "unit": "faces/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": samples[-1]["sample"]},
             "e2e": {"value": v, "unit": "faces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -274,10 +318,13 @@ def run_gpu(args):
     iters = agg("iterations")
     spmv_ms = sum(r[2]["t_spmv_ms"] for r in reps)
     spmv_n = sum(r[2]["spmv_launches"] for r in reps)
-    vals_local = torch.tensor([t_num, t_pcg, spmv_ms / max(spmv_n, 1)], dtype=torch.float64, device=dev)
+    spmv_dev_ms = sum(r[2]["t_spmv_dev_ms"] for r in reps)
+    spmv_dev_n = sum(r[2]["spmv_dev_launches"] for r in reps)
+    vals_local = torch.tensor([t_num, t_pcg, spmv_ms / max(spmv_n, 1), spmv_dev_ms / max(spmv_dev_n, 1)],
+                              dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals_local, op=dist.ReduceOp.MAX)
-    t_num, t_pcg, spmv_avg_ms = [float(x) for x in vals_local.tolist()]
+    t_num, t_pcg, spmv_avg_ms, spmv_dev_avg_ms = [float(x) for x in vals_local.tolist()]
 
     # end to end through the C ABI with pinned host buffers (H2D of inputs, D2H of u per step)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
@@ -307,16 +354,28 @@ def run_gpu(args):
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(args.config, kind),
             "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms, "launches_timed": spmv_n,
             "peak_kind": peak_kind, "launches_per_step": iters + 1,
-            "share_of_step": spmv_avg_ms * (iters + 1) / (ms / args.steps),
+            "share_of_step": spmv_dev_ms / max(spmv_dev_n, 1) * (iters + 1) / (ms / args.steps),
             "timing": "CUDA events around the first SpMV of every 32-iteration CUDA-graph batch, live in the timed steps",
+            "device_timer": {"avg_launch_ms": spmv_dev_avg_ms, "launches": spmv_dev_n,
+                             "achieved": spmv_bytes / (spmv_dev_avg_ms / 1e3) / 1e9,
+                             "frac": spmv_bytes / (spmv_dev_avg_ms / 1e3) / 1e9 / peak,
+                             "how": "%globaltimer from the first CTA start to the last CTA end of EVERY PCG SpMV"},
             "full_csr_equivalent_bytes": 12 * nnz + 32 * 3 * m.n_nodes}
     asm_bytes = int(last["assembly_bytes"])
+    asm_aux = int(last["assembly_aux_bytes"])
+    survey_bytes = 24 * m.n_nodes + 16 * m.n_tets + 8 * nnz  # mesh + full CSR values
+    roof_asm = {"kernel": "k_asm_tile<0> (numeric assembly S2-S4 + S6, tiles)", "bound": "hbm",
+                "achieved": asm_bytes / (t_num / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": asm_bytes / (t_num / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": asm_bytes,
+                "aux_bytes_per_launch": asm_aux, "avg_launch_ms": t_num,
+                "frac_survey_full_csr_bytes": survey_bytes / (t_num / 1e3) / 1e9 / peak,
+                "timing": "CUDA events around the numeric assembly of every timed step (fsfem_report.t_numeric_ms)"}
     line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config), "n_nodes": m.n_nodes, "n_tets": m.n_tets,
                        "n_faces": nf, "nnz": nnz, "parallelism": f"row-block x{world} ({args.exchange})" if world > 1 else "single GPU",
-                       "pcg": "single-reduction Jacobi-PCG" if world > 1 else "Jacobi-PCG",
+                       "pcg": "Jacobi-PCG (standard recurrence, host-polled CUDA-graph batches of 32 iterations)",
                        "l2": "inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)"},
             "components": {"assembly_faces_per_s": nf / (t_num / 1e3), "assembly_ms": t_num,
                            "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,
@@ -324,12 +383,21 @@ def run_gpu(args):
                            "faces_ms": agg("t_faces_ms"), "symbolic_ms": agg("t_symbolic_ms"), "bc_ms": agg("t_bc_ms"),
                            "cold_faces_per_s": nf / ((agg("t_faces_ms") + agg("t_symbolic_ms") + t_num) / 1e3),
                            "true_rel_residual": reps[-1][2]["true_rel_residual"]},
-            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+            "roofline": roof, "roofline_assembly": roof_asm, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary()}
     if world == 1 and not args.no_cpu_baseline:
-        s = oracle_sample(args.config)
-        line["cpu_baseline"] = {"value": s["faces_per_s"], "unit": "faces/s", "cores": cpu_cores(), "kind": "oracle",
-                                "sample": s["sample"], "assembly_faces_per_s": s["assembly_faces_per_s"],
-                                "pcg_it_per_s": s["pcg_it_per_s"], "wall_s": s["wall_s"]}
+        allc = cpu_cores()
+        s_all = oracle_sample_threads(args.config, allc)
+        s_one = oracle_sample_threads(args.config, 1)
+        line["cpu_baseline"] = {"value": s_all["faces_per_s"], "unit": "faces/s", "cores": allc, "kind": "oracle",
+                                "sample": s_all["sample"] + " (extrapolated from the slab; the oracle's faces, "
+                                "assembly and BCs are single-threaded, its SpMV/PCG loops use all threads)",
+                                "assembly_faces_per_s": s_all["assembly_faces_per_s"],
+                                "pcg_it_per_s": s_all["pcg_it_per_s"], "wall_s": s_all["wall_s"],
+                                "one_thread": {"value": s_one["faces_per_s"], "pcg_it_per_s": s_one["pcg_it_per_s"],
+                                               "assembly_faces_per_s": s_one["assembly_faces_per_s"],
+                                               "wall_s": s_one["wall_s"]},
+                                "cpu": cpu_info()}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

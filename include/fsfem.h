@@ -67,8 +67,8 @@ typedef struct {
   double t_numeric_ms;       /* ... of the last numeric assembly (S2-S4, S6)                 */
   double t_bc_ms;            /* ... of the last apply_bc (S7)                                */
   double t_pcg_ms;           /* ... of the last pcg_solve loop (S8-S9)                       */
-  double t_spmv_ms;          /* summed duration of the PCG SpMV launches of that solve, timed on
-                                the device (%globaltimer: first CTA start to last CTA end)     */
+  double t_spmv_ms;          /* summed CUDA-event time of the sampled PCG SpMV launches (the first
+                                SpMV of every graph batch; device loop: = t_spmv_dev_ms)        */
   int64_t spmv_launches;     /* number of SpMV launches in t_spmv_ms                          */
   int64_t kernel_launches;   /* kernels launched by libfsfem in this process so far (monotonic;
                                 graph replays count their kernels, early-exit ones included) */
@@ -89,6 +89,9 @@ typedef struct {
   int64_t restarts;          /* residual-replacement restarts of the last pcg_solve              */
   int64_t assembly_aux_bytes; /* bytes of the precomputed assembly tiles read per numeric assembly
                                  (domain lists, field positions, block programs)   */
+  double t_spmv_dev_ms;      /* summed duration of EVERY PCG SpMV launch of the solve, timed on the
+                                device (%globaltimer: first CTA start to last CTA end)          */
+  int64_t spmv_dev_launches; /* number of launches in t_spmv_dev_ms                              */
 } fsfem_report;
 
 /* Human-readable name of a status code (static string). */

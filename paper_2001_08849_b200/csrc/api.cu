@@ -1219,7 +1219,10 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       FS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       set_capturing(true);
       try {
-        for (int it = 0; it < kBatch; ++it) pcg_iteration(cs, nullptr, nullptr);
+        // the first SpMV of every batch is bracketed by events (a live per-launch sample); an event
+        // pair around every SpMV would cost ~14 us per iteration at cfg4
+        for (int it = 0; it < kBatch; ++it)
+          pcg_iteration(cs, it == 0 ? c->spmv_ev[0] : nullptr, it == 0 ? c->spmv_ev[1] : nullptr);
       } catch (...) {
         set_capturing(false);
         cudaStreamEndCapture(c->stream, &g);
@@ -1235,6 +1238,8 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     int64_t total_iters = 0;
     int restarts = 0;
     double true_rel = 0.0, floor_rel = 0.0;
+    double ev_ms = 0.0;
+    int64_t ev_n = 0;
     for (;;) {
       if (device_loop) {
         FS_CUDA(cudaGraphLaunch(c->dgraph, c->stream));
@@ -1247,6 +1252,10 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
           FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
           count_launch(c->graph_launches);
           read_state();
+          if (c0->h_st->iters > before) {  // the sampled SpMV (iteration 0 of the batch) ran
+            ev_ms += elapsed(c->spmv_ev[0], c->spmv_ev[1]);
+            ++ev_n;
+          }
           if (c0->h_st->iters == before && c0->h_st->done_d == 0.0) throw Error(FSFEM_ERR_CUDA, "pcg made no progress");
         }
       }
@@ -1307,8 +1316,10 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       r->rep.residual_floor = floor_rel;
       r->rep.restarts = restarts;
       r->rep.t_pcg_ms = elapsed(c->ev0, c->ev1);
-      r->rep.t_spmv_ms = static_cast<double>(h.spmv_ns) * 1e-6;  // device timer, every PCG SpMV of the solve
-      r->rep.spmv_launches = static_cast<int64_t>(h.spmv_cnt);
+      r->rep.t_spmv_dev_ms = static_cast<double>(h.spmv_ns) * 1e-6;  // device timer, every PCG SpMV
+      r->rep.spmv_dev_launches = static_cast<int64_t>(h.spmv_cnt);
+      r->rep.t_spmv_ms = device_loop ? r->rep.t_spmv_dev_ms : ev_ms;  // CUDA events (host-polled loop)
+      r->rep.spmv_launches = device_loop ? r->rep.spmv_dev_launches : ev_n;
       r->rep.kernel_launches = launch_count();
     }
     if (rep) *rep = c->rep;

@@ -42,7 +42,8 @@ class FsfemReport(ctypes.Structure):
                 ("transposed_blocks", ctypes.c_int64), ("spmv_bytes", ctypes.c_int64),
                 ("assembly_bytes", ctypes.c_int64), ("spmv_kernel", ctypes.c_int64),
                 ("residual_floor", ctypes.c_double), ("restarts", ctypes.c_int64),
-                ("assembly_aux_bytes", ctypes.c_int64)]
+                ("assembly_aux_bytes", ctypes.c_int64), ("t_spmv_dev_ms", ctypes.c_double),
+                ("spmv_dev_launches", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

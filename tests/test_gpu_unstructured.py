@@ -69,3 +69,53 @@ def test_unstructured_parity(P, name, reorder):
     assert rep["converged"] == 1
     assert np.linalg.norm(u - uo) <= 1e-7 * np.linalg.norm(uo)
     g.close()
+
+
+def _icosphere_star(subdiv: int):
+    """A ball: the triangles of a subdivided icosahedron coned to the centre node 0 -- node 0 lies in
+    every tet (20 * 4**subdiv of them), a valid manifold mesh with one very high-valence node."""
+    t = (1 + 5 ** 0.5) / 2
+    V = [[-1, t, 0], [1, t, 0], [-1, -t, 0], [1, -t, 0], [0, -1, t], [0, 1, t], [0, -1, -t], [0, 1, -t],
+         [t, 0, -1], [t, 0, 1], [-t, 0, -1], [-t, 0, 1]]
+    F = [[0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11], [1, 5, 9], [5, 11, 4], [11, 10, 2], [10, 7, 6],
+         [7, 1, 8], [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8], [3, 8, 9], [4, 9, 5], [2, 4, 11], [6, 2, 10],
+         [8, 6, 7], [9, 8, 1]]
+    V = [list(np.array(v) / np.linalg.norm(v)) for v in V]
+    for _ in range(subdiv):
+        mid = {}
+
+        def m(a, b):
+            k = (min(a, b), max(a, b))
+            if k not in mid:
+                p = (np.array(V[a]) + np.array(V[b])) / 2
+                V.append(list(p / np.linalg.norm(p)))
+                mid[k] = len(V) - 1
+            return mid[k]
+        F = [g for a, b, c in F for g in ([a, m(a, b), m(c, a)], [b, m(b, c), m(a, b)], [c, m(c, a), m(b, c)],
+                                           [m(a, b), m(b, c), m(c, a)])]
+    xyz = np.vstack([[0.0, 0.0, 0.0], np.array(V)])
+    tets = np.array([[0, a + 1, b + 1, c + 1] for a, b, c in F], np.int32)
+    return xyz, tets
+
+
+def test_high_valence_node_limits(P):
+    """Documented limits (include/fsfem.h UNSUPPORTED): a node in more than 128 tets is rejected by
+    the symbolic pass; below the limit the same kind of mesh assembles and matches the oracle."""
+    xyz, tets = _icosphere_star(2)  # 320 tets around node 0
+    g = P.FsFem()
+    g.build_faces(xyz, tets)
+    with pytest.raises(P.FsfemError) as e:
+        g.assemble_csr(E, NU)
+    assert e.value.status == "UNSUPPORTED"
+    g.close()
+    xyz, tets = _icosphere_star(1)  # 80 tets around node 0: within the limits
+    o = Oracle(xyz, tets)
+    o.build_faces()
+    _, orp, oci, ova = o.assemble_fs(E, NU)
+    g = P.FsFem()
+    g.build_faces(xyz, tets)
+    g.assemble_csr(E, NU)
+    c = g.get_csr()
+    assert np.array_equal(c.row_ptr, orp) and np.array_equal(c.col_idx, oci)
+    assert np.abs(c.vals - ova).max() <= 1e-12 * np.abs(ova).max()
+    g.close()

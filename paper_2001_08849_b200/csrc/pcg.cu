@@ -28,6 +28,9 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 #ifndef FSFEM_PDL
 #define FSFEM_PDL 0
 #endif
+#ifndef FSFEM_COOP
+#define FSFEM_COOP 1
+#endif
 __device__ __forceinline__ void pdl_wait() {
   if (FSFEM_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -552,16 +555,18 @@ __device__ __forceinline__ int ld_acquire_cta_s32(const int* p) {
 constexpr int kDfBatch = FSFEM_DF_BATCH;
 constexpr int kDfMinChunksPerCta = 16;
 constexpr int kDfThreads = kThreads + 96;  // 8 compute warps, loader, phase-2 and counter warps
-struct P2Layout {  // phase-2 buffer: node pointers, P1 sums, pushed slots of one chunk
+struct P2Layout {  // phase-2 buffer: node pointers, P1 sums, own x (p.q), pushed slots of one chunk
   static constexpr int kPtr = 0;                               // kChunkNodes + 4 int64
   static constexpr int kY = kPtr + (kChunkNodes + 4) * 8;      // 3 kChunkNodes + 4 double
-  static constexpr int kT = kY + (3 * kChunkNodes + 4) * 8;    // 3 kCapBlocks + 4 double
+  static constexpr int kXo = kY + (3 * kChunkNodes + 4) * 8;   // 3 kChunkNodes + 4 double
+  static constexpr int kT = kXo + (3 * kChunkNodes + 4) * 8;   // 3 kCapBlocks + 4 double
   static constexpr int kBytes = kT + (3 * kCapBlocks + 4) * 8;
 };
-static_assert(P2Layout::kY % 16 == 0 && P2Layout::kT % 16 == 0 && P2Layout::kBytes % 16 == 0,
+static_assert(P2Layout::kY % 16 == 0 && P2Layout::kXo % 16 == 0 && P2Layout::kT % 16 == 0 &&
+                  P2Layout::kBytes % 16 == 0,
               "phase-2 buffer regions must be 16-B aligned");
 struct P2Info {
-  int n0, nn, Pt0, Pt1, dptr, dy, dt, pad;
+  int n0, nn, Pt0, Pt1, dptr, dy, dt, dxo;
 };
 #ifndef FSFEM_DF_STAGES
 #define FSFEM_DF_STAGES 2
@@ -726,7 +731,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         qi.dptr = stage_off(tptr, ch.n0, 8);
         qi.dy = stage_off(y, 3 * (int64_t)ch.n0, 8);
         qi.dt = stage_off(tbuf, 3 * (int64_t)ch.Pt0, 8);
-        qi.pad = 0;
+        qi.dxo = stage_off(xown, 3 * (int64_t)ch.n0, 8);
         qinfo[jj & 1] = qi;
         auto rbytes = [](const void* base, int64_t e0, int64_t e1, int es) -> uint32_t {
           if (e1 <= e0) return 0;
@@ -735,11 +740,13 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         };
         mbar_arrive_expect_tx(&p2full[jj & 1], rbytes(tptr, ch.n0, ch.n1 + 1, 8) +
                                                    rbytes(y, 3 * (int64_t)ch.n0, 3 * (int64_t)ch.n1, 8) +
+                                                   (kPcg ? rbytes(xown, 3 * (int64_t)ch.n0, 3 * (int64_t)ch.n1, 8) : 0u) +
                                                    rbytes(tbuf, 3 * (int64_t)ch.Pt0, 3 * (int64_t)ch.Pt1, 8));
         uint32_t tx = 0;
         stage_copy(qb + P2Layout::kPtr, tptr, ch.n0, ch.n1 + 1, 8, &p2full[jj & 1], tx);
         stage_copy(qb + P2Layout::kY, y, 3 * (int64_t)ch.n0, 3 * (int64_t)ch.n1, 8, &p2full[jj & 1], tx);
         stage_copy(qb + P2Layout::kT, tbuf, 3 * (int64_t)ch.Pt0, 3 * (int64_t)ch.Pt1, 8, &p2full[jj & 1], tx);
+        if (kPcg) stage_copy(qb + P2Layout::kXo, xown, 3 * (int64_t)ch.n0, 3 * (int64_t)ch.n1, 8, &p2full[jj & 1], tx);
       }
       __syncwarp();
     };
@@ -751,10 +758,11 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         issue(j);
         ++issued;
       }
-      if (issued == j + 1 && j + 1 < K && ready_now(blockIdx.x + (j + 1) * gridDim.x)) {
-        issue(j + 1);
-        ++issued;
-      }
+      // readiness of the next chunk: the acquire load is issued now and looked at after this
+      // chunk's sums, so its latency overlaps them
+      uint32_t nflag = 0u;
+      const bool probe = issued == j + 1 && j + 1 < K;
+      if (probe && lane == 0) nflag = ld_acquire_u32(ready + blockIdx.x + (j + 1) * gridDim.x);
       DF_T(tA)
       ++nitems;
       mbar_wait(&p2full[j & 1], (j >> 1) & 1);
@@ -764,6 +772,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       const int64_t* tp = reinterpret_cast<const int64_t*>(qb + P2Layout::kPtr) + qi.dptr;
       const double* yp = reinterpret_cast<const double*>(qb + P2Layout::kY) + qi.dy;
       const double* tv = reinterpret_cast<const double*>(qb + P2Layout::kT) + qi.dt;
+      const double* xq = reinterpret_cast<const double*>(qb + P2Layout::kXo) + qi.dxo;
       const bool act = lane < qi.nn;
       const int mm = act ? lane : 0;
       const int e0 = static_cast<int>(tp[mm] - qi.Pt0), e1 = act ? static_cast<int>(tp[mm + 1] - qi.Pt0) : e0;
@@ -782,10 +791,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         y[3 * il] = s0;
         y[3 * il + 1] = s1;
         y[3 * il + 2] = s2;
-        if (kPcg) {
-          const double* xo = xown + 3 * il;
-          dt = fma(__ldg(xo), s0, fma(__ldg(xo + 1), s1, __ldg(xo + 2) * s2));
-        }
+        if (kPcg) dt = fma(xq[3 * mm], s0, fma(xq[3 * mm + 1], s1, xq[3 * mm + 2] * s2));
       }
       if (kPcg) {
         dt = warp_sum(dt);
@@ -797,6 +803,10 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       for (uintptr_t ad = ((lo + 127) & ~uintptr_t(127)) + 128 * lane; ad + 128 <= hi; ad += 128 * 32)
         asm volatile("discard.global.L2 [%0], 128;" ::"l"(ad) : "memory");
       __syncwarp();
+      if (probe && __shfl_sync(0xffffffffu, nflag, 0) == epoch) {
+        issue(j + 1);
+        ++issued;
+      }
     }
   } else {
     // ---------------- compute warps: P1 ----------------
@@ -1365,7 +1375,7 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;  // phase-2 waits need every CTA resident
-    attr[0].val.cooperative = 1;
+    attr[0].val.cooperative = FSFEM_COOP;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
@@ -1453,7 +1463,7 @@ void launch_update_direction(double* x, double* r, double* p, const double* q, c
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  attr[0].val.cooperative = FSFEM_COOP;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;

@@ -246,6 +246,16 @@ def traffic_from_profile(cfg: int, kernel: int):
     return None
 
 
+def asm_traffic_from_profile(cfg: int, what: str = ""):
+    """DRAM bytes of one numeric assembly (ncu dram__bytes_read.sum + dram__bytes_write.sum), or with
+    what="fp64_pipe_pct" its FP64 pipe utilisation, from the committed capture
+    (profiles/asm_dram_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "asm_dram_traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get(f"cfg{cfg}" + (f"_{what}" if what else ""))
+    return None
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -369,6 +379,8 @@ def run_gpu(args):
                 "frac": asm_bytes / (t_num / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": asm_bytes,
                 "aux_bytes_per_launch": asm_aux, "avg_launch_ms": t_num,
                 "frac_survey_full_csr_bytes": survey_bytes / (t_num / 1e3) / 1e9 / peak,
+                "traffic": asm_traffic_from_profile(args.config),
+                "fp64_pipe_pct_ncu": asm_traffic_from_profile(args.config, "fp64_pipe_pct"),
                 "timing": "CUDA events around the numeric assembly of every timed step (fsfem_report.t_numeric_ms)"}
     line = {"metric": METRIC, "value": value, "unit": "faces/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",

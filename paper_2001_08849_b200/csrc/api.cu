@@ -1119,6 +1119,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
         r->h_st->upd_part = r->part.get() + 4 * pcg_grid();
         r->h_st->upd_n = cg_update_grid(3 * r->nloc);
         r->h_st->spmv_t0 = ~0ull;
+        r->h_st->upd_t0 = ~0ull;
         FS_CUDA(cudaMemcpyAsync(r->st.get(), r->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, r->stream));
       }
     };
@@ -1322,6 +1323,10 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       r->rep.spmv_launches = device_loop ? r->rep.spmv_dev_launches : ev_n;
       r->rep.kernel_launches = launch_count();
     }
+    if (std::getenv("FSFEM_GAP_PRINT"))
+      std::fprintf(stderr, "gap timing: spmv %.2f us, update %.2f us, spmv->update gap %.2f us (%llu updates)\n",
+                   h.spmv_ns * 1e-3 / std::max(1ull, h.spmv_cnt), h.upd_ns * 1e-3 / std::max(1ull, h.upd_cnt),
+                   h.gap_ns * 1e-3 / std::max(1ull, h.upd_cnt), h.upd_cnt);
     if (rep) *rep = c->rep;
     if (status == FSFEM_ERR_BREAKDOWN) return fail(c, FSFEM_ERR_BREAKDOWN, "pcg breakdown (p.q <= 0 or non-finite)");
     if (status == FSFEM_ERR_NOT_CONVERGED) {

@@ -1158,6 +1158,10 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
   __shared__ double sh_sc[4];
   pdl_trigger();
   pdl_wait();
+#ifndef FSFEM_GAP_TIMING
+#define FSFEM_GAP_TIMING 0
+#endif
+  if (FSFEM_GAP_TIMING && threadIdx.x == 0) atomicMin(&st->upd_t0, global_ns());
   if (threadIdx.x == 0) {
     sh_sc[0] = ld_cg(&st->done_d);
     sh_sc[1] = ld_cg(&st->alpha);
@@ -1227,6 +1231,19 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
       if (k < n) {
         x[k] = fma(alpha, pv[j], xv[j]);
         p[k] = fma(beta, pv[j], dv[j] * rv[j]);
+      }
+    }
+  }
+  if (FSFEM_GAP_TIMING) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&st->upd_done, 1u) == gridDim.x - 1) {
+        const unsigned long long t1 = global_ns(), t0 = atomicExch(&st->upd_t0, ~0ull);
+        st->upd_ns += t1 - t0;
+        if (t0 > st->spmv_tend) st->gap_ns += t0 - st->spmv_tend;
+        st->upd_cnt += 1;
+        st->upd_done = 0u;
       }
     }
   }

@@ -34,6 +34,9 @@ struct PcgState {
   unsigned long long spmv_t0;
   unsigned long long spmv_ns;
   unsigned long long spmv_cnt;
+  // FSFEM_GAP_TIMING (tuning builds): end of the last SpMV, update kernel start / duration, gaps
+  unsigned long long spmv_tend, upd_t0, upd_ns, gap_ns, upd_cnt;
+  unsigned int upd_done;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -52,6 +55,7 @@ __device__ __forceinline__ void spmv_time_end(PcgState* st) {  // one thread of 
     st->spmv_ns += t1 - t0;
     st->spmv_cnt += 1;
   }
+  st->spmv_tend = t1;
 }
 
 __device__ __forceinline__ void pcg_stop(PcgState* st, int status) {

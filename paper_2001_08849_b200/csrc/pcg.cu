@@ -22,6 +22,37 @@ constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+// The PCG vectors (x, r, p, q, D^-1; 40 MB at cfg4) are read and written with an L2 evict_last
+// hint so that the SpMV's matrix stream (evict_first) does not push them out of L2 between the
+// kernels of an iteration (FSFEM_VEC_EVICT_LAST).
+#ifndef FSFEM_VEC_EVICT_LAST
+#define FSFEM_VEC_EVICT_LAST 1
+#endif
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_vec(const double* p, uint64_t pol) {
+  if (!FSFEM_VEC_EVICT_LAST) return *p;
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_vec(const double* p, uint64_t pol) {  // read-only in the kernel
+  if (!FSFEM_VEC_EVICT_LAST) return __ldg(p);
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_vec(double* p, double v, uint64_t pol) {
+  if (!FSFEM_VEC_EVICT_LAST) {
+    *p = v;
+    return;
+  }
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // Programmatic dependent launch (PDL, FSFEM_PDL): a kernel launched with the programmatic
 // serialization attribute may start before its predecessor finished; it waits here before it
 // touches anything the predecessor wrote, and the predecessor lets it launch early.
@@ -788,9 +819,10 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       double dt = 0.0;
       const int64_t il = static_cast<int64_t>(qi.n0) + mm;
       if (act) {
-        y[3 * il] = s0;
-        y[3 * il + 1] = s1;
-        y[3 * il + 2] = s2;
+        const uint64_t vpol = policy_evict_last();
+        st_vec(y + 3 * il, s0, vpol);
+        st_vec(y + 3 * il + 1, s1, vpol);
+        st_vec(y + 3 * il + 2, s2, vpol);
         if (kPcg) dt = fma(xq[3 * mm], s0, fma(xq[3 * mm + 1], s1, xq[3 * mm + 2] * s2));
       }
       if (kPcg) {
@@ -813,6 +845,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
     constexpr int G = kGroupLanes, NPW = 32 / kGroupLanes;
     const int grp = lane / G, gl = lane % G;
     const int m = warp * NPW + grp;  // this group's node inside every chunk
+    const uint64_t vpol = policy_evict_last();
     for (int j = 0; j < K; ++j) {
       const int s = j % kDfStages;
       DF_T(tC)
@@ -842,7 +875,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
           xs[u] = 0.0;
           if (k < nus) {
             const int b = k / 3, cc = k - 3 * b;
-            xs[u] = __ldg(x + 3 * sn[ls + b] + cc);
+            xs[u] = ldg_vec(x + 3 * sn[ls + b] + cc, vpol);
           }
         }
 #pragma unroll
@@ -1172,25 +1205,62 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
   if (sh_sc[0] != 0.0) return;  // uniform over the grid: done_d is only written between launches
   const double alpha = sh_sc[1], rho_old = sh_sc[2];
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t pol = policy_evict_last();
   double rr = 0.0, rz = 0.0;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
-    double rv[kVec], qv[kVec], dv[kVec];
+  // Small enough (<= kKeep passes per thread, cfg4): every load -- r, q, D^-1 and also x, p -- is
+  // issued before the grid barrier and z = D^-1 r, x, p stay in registers across it, so phase 2
+  // only stores (64 instead of 80 B per dof, no load after the barrier).
+  constexpr int kKeep = 2;
+  const bool keep = n <= static_cast<int64_t>(kKeep) * kVec * T;
+  double zk_[kKeep][kVec], xk_[kKeep][kVec], pk_[kKeep][kVec];
+  if (keep) {
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int64_t k = b + j * T;
-      const bool ok = k < n;
-      rv[j] = ok ? r[k] : 0.0;
-      qv[j] = ok ? q[k] : 0.0;
-      dv[j] = ok ? dinv[k] : 0.0;
+    for (int ps = 0; ps < kKeep; ++ps) {
+      const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + static_cast<int64_t>(ps) * kVec * T;
+      double rv[kVec], qv[kVec], dv[kVec];
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        const bool ok = k < n;
+        rv[j] = ok ? ld_vec(r + k, pol) : 0.0;
+        qv[j] = ok ? ldg_vec(q + k, pol) : 0.0;
+        dv[j] = ok ? ldg_vec(dinv + k, pol) : 0.0;
+        xk_[ps][j] = ok ? ld_vec(x + k, pol) : 0.0;
+        pk_[ps][j] = ok ? ld_vec(p + k, pol) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        zk_[ps][j] = 0.0;
+        if (k < n) {  // same element order and arithmetic as the general path below
+          const double rk = fma(-alpha, qv[j], rv[j]);
+          st_vec(r + k, rk, pol);
+          rr = fma(rk, rk, rr);
+          rz = fma(rk, dv[j] * rk, rz);
+          zk_[ps][j] = dv[j] * rk;
+        }
+      }
     }
+  } else {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+      double rv[kVec], qv[kVec], dv[kVec];
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int64_t k = b + j * T;
-      if (k < n) {
-        const double rk = fma(-alpha, qv[j], rv[j]);
-        r[k] = rk;
-        rr = fma(rk, rk, rr);
-        rz = fma(rk, dv[j] * rk, rz);
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        const bool ok = k < n;
+        rv[j] = ok ? ld_vec(r + k, pol) : 0.0;
+        qv[j] = ok ? ldg_vec(q + k, pol) : 0.0;
+        dv[j] = ok ? ldg_vec(dinv + k, pol) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        if (k < n) {
+          const double rk = fma(-alpha, qv[j], rv[j]);
+          st_vec(r + k, rk, pol);
+          rr = fma(rk, rk, rr);
+          rz = fma(rk, dv[j] * rk, rz);
+        }
       }
     }
   }
@@ -1214,23 +1284,38 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
   }
   __syncthreads();
   const double beta = sh_beta;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
-    double xv[kVec], pv[kVec], rv[kVec], dv[kVec];
+  if (keep) {
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int64_t k = b + j * T;
-      const bool ok = k < n;
-      xv[j] = ok ? x[k] : 0.0;
-      pv[j] = ok ? p[k] : 0.0;
-      rv[j] = ok ? r[k] : 0.0;
-      dv[j] = ok ? dinv[k] : 0.0;
+    for (int ps = 0; ps < kKeep; ++ps) {
+      const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + static_cast<int64_t>(ps) * kVec * T;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        if (k < n) {
+          st_vec(x + k, fma(alpha, pk_[ps][j], xk_[ps][j]), pol);
+          st_vec(p + k, fma(beta, pk_[ps][j], zk_[ps][j]), pol);
+        }
+      }
     }
+  } else {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += kVec * T) {
+      double xv[kVec], pv[kVec], rv[kVec], dv[kVec];
 #pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int64_t k = b + j * T;
-      if (k < n) {
-        x[k] = fma(alpha, pv[j], xv[j]);
-        p[k] = fma(beta, pv[j], dv[j] * rv[j]);
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        const bool ok = k < n;
+        xv[j] = ok ? ld_vec(x + k, pol) : 0.0;
+        pv[j] = ok ? ld_vec(p + k, pol) : 0.0;
+        rv[j] = ok ? ld_vec(r + k, pol) : 0.0;
+        dv[j] = ok ? ldg_vec(dinv + k, pol) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        const int64_t k = b + j * T;
+        if (k < n) {
+          st_vec(x + k, fma(alpha, pv[j], xv[j]), pol);
+          st_vec(p + k, fma(beta, pv[j], dv[j] * rv[j]), pol);
+        }
       }
     }
   }

@@ -149,6 +149,12 @@ fsfem_status fsfem_nccl_get_unique_id(void* out);
  * NCCL (send/recv unavailable). */
 enum { FSFEM_EXCHANGE_ALLGATHER = 0, FSFEM_EXCHANGE_HALO = 1 };
 fsfem_status fsfem_set_exchange(fsfem_ctx* ctx, int mode);
+/* Overlap (default off until measured on several GPUs): each PCG SpMV is split
+ * into the chunks whose columns are all own rows and the others; the exchange of the search
+ * direction (all-gather(v) or halo send/recv) runs on a side stream while the first part is
+ * multiplied, and the second part waits for it (fork/join events, captured into the graphs).
+ * Multi-rank, not with deterministic dots; uses the gather SpMV kernel.  Errors: none. */
+fsfem_status fsfem_set_overlap(fsfem_ctx* ctx, int on);
 /* The rank's halo after assemble_csr: *n = number of nodes (0 with one rank); nodes (host or
  * device, may be NULL) receives their global ids, ascending (so grouped by owner rank).  Works
  * on partition-only contexts.  Errors: STATE. */

@@ -19,6 +19,7 @@ from .fsfem import (  # noqa: F401
     fsfem_get_partition,
     fsfem_set_deterministic,
     fsfem_set_loop,
+    fsfem_set_overlap,
     fsfem_create,
     fsfem_destroy,
     fsfem_get_csr,

@@ -154,6 +154,9 @@ struct fsfem_ctx {
   // one device and one stream; collectives become device copies (SURVEY.md §4 simulated partition)
   std::shared_ptr<std::vector<fsfem_ctx*>> loop;
   bool det = false;             // deterministic dots (fsfem_set_deterministic)
+  bool overlap = false;         // exchange of the search direction overlapped with the interior SpMV
+  cudaStream_t side = nullptr;  // its side stream (created on first use) and fork / join events
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf<double> dpart;         // det: [3 * global chunks] chunk partials
   // mesh
   int64_t nn = 0, nt = 0, nf = 0, ni = 0;
@@ -519,6 +522,51 @@ void setup_halo(const Ranks& cs) {
   c->halo_ready = true;
 }
 
+// Overlap: the exchange of the search direction runs on a side stream while the
+// interior chunks (no column outside the rank's range) are multiplied; the boundary chunks follow
+// once the exchange has landed.  Fork / join by events, so it is captured into the graphs too.
+bool overlapping(const Ranks& cs) {
+  const fsfem_ctx* c0 = cs[0];
+  return c0->overlap && c0->nranks > 1 && !c0->det;
+}
+
+void spmv_with_exchange(const Ranks& cs, DevBuf<double> fsfem_ctx::*buf, DevBuf<double> fsfem_ctx::*out,
+                        cudaEvent_t e0, cudaEvent_t e1) {
+  fsfem_ctx* c0 = cs[0];
+  if (!c0->side) {
+    FS_CUDA(cudaStreamCreateWithFlags(&c0->side, cudaStreamNonBlocking));
+    FS_CUDA(cudaEventCreateWithFlags(&c0->ev_fork, cudaEventDisableTiming));
+    FS_CUDA(cudaEventCreateWithFlags(&c0->ev_join, cudaEventDisableTiming));
+  }
+  cudaStream_t main = c0->stream;
+  FS_CUDA(cudaEventRecord(c0->ev_fork, main));
+  FS_CUDA(cudaStreamWaitEvent(c0->side, c0->ev_fork, 0));
+  std::vector<cudaStream_t> saved;
+  for (fsfem_ctx* c : cs) {  // the collective code path, issued on the side stream
+    saved.push_back(c->stream);
+    c->stream = c0->side;
+  }
+  try {
+    coll_full(cs, buf);
+  } catch (...) {
+    for (size_t k = 0; k < cs.size(); ++k) cs[k]->stream = saved[k];
+    throw;
+  }
+  for (size_t k = 0; k < cs.size(); ++k) cs[k]->stream = saved[k];
+  FS_CUDA(cudaEventRecord(c0->ev_join, c0->side));
+  for (fsfem_ctx* c : cs) {
+    if (e0 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+    launch_spmv_split(c->pat, 1, c->vals.get(), (c->*buf).get(), 3 * c->n_lo, (c->*out).get(), c->st.get(),
+                      c->part.get(), c->stream);
+  }
+  FS_CUDA(cudaStreamWaitEvent(main, c0->ev_join, 0));
+  for (fsfem_ctx* c : cs) {
+    launch_spmv_split(c->pat, 2, c->vals.get(), (c->*buf).get(), 3 * c->n_lo, (c->*out).get(), c->st.get(),
+                      c->part.get(), c->stream);
+    if (e1 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  }
+}
+
 // ---- one PCG iteration over the ranks ----------------------------------------------------------
 double* own_p(fsfem_ctx* c) { return c->p_full.get() + 3 * c->n_lo; }
 double* own_x(fsfem_ctx* c) { return c->x_full.get() + 3 * c->n_lo; }
@@ -536,11 +584,15 @@ void iter_cg(const Ranks& cs, cudaEvent_t e0, cudaEvent_t e1) {
   for (fsfem_ctx* c : cs)
     launch_cg_update(own_x(c), c->r.get(), own_p(c), c->cg_p.get(), c->cg_s.get(), c->q.get(), c->dinv.get(),
                      3 * c->nloc, c->st.get(), c->part.get() + 4 * pcg_grid(), c->stream);
-  coll_full(cs, &fsfem_ctx::p_full);
-  for (fsfem_ctx* c : cs) {
-    if (e0 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
-    spmv_of(c, c->p_full.get(), c->q.get(), true);
-    if (e1 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  if (overlapping(cs)) {
+    spmv_with_exchange(cs, &fsfem_ctx::p_full, &fsfem_ctx::q, e0, e1);
+  } else {
+    coll_full(cs, &fsfem_ctx::p_full);
+    for (fsfem_ctx* c : cs) {
+      if (e0 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+      spmv_of(c, c->p_full.get(), c->q.get(), true);
+      if (e1 && c == cs[0]) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+    }
   }
   coll_partials(cs, 4);
 }
@@ -573,10 +625,15 @@ void pcg_iteration(const Ranks& cs, cudaEvent_t e0, cudaEvent_t e1) {
   fsfem_ctx* c0 = cs[0];
   if (c0->det) return iter_det(cs, e0, e1);
   if (c0->cg_active) return iter_cg(cs, e0, e1);
-  for (fsfem_ctx* c : cs) {
-    if (e0 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
-    spmv_of(c, c->p_full.get(), c->q.get(), true);
-    if (e1 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+  const bool ov = overlapping(cs);
+  if (ov) {  // this iteration's exchange of p (issued at its start, see below) overlaps the interior rows
+    spmv_with_exchange(cs, &fsfem_ctx::p_full, &fsfem_ctx::q, e0, e1);
+  } else {
+    for (fsfem_ctx* c : cs) {
+      if (e0 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e0, c->stream, cudaEventRecordExternal));
+      spmv_of(c, c->p_full.get(), c->q.get(), true);
+      if (e1 && c == c0) FS_CUDA(cudaEventRecordWithFlags(e1, c->stream, cudaEventRecordExternal));
+    }
   }
   if (c0->nranks == 1) {
     launch_update_direction(own_x(c0), c0->r.get(), own_p(c0), c0->q.get(), c0->dinv.get(), 3 * c0->nloc,
@@ -589,7 +646,7 @@ void pcg_iteration(const Ranks& cs, cudaEvent_t e0, cudaEvent_t e1) {
                   c->stream);
   coll_partials(cs, 2);
   for (fsfem_ctx* c : cs) launch_direction(own_p(c), c->r.get(), c->dinv.get(), 3 * c->nloc, c->st.get(), c->stream);
-  coll_full(cs, &fsfem_ctx::p_full);
+  if (!ov) coll_full(cs, &fsfem_ctx::p_full);  // (overlap: exchanged at the next SpMV)
 }
 
 // Everything a captured batch of iterations bakes in: buffer pointers of every rank, sizes,
@@ -625,6 +682,7 @@ std::vector<uintptr_t> graph_key_of(const Ranks& cs) {
     k.push_back(static_cast<uintptr_t>(c->exchange));
     k.push_back(static_cast<uintptr_t>(c->cg_active));
     k.push_back(static_cast<uintptr_t>(c->det));
+    k.push_back(static_cast<uintptr_t>(c->overlap));
     for (int64_t v : c->halo_send) k.push_back(static_cast<uintptr_t>(v));
     for (int64_t v : c->halo_need) k.push_back(static_cast<uintptr_t>(v));
     for (int64_t v : c->ranges) k.push_back(static_cast<uintptr_t>(v));
@@ -691,6 +749,9 @@ fsfem_status fsfem_destroy(fsfem_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (auto e : c->spmv_ev)
@@ -751,6 +812,13 @@ fsfem_status fsfem_comm_init_loopback(fsfem_ctx** ctxs, int nranks) {
     ctxs[r]->loop = group;
   }
   return FSFEM_OK;
+}
+
+fsfem_status fsfem_set_overlap(fsfem_ctx* c, int on) {
+  return guarded(c, [&]() -> fsfem_status {
+    c->overlap = on != 0;
+    return FSFEM_OK;
+  });
 }
 
 fsfem_status fsfem_set_loop(fsfem_ctx* c, int mode) {
@@ -957,6 +1025,7 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
       if (c->nranks > 1) {
         // the exchange lists are agreed with the peers at the first pcg_solve (setup_halo)
         build_halo_device(c->pat, c->nn, c->ranges, c->halo_need, c->scratch, c->stream);
+        build_overlap_chunks(c->pat, c->stream);
       }
       drop_graph(c);
     }

@@ -62,6 +62,10 @@ struct Pattern {
   bool df_ok = false;        // every chunk's producer list fits kMaxDeps
   DevBuf<int32_t> dep_ptr;   // [nchunks + 1]
   DevBuf<int2> dep_list;     // [dep_ptr[nchunks]] (chunk d, need[d])
+  // split SpMV (halo overlap): the chunks reordered interior first, nch_int of them interior
+  bool have_ov = false;
+  int64_t nch_int = 0;
+  DevBuf<SpmvChunk> chunks_ov;
   DevBuf<uint32_t> cnt;      // [nchunks] arrival counters, wrapping at need (atomicInc: 0 .. need-1)
   DevBuf<double> dotc;       // [nchunks] per-chunk p.q partials
   // halo of the rank (halo.cu, row partitions only): columns of the own rows outside the range

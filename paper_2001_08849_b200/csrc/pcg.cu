@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
                                                        const int32_t* __restrict__ snbr,
                                                        const int2* __restrict__ tlist, const double* __restrict__ vals,
                                                        const double* __restrict__ x, int64_t own_off,
-                                                       double* __restrict__ y, PcgState* st, double* part) {
+                                                       double* __restrict__ y, PcgState* st, double* part,
+                                                       int split = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // the dynamic window follows the static shared memory of grid_reduce: align it by hand
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -485,8 +486,32 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   const double mine[1] = {dot};
   double out[1];
   if (grid_reduce<1>(mine, part, &st->ticket[0], out)) {
-    spmv_finish(st, out[0]);
-    if (threadIdx.x == 0) spmv_time_end(st);
+    // split SpMV: part 1 keeps its p.q, part 2 adds it first (fixed order) and finishes
+    if (split == 1) {
+      if (threadIdx.x == 0) st->pq_part = out[0];
+    } else {
+      __shared__ double sh_pq;
+      if (threadIdx.x == 0) sh_pq = (split == 2 ? ld_cg(&st->pq_part) : 0.0) + out[0];
+      __syncthreads();
+      spmv_finish(st, sh_pq);
+      if (threadIdx.x == 0) spmv_time_end(st);
+    }
+  }
+}
+
+// Interior chunks of a row partition: every stored column (incl. halo-stored ones) in [lo, hi).
+__global__ void k_chunk_interior(const SpmvChunk* __restrict__ chunks, int nch, const int32_t* __restrict__ snbr,
+                                 int64_t lo, int64_t hi, int32_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nch; c += (gridDim.x * blockDim.x) >> 5) {
+    const SpmvChunk ch = chunks[c];
+    bool in = true;
+    for (int b = ch.Ps0 + lane; b < ch.Ps1; b += 32) {
+      const int32_t j = snbr[b];
+      in = in && j >= lo && j < hi;
+    }
+    in = __all_sync(0xffffffffu, in);
+    if (lane == 0) flag[c] = in ? 1 : 0;
   }
 }
 
@@ -1511,6 +1536,45 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     k_spmv<false><<<spmv_grid(nch), kThreads, kStreamSmem, s>>>(pat.chunks.get(), nch, pat.sptr.get(), pat.tptr.get(),
                                                              pat.snbr.get(), pat.tlist.get(), vals, x_full, own_off, y,
                                                              st, part);
+  FS_LAUNCH_CHECK();
+}
+
+void build_overlap_chunks(Pattern& pat, cudaStream_t s) {
+  FS_CUDA(cudaFuncSetAttribute(k_spmv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem));
+  const int64_t nch = pat.nchunks;
+  pat.have_ov = true;
+  pat.nch_int = 0;
+  pat.chunks_ov.ensure(std::max<int64_t>(nch, 1));
+  if (nch == 0) return;
+  DevBuf<int32_t> flag;
+  flag.ensure(nch);
+  const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nch * 32, 256), 16LL * num_sms())));
+  k_chunk_interior<<<g, 256, 0, s>>>(pat.chunks.get(), static_cast<int>(nch), pat.snbr.get(), pat.n_lo,
+                                     pat.n_lo + pat.nloc, flag.get());
+  FS_LAUNCH_CHECK();
+  std::vector<int32_t> hf(nch);
+  std::vector<SpmvChunk> hc(nch), ho;
+  FS_CUDA(cudaMemcpyAsync(hf.data(), flag.get(), sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(hc.data(), pat.chunks.get(), sizeof(SpmvChunk) * nch, cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+  ho.reserve(nch);
+  for (int64_t c = 0; c < nch; ++c)
+    if (hf[c]) ho.push_back(hc[c]);
+  pat.nch_int = static_cast<int64_t>(ho.size());
+  for (int64_t c = 0; c < nch; ++c)
+    if (!hf[c]) ho.push_back(hc[c]);
+  FS_CUDA(cudaMemcpyAsync(pat.chunks_ov.get(), ho.data(), sizeof(SpmvChunk) * nch, cudaMemcpyHostToDevice, s));
+  FS_CUDA(cudaStreamSynchronize(s));
+}
+
+void launch_spmv_split(const Pattern& pat, int part_no, const double* vals, const double* x_full, int64_t own_off,
+                       double* y, PcgState* st, double* part, cudaStream_t s) {
+  const SpmvChunk* ch = pat.chunks_ov.get() + (part_no == 1 ? 0 : pat.nch_int);
+  const int n = static_cast<int>(part_no == 1 ? pat.nch_int : pat.nchunks - pat.nch_int);
+  // an empty part still runs one CTA: its grid reduction passes the p.q on (part 1) or finishes it
+  k_spmv<true><<<std::max(1, spmv_grid(n)), kThreads, kStreamSmem, s>>>(ch, n, pat.sptr.get(), pat.tptr.get(),
+                                                                        pat.snbr.get(), pat.tlist.get(), vals, x_full,
+                                                                        own_off, y, st, part, part_no);
   FS_LAUNCH_CHECK();
 }
 

@@ -34,6 +34,7 @@ struct PcgState {
   unsigned long long spmv_t0;
   unsigned long long spmv_ns;
   unsigned long long spmv_cnt;
+  double pq_part;  // split SpMV (halo exchange overlap): p.q of the interior chunks
   // FSFEM_GAP_TIMING (tuning builds): end of the last SpMV, update kernel start / duration, gaps
   unsigned long long spmv_tend, upd_t0, upd_ns, gap_ns, upd_cnt;
   unsigned int upd_done;
@@ -175,6 +176,12 @@ int spmv_kind(const Pattern& pat);  // 0 small, 1 gather, 2 dataflow (pcg.cu)
 // kernel forms K_ij^T x_i from the own slice, PCG also the p.q partial).
 void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, int64_t own_off, double* y,
                  PcgState* st, double* part, bool pcg, cudaStream_t s);
+// Split PCG SpMV: part 1 = the chunks whose columns are all own rows (they need
+// no exchanged entry), part 2 = the others; p.q = part 1 + part 2 in that order (gather kernel).
+void launch_spmv_split(const Pattern& pat, int part_no, const double* vals, const double* x_full, int64_t own_off,
+                       double* y, PcgState* st, double* part, cudaStream_t s);
+// Interior/boundary chunk order for the split SpMV (once per pattern, row partitions).
+void build_overlap_chunks(Pattern& pat, cudaStream_t s);
 void launch_update(double* x, double* r, const double* p, const double* q, const double* dinv, int64_t n, PcgState* st,
                    double* part, cudaStream_t s);
 void launch_direction(double* p, const double* r, const double* dinv, int64_t n, PcgState* st, cudaStream_t s);

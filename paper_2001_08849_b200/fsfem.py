@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "TOPOLOGY", 3: "DEGENERATE", 4: "U
 METHOD_FS, METHOD_FEM_T4 = 0, 1
 
 EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_error", "fsfem_comm_init",
-           "fsfem_comm_init_loopback", "fsfem_get_partition", "fsfem_set_deterministic", "fsfem_set_loop", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
+           "fsfem_comm_init_loopback", "fsfem_get_partition", "fsfem_set_deterministic", "fsfem_set_loop", "fsfem_set_overlap", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
            "fsfem_surface_loads"]
@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_get_partition": (I, [P, P]),
         "fsfem_set_deterministic": (I, [P, I]),
         "fsfem_set_loop": (I, [P, I]),
+        "fsfem_set_overlap": (I, [P, I]),
         "fsfem_set_method": (I, [P, I]),
         "fsfem_set_reorder": (I, [P, I]),
         "fsfem_set_pcg_variant": (I, [P, I]),
@@ -184,6 +185,11 @@ def fsfem_get_partition(ctx, nranks: int) -> np.ndarray:
 def fsfem_set_loop(ctx, mode: int) -> None:
     """0: device-side while loop (default), 1: host-polled graph batches."""
     _raise(ctx, load_library().fsfem_set_loop(ctx, int(mode)))
+
+
+def fsfem_set_overlap(ctx, on: bool) -> None:
+    """Exchange of the search direction overlapped with the interior rows' SpMV (multi-rank)."""
+    _raise(ctx, load_library().fsfem_set_overlap(ctx, 1 if on else 0))
 
 
 def fsfem_set_deterministic(ctx, on: bool) -> None:
@@ -327,6 +333,9 @@ class FsFem:
 
     def set_loop(self, mode: int):
         fsfem_set_loop(self.ctx, mode)
+
+    def set_overlap(self, on: bool = True):
+        fsfem_set_overlap(self.ctx, on)
 
     def set_reorder(self, mode: int):
         fsfem_set_reorder(self.ctx, mode)

@@ -29,7 +29,7 @@ def lib():
     return P
 
 
-def solve_group(P, m, G, variant=0, exchange=0, det=False, rel_tol=1e-10):
+def solve_group(P, m, G, variant=0, exchange=0, det=False, rel_tol=1e-10, overlap=False):
     import torch
     stream = torch.cuda.Stream()
     gs = [P.FsFem(device=0, stream=stream.cuda_stream) for _ in range(G)]
@@ -43,6 +43,7 @@ def solve_group(P, m, G, variant=0, exchange=0, det=False, rel_tol=1e-10):
                 g.set_deterministic(True)
             g.set_exchange(exchange)
             g.set_pcg_variant(variant)
+            g.set_overlap(overlap)
             g.build_faces(m.xyz, m.tets)
             g.assemble_csr(E, NU)
             g.apply_bc(m.dirichlet, m.loads.reshape(-1))
@@ -95,6 +96,21 @@ def test_loopback_solve_matches_oracle_cfg3(lib, G, variant, exchange):
     assert np.linalg.norm(u - uo) <= 1e-7 * np.linalg.norm(uo)
     fixed = np.repeat(np.isin(np.arange(m.n_nodes), m.dirichlet), 3)
     assert np.all(u[fixed] == 0.0)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("variant,exchange", [(0, 0), (0, 1), (1, 0), (1, 1)],
+                         ids=["std-allgather", "std-halo", "single-allgather", "single-halo"])
+def test_loopback_overlap_matches_oracle_cfg3(lib, G, variant, exchange):
+    """f1 overlap: the exchange of the search direction on a side stream while the interior chunks
+    are multiplied, the boundary chunks after the join (fsfem_set_overlap)."""
+    m = config_mesh(3)
+    uo = np.load(os.path.join(GOLDEN, "oracle_cfg3_u.npy"))
+    u, rep, rng = solve_group(lib, m, G, variant, exchange, overlap=True)
+    assert rep["converged"] == 1 and rep["rel_residual"] <= 1e-10
+    assert np.linalg.norm(u - uo) <= 1e-7 * np.linalg.norm(uo)
+    u2, rep2, _ = solve_group(lib, m, G, variant, exchange, overlap=True)
+    assert np.array_equal(u, u2)  # the side stream does not make the result timing dependent
 
 
 def test_loopback_bitwise_reproducible(lib):

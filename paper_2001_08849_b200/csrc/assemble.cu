@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(256) k_tet_s(const double* __restrict__ xyz, c
 // Local domain order = ascending domain id.  Tasks are stored longest first (load balance; which
 // thread runs a task does not change its sum).
 // =============================================================================================
+#ifndef FSFEM_ASM_SPLIT
+#define FSFEM_ASM_SPLIT 1
+#endif
 constexpr int kTileRows = 16;
 constexpr int kMaxDom = 640;      // domains per tile (shared-memory s records: 120 B each)
 constexpr int kMaxVerts = 254;    // u8 local vertex ids, 255 = none
@@ -829,11 +832,28 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
           double o1[15], o2[15];
           domain_s<kTet>(X, fv + 5 * k, o1);
           domain_s<kTet>(X, fv + 5 * min(k2, h.ndom - 1), o2);
+#if FSFEM_ASM_SPLIT
+          // split record layout: (x, y) of s_K as one 16-B pair at SA[5 k + K], z at SB[5 k + K]
+          double2* SA = reinterpret_cast<double2*>(S);
+          double* SB = S + 10 * kMaxDom;
+#pragma unroll
+          for (int K = 0; K < 5; ++K) {
+            SA[5 * k + K] = make_double2(o1[3 * K], o1[3 * K + 1]);
+            SB[5 * k + K] = o1[3 * K + 2];
+          }
+          if (k2 < h.ndom)
+#pragma unroll
+            for (int K = 0; K < 5; ++K) {
+              SA[5 * k2 + K] = make_double2(o2[3 * K], o2[3 * K + 1]);
+              SB[5 * k2 + K] = o2[3 * K + 2];
+            }
+#else
 #pragma unroll
           for (int q = 0; q < 15; ++q) S[15 * k + q] = o1[q];
           if (k2 < h.ndom)
 #pragma unroll
             for (int q = 0; q < 15; ++q) S[15 * k2 + q] = o2[q];
+#endif
         }
       }
       // every producer is done reading X[b] before the next iteration gathers tile j + 2's
@@ -866,9 +886,18 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
           const int en = ent[e];
           const int code = en & 31;
           const int pi = code / 5, pj = code - 5 * pi;
+#if FSFEM_ASM_SPLIT
+          const double2* SA = reinterpret_cast<const double2*>(S);
+          const double* SB = S + 10 * kMaxDom;
+          const int kd = 5 * (en >> 5);
+          const double2 axy = SA[kd + pi], cxy = SA[kd + pj];
+          const double a0 = axy.x, a1 = axy.y, a2 = SB[kd + pi];
+          const double c0 = cxy.x, c1 = cxy.y, c2 = SB[kd + pj];
+#else
           const double* sd = S + 15 * (en >> 5);
           const double a0 = sd[3 * pi], a1 = sd[3 * pi + 1], a2 = sd[3 * pi + 2];
           const double c0 = sd[3 * pj], c1 = sd[3 * pj + 1], c2 = sd[3 * pj + 2];
+#endif
           M[0] = fma(a0, c0, M[0]);
           M[1] = fma(a0, c1, M[1]);
           M[2] = fma(a0, c2, M[2]);
@@ -884,8 +913,14 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
         for (int c = 0; c < tk.count; ++c, e += kDiagSplit) {
           const int en = ent[e];
           const int pi = (en & 31) / 6;  // code = 5 pi + pi
+#if FSFEM_ASM_SPLIT
+          const int kd = 5 * (en >> 5) + pi;
+          const double2 axy = reinterpret_cast<const double2*>(S)[kd];
+          const double a0 = axy.x, a1 = axy.y, a2 = (S + 10 * kMaxDom)[kd];
+#else
           const double* sd = S + 15 * (en >> 5) + 3 * pi;
           const double a0 = sd[0], a1 = sd[1], a2 = sd[2];
+#endif
           M[0] = fma(a0, a0, M[0]);
           M[1] = fma(a0, a1, M[1]);
           M[2] = fma(a0, a2, M[2]);

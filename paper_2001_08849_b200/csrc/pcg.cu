@@ -704,6 +704,9 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       if (j + kDfStages + 1 < K) nx = chunks[c + (kDfStages + 1) * gridDim.x];
       if (lane == 0) st_release_cta_s32(&sh_p1done, j + 1);  // -> counter warp
     }
+#ifdef FSFEM_DF_STREAMONLY
+  } else if (warp > kWarps) {  // timing experiment: no counting, no phase 2
+#endif
   } else if (warp == kWarps + 2) {
     // ---------------- counter warp: dependency counts, in batches ----------------
     // A gpu-scope fence costs microseconds under this load, so the warp takes every chunk whose
@@ -867,6 +870,15 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
     }
   } else {
     // ---------------- compute warps: P1 ----------------
+#ifdef FSFEM_DF_STREAMONLY
+    for (int j = 0; j < K; ++j) {  // timing experiment: consume the stages only
+      const int s = j % kDfStages;
+      mbar_wait(&full[s], (j / kDfStages) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (K >= 0) return;
+#endif
     constexpr int G = kGroupLanes, NPW = 32 / kGroupLanes;
     const int grp = lane / G, gl = lane % G;
     const int m = warp * NPW + grp;  // this group's node inside every chunk
@@ -900,7 +912,11 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
           xs[u] = 0.0;
           if (k < nus) {
             const int b = k / 3, cc = k - 3 * b;
+#ifdef FSFEM_DF_NOGATHER
+            xs[u] = static_cast<double>(sn[ls + b] & 7) + cc;  // timing experiment only (wrong product)
+#else
             xs[u] = ldg_vec(x + 3 * sn[ls + b] + cc, vpol);
+#endif
           }
         }
 #pragma unroll
@@ -914,7 +930,11 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
             s1 = fma(v1, xs[u], s1);
             s2 = fma(v2, xs[u], s2);
             const int tp = tq[ls + b];
+#ifndef FSFEM_DF_NOPUSH
             if (tp >= 0) tbuf[3 * static_cast<int64_t>(tp) + cc] = fma(v2, xi2, fma(v1, xi1, v0 * xi0));
+#else
+            if (tp == -7) tbuf[0] = v0 * xi0;  // timing experiment: no pushes (wrong product)
+#endif
           }
         }
       }

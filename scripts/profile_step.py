@@ -52,7 +52,11 @@ def main():
     for _ in range(a.solves - 1):
         fsfem_assemble_csr(g.ctx, 1.0e6, 0.3)
         fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
-        r = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)
+        try:
+            r = fsfem_pcg_solve(g.ctx, u, True, 1e-10, a.pcg_iters, allow_not_converged=True)
+        except Exception as e:  # tuning builds that skip work may break PCG: report the timings anyway
+            r = g.report()
+            print("solve error:", str(e)[:80])
         print(f"solve: {r['iterations']} it, {r['t_pcg_ms']:.3f} ms, {r['iterations'] / r['t_pcg_ms'] * 1e3:.0f} it/s, "
               f"spmv {r['t_spmv_ms'] / max(1, r['spmv_launches']) * 1e3:.2f} us (events), "
               f"{r['t_spmv_dev_ms'] / max(1, r['spmv_dev_launches']) * 1e3:.2f} us (device timer)")

@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       if (j + kDfStages + 1 < K) nx = chunks[c + (kDfStages + 1) * gridDim.x];
       if (lane == 0) st_release_cta_s32(&sh_p1done, j + 1);  // -> counter warp
     }
-#ifdef FSFEM_DF_STREAMONLY
+#if defined(FSFEM_DF_STREAMONLY) || defined(FSFEM_DF_P1ONLY)
   } else if (warp > kWarps) {  // timing experiment: no counting, no phase 2
 #endif
   } else if (warp == kWarps + 2) {

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -87,6 +88,29 @@ int num_sms() {
     if (g_sms <= 0) g_sms = 148;
   }
   return g_sms;
+}
+
+static long long now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+PhaseTimer::PhaseTimer(cudaStream_t st, const char* tg) : s(st), tag(tg), on(false), t0(0) {
+  static const int enabled = [] {
+    const char* e = std::getenv("FSFEM_PHASE_TIMES");
+    return e != nullptr && e[0] == '1' ? 1 : 0;
+  }();
+  on = enabled != 0;
+  if (on) {
+    cudaStreamSynchronize(s);
+    t0 = now_ns();
+  }
+}
+void PhaseTimer::mark(const char* name) {
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  const long long t = now_ns();
+  std::fprintf(stderr, "  [%s] %-28s %9.3f ms\n", tag, name, (t - t0) * 1e-6);
+  t0 = t;
 }
 
 // ---- NCCL, resolved at run time (torch has already loaded libnccl.so.2 in practice) ----
@@ -927,6 +951,7 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
                        c->face_opp, c->tet_face, &nf, &ni, c->h_flags);
     fsfem_status s = decode_flags(c, c->h_flags[0], "build_faces");
     if (s != FSFEM_OK) return s;
+    PhaseTimer pt(c->stream, "faces");
     // row partition: node ranges balanced by node-face incidences, aligned to
     // the deterministic dot chunk when that mode is on (every rank computes the same ranges)
     partition_ranges_device(c->face_nodes.get(), c->face_opp.get(), nf, n_nodes, c->nranks, c->det ? kDetChunkNodes : 32,
@@ -936,8 +961,10 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
     // Internal node order (reorder.cu): renumber in Morton order when the caller's numbering is
     // not banded (mean tet id span > 16 N^(2/3)), never with several ranks (the documented row
     // partition is in the caller's numbering).
+    pt.mark("partition ranges");
     c->span_tmp.ensure(1);
     c->mean_span = mean_tet_span_device(c->tets.get(), n_tets, c->span_tmp.get(), c->stream);
+    pt.mark("mean tet span");
     const bool want = c->nranks == 1 &&
                       (c->reorder_mode == 1 ||
                        (c->reorder_mode == 0 && c->mean_span > 16.0 * std::pow(static_cast<double>(n_nodes), 2.0 / 3.0)));

@@ -1006,7 +1006,9 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
   DevBuf<int32_t>& inv = pat.tile_tmp;
   order.ensure(nloc);
   inv.ensure(nloc);
+  PhaseTimer pt(s, "tiles");
   morton_order_device(xyz + 3 * pat.n_lo, nloc, order.get(), inv.get(), scratch, s);
+  pt.mark("morton order");
   std::vector<int32_t> ts;
   for (int64_t a = 0; a < nloc; a += kTileRows) ts.push_back(static_cast<int32_t>(a));
   ts.push_back(static_cast<int32_t>(nloc));
@@ -1035,6 +1037,7 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
     sz.resize(nt);
     FS_CUDA(cudaMemcpyAsync(sz.data(), pat.tile_bytes.get(), sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
+    pt.mark("tile build + D2H sizes");
     std::vector<int32_t> nts;
     bool split = false;
     for (int64_t k = 0; k < nt; ++k) {
@@ -1061,6 +1064,7 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
     tot += sz[k];
     mx = std::max(mx, sz[k]);
   }
+  pt.mark("host tile sizes");
   pat.ntiles = nt;
   pat.tile_blob_max = mx;
   pat.tile_blob_bytes = tot;

@@ -87,6 +87,17 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Launch-shape helper: number of SMs of the current device (cached by the context).
 int num_sms();
 
+// Host phase timer for the cold path (FSFEM_PHASE_TIMES=1: every mark synchronises the stream
+// and prints the wall time since the previous mark to stderr; otherwise a no-op).
+struct PhaseTimer {
+  cudaStream_t s;
+  const char* tag;
+  bool on;
+  long long t0;
+  PhaseTimer(cudaStream_t st, const char* tg);
+  void mark(const char* name);
+};
+
 // ---- scan / reduce primitives (scan.cu) ----
 // Exclusive prefix sum of in[0..n) into out[0..n], out[n] = total.  Deterministic.
 void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t s, void* tmp, size_t tmp_bytes);

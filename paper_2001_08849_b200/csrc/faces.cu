@@ -352,6 +352,7 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   FS_CUDA(cudaMemsetAsync(cur, 0, sizeof(int32_t) * (nn + 1), s));
   FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
   FS_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(unsigned long long) * 3, s));
+  PhaseTimer pt(s, "faces");
 
   const int nbb = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(1, ceil_div(nn, 256))));
   k_bbox_partial<<<nbb, 256, 0, s>>>(d_xyz, nn, bbp);
@@ -364,6 +365,7 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   // errors (ids out of range) must stop here: the scatter would index out of bounds
   FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
+  pt.mark("bbox + count + D2H");
   if (h_flags[0] != kNoError) return;  // caller decodes
   exclusive_scan_i32(cnt, off, nn, s, tmp, tmp_bytes);
   k_face_scatter<<<grid_t, 256, 0, s>>>(reinterpret_cast<const int4*>(d_tets), nt, off, cur, keys, pay);
@@ -374,6 +376,7 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   FS_LAUNCH_CHECK();
   FS_CUDA(cudaMemcpyAsync(h_flags + 2, flags + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
+  pt.mark("scan + scatter + bucket sort");
   const int n_big = static_cast<int>(h_flags[2] & 0xffffffffu);
   if (n_big > 0) {
     const size_t smem = (2 * sizeof(unsigned long long) + 2 * sizeof(uint32_t)) * kBigCap;
@@ -386,6 +389,7 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   int32_t nf32 = 0;
   FS_CUDA(cudaMemcpyAsync(&nf32, foff + nn, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
+  pt.mark("big buckets + scan + D2H");
   if (h_flags[0] != kNoError) return;
   const int64_t nf = nf32;
   face_nodes.ensure(3 * nf);
@@ -397,6 +401,7 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   FS_LAUNCH_CHECK();
   FS_CUDA(cudaMemcpyAsync(h_flags + 1, flags + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
+  pt.mark("emit");
   *n_faces = nf;
   *n_interior = static_cast<int64_t>(h_flags[1]);
 }

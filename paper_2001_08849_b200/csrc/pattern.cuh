@@ -37,7 +37,6 @@ struct Pattern {
   int64_t nsb = 0;   // stored blocks
   int64_t ntb = 0;   // transposed (gathered) blocks
   int64_t nfi = 0;   // node-face incidences (sum over own nodes of |F(i)|)
-  int64_t max_row_blocks = 0;  // max stored blocks of one row
   DevBuf<int64_t> node_ptr;  // [nloc+1] full neighbour list offsets
   DevBuf<int32_t> nbr;       // [nblk] sorted neighbour node ids of every own node
   DevBuf<int64_t> sptr;      // [nloc+1] stored block offsets
@@ -62,6 +61,7 @@ struct Pattern {
   bool df_ok = false;        // every chunk's producer list fits kMaxDeps
   DevBuf<int32_t> dep_ptr;   // [nchunks + 1]
   DevBuf<int2> dep_list;     // [dep_ptr[nchunks]] (chunk d, need[d])
+  DevBuf<int2> dep_tmp;      // [nchunks * (kMaxDeps + 1)] unsorted lists (symbolic scratch)
   // split SpMV (halo overlap): the chunks reordered interior first, nch_int of them interior
   bool have_ov = false;
   int64_t nch_int = 0;

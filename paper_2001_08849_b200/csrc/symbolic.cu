@@ -21,6 +21,7 @@ namespace {
 constexpr int kPatWarps = 4;
 constexpr int kMaxTetsPerNode = 128;                 // UNSUPPORTED beyond (general meshes: ~20-60)
 constexpr int kCandCap = 8 * kMaxTetsPerNode;        // node candidates per node
+constexpr int kPadDeg = 64;  // padded pattern lists of pass 1 (longer lists: a second pattern pass)
 constexpr int kSentinel = 0x7fffffff;
 
 __global__ void k_count_node_tets(const int32_t* __restrict__ tets, int64_t nt4, int64_t n_lo, int64_t n_hi,
@@ -90,7 +91,8 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
     const int32_t* __restrict__ face_opp, const int32_t* __restrict__ nt_ptr, const int32_t* __restrict__ nt_idx,
     int64_t n_lo, int64_t nloc, int32_t* __restrict__ deg, int32_t* __restrict__ nfc,
     const int64_t* __restrict__ node_ptr, const int64_t* __restrict__ nf_ptr, int32_t* __restrict__ nbr,
-    int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err, int fem) {
+    int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err, int fem,
+    int32_t* __restrict__ pad_nbr, int32_t* __restrict__ pad_nf, int* __restrict__ pad_over) {
   __shared__ int32_t cand[kPatWarps][kCandCap], tmp[kPatWarps][kCandCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t il = blockIdx.x * (int64_t)kPatWarps + w; il < nloc; il += (int64_t)gridDim.x * kPatWarps) {
@@ -121,6 +123,13 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
     const int dn = warp_sort_unique(cand[w], tmp[w], 8 * ntet, lane);
     if (!kWrite) {
       if (lane == 0) deg[il] = dn;
+      if (pad_nbr != nullptr) {  // the sorted list at a fixed stride: pass 2 becomes a copy
+        if (dn > kPadDeg) {
+          if (lane == 0) *pad_over = 1;
+        } else {
+          for (int k = lane; k < dn; k += 32) pad_nbr[il * kPadDeg + k] = cand[w][k];
+        }
+      }
     } else {
       const int64_t P = node_ptr[il];
       const int32_t self = static_cast<int32_t>(n_lo + il);
@@ -148,11 +157,38 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
     }
     if (!kWrite) {
       if (lane == 0) nfc[il] = fn;
+      if (pad_nf != nullptr) {
+        if (fn > kPadDeg) {
+          if (lane == 0) *pad_over = 1;
+        } else {
+          for (int k = lane; k < fn; k += 32) pad_nf[il * kPadDeg + k] = cand[w][k];
+        }
+      }
     } else {
       const int64_t Q = nf_ptr[il];
       for (int k = lane; k < fn; k += 32) nf_idx[Q + k] = cand[w][k];
     }
     __syncwarp();
+  }
+}
+
+// Pass 2 from the padded lists of pass 1: warp per node, copy to the packed offsets.
+__global__ void k_pattern_compact(const int32_t* __restrict__ pad_nbr, const int32_t* __restrict__ pad_nf,
+                                  int64_t n_lo, int64_t nloc, const int64_t* __restrict__ node_ptr,
+                                  const int64_t* __restrict__ nf_ptr, int32_t* __restrict__ nbr,
+                                  int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t il = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); il < nloc; il += nwarp) {
+    const int64_t P = node_ptr[il], dn = node_ptr[il + 1] - P;
+    const int32_t self = static_cast<int32_t>(n_lo + il);
+    for (int k = lane; k < dn; k += 32) {
+      const int32_t j = pad_nbr[il * kPadDeg + k];
+      nbr[P + k] = j;
+      if (j == self) diag_slot[il] = k;
+    }
+    const int64_t Q = nf_ptr[il], fn = nf_ptr[il + 1] - Q;
+    for (int k = lane; k < fn; k += 32) nf_idx[Q + k] = pad_nf[il * kPadDeg + k];
   }
 }
 
@@ -286,6 +322,96 @@ __global__ void __launch_bounds__(kDepWarps * 32) k_chunk_deps(const SpmvChunk* 
   }
 }
 
+// SpMV streaming chunks (pattern.cuh), built on the device: windows of kChunkNodes own nodes
+// (aligned to the rank's first node); a window whose stored or transposed block count exceeds
+// kCapBlocks is cut greedily into runs that fit (high-valence rows).  out == nullptr: count only.
+// Returns -1 when one node alone exceeds kCapBlocks.
+__device__ int window_chunks(const int64_t* __restrict__ sptr, const int64_t* __restrict__ tptr, int64_t a, int64_t b,
+                             SpmvChunk* out, int64_t* bad_node) {
+  int n = 0;
+  for (int64_t n0 = a; n0 < b;) {
+    int64_t n1 = n0;
+    while (n1 < b && sptr[n1 + 1] - sptr[n0] <= kCapBlocks && tptr[n1 + 1] - tptr[n0] <= kCapBlocks) ++n1;
+    if (n1 == n0) {
+      *bad_node = n0;
+      return -1;
+    }
+    if (out)
+      out[n] = SpmvChunk{static_cast<int32_t>(n0), static_cast<int32_t>(n1), static_cast<int32_t>(sptr[n0]),
+                         static_cast<int32_t>(sptr[n1]), static_cast<int32_t>(tptr[n0]), static_cast<int32_t>(tptr[n1]),
+                         0, 0};
+    ++n;
+    n0 = n1;
+  }
+  return n;
+}
+
+__global__ void k_chunk_count(const int64_t* __restrict__ sptr, const int64_t* __restrict__ tptr, int64_t nloc,
+                              int64_t n_lo, int32_t* __restrict__ cnt, unsigned long long* __restrict__ err) {
+  const int64_t nw = (nloc + kChunkNodes - 1) / kChunkNodes;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t bad = 0;
+    const int n = window_chunks(sptr, tptr, w * kChunkNodes, min(nloc, (w + 1) * kChunkNodes), nullptr, &bad);
+    if (n < 0) report_error(err, FSFEM_ERR_UNSUPPORTED, n_lo + bad);
+    cnt[w] = max(n, 0);
+  }
+}
+
+__global__ void k_chunk_emit(const int64_t* __restrict__ sptr, const int64_t* __restrict__ tptr, int64_t nloc,
+                             const int32_t* __restrict__ off, SpmvChunk* __restrict__ chunks) {
+  const int64_t nw = (nloc + kChunkNodes - 1) / kChunkNodes;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t bad = 0;
+    window_chunks(sptr, tptr, w * kChunkNodes, min(nloc, (w + 1) * kChunkNodes), chunks + off[w], &bad);
+  }
+}
+
+// Reverse producer lists of the dataflow SpMV: for every chunk d the chunks c that need it (d
+// itself and every c with d among its producers), each with its need ndeps[c] + 1, ascending c.
+// A chunk with more than kMaxDeps producers (ndeps = -1) disables the dataflow kernel (*bad).
+__global__ void k_rdeps_count(const int32_t* __restrict__ ndeps, const int32_t* __restrict__ deps, int nch,
+                              int32_t* __restrict__ cnt, unsigned long long* __restrict__ bad) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += gridDim.x * blockDim.x) {
+    const int nd = ndeps[c];
+    if (nd < 0) {
+      atomicExch(bad, 1ull);
+      continue;
+    }
+    atomicAdd(cnt + c, 1);
+    for (int k = 0; k < nd; ++k) atomicAdd(cnt + deps[static_cast<int64_t>(c) * kMaxDeps + k], 1);
+  }
+}
+
+__global__ void k_rdeps_fill(const int32_t* __restrict__ ndeps, const int32_t* __restrict__ deps, int nch,
+                             const int32_t* __restrict__ ptr, int32_t* __restrict__ cur, int2* __restrict__ tmp) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += gridDim.x * blockDim.x) {
+    const int nd = ndeps[c];
+    if (nd < 0) continue;
+    const int2 e = make_int2(c, nd + 1);
+    tmp[ptr[c] + atomicAdd(cur + c, 1)] = e;
+    for (int k = 0; k < nd; ++k) {
+      const int d = deps[static_cast<int64_t>(c) * kMaxDeps + k];
+      tmp[ptr[d] + atomicAdd(cur + d, 1)] = e;
+    }
+  }
+}
+
+// Warp per list: rank by consumer chunk (distinct within a list) into the final order.
+__global__ void k_rdeps_sort(const int32_t* __restrict__ ptr, int nch, const int2* __restrict__ tmp,
+                             int2* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t d = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); d < nch; d += nwarp) {
+    const int a = ptr[d], n = ptr[d + 1] - a;
+    for (int i = lane; i < n; i += 32) {
+      const int2 e = tmp[a + i];
+      int r = 0;
+      for (int j = 0; j < n; ++j) r += tmp[a + j].x < e.x ? 1 : 0;
+      list[a + r] = e;
+    }
+  }
+}
+
 // Expand the symmetric block storage to the public CSR (row_ptr int64, col_idx int32, vals):
 // row 3i+a lists columns 3j+c for j in nbr(i) ascending.  In nbr order a row is
 // [halo stored (j < n_lo)] [transposed (n_lo <= j < i)] [stored j >= i]; the diagonal is the
@@ -362,6 +488,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   const size_t o_nfc = carve(sizeof(int32_t) * (nloc + 1));
   const size_t o_flags = carve(sizeof(unsigned long long) * 2);
   const size_t o_tmp = carve(scan_tmp_bytes(nloc + 1));
+  const size_t o_pad = carve(sizeof(int32_t) * 2 * kPadDeg * std::max<int64_t>(nloc, 1) + 16);
   unsigned char* base = scratch.ensure(o);
   int32_t* cnt = reinterpret_cast<int32_t*>(base + o_cnt);
   int32_t* ptr = reinterpret_cast<int32_t*>(base + o_ptr);
@@ -372,10 +499,15 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(base + o_flags);
   void* tmp = base + o_tmp;
   const size_t tb = scan_tmp_bytes(nloc + 1);
+  int32_t* pad_nbr = reinterpret_cast<int32_t*>(base + o_pad);
+  int32_t* pad_nf = pad_nbr + kPadDeg * nloc;
+  int* pad_over = reinterpret_cast<int*>(pad_nf + kPadDeg * nloc);
 
+  PhaseTimer pt(s, "symbolic");
   FS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nloc + 1), s));
   FS_CUDA(cudaMemsetAsync(cur, 0, sizeof(int32_t) * (nloc + 1), s));
   FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
+  FS_CUDA(cudaMemsetAsync(pad_over, 0, sizeof(int), s));
   const int g4 = static_cast<int>(std::min<int64_t>(ceil_div(4 * nt, 256), 8LL * sms));
   k_count_node_tets<<<g4, 256, 0, s>>>(d_tets, 4 * nt, n_lo, n_lo + nloc, cnt);
   FS_LAUNCH_CHECK();
@@ -385,8 +517,10 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   const int gw = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kPatWarps), 32LL * sms)));
   k_sort_segments<<<gw, kPatWarps * 32, 0, s>>>(ptr, nloc, idx, flags);
   FS_LAUNCH_CHECK();
+  pt.mark("node tets");
   k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc, deg,
-                                                      nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags, fem);
+                                                      nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags, fem,
+                                                      pad_nbr, pad_nf, pad_over);
   FS_LAUNCH_CHECK();
   node_ptr.ensure(nloc + 1);
   nf_ptr.ensure(nloc + 1);
@@ -396,17 +530,27 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   FS_CUDA(cudaMemcpyAsync(&tot[0], node_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaMemcpyAsync(&tot[1], nf_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  int h_over = 0;
+  FS_CUDA(cudaMemcpyAsync(&h_over, pad_over, sizeof(int), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
+  pt.mark("pattern count + scans");
   if (h_flags[0] != kNoError) return;
   pat.nblk = tot[0];
   pat.nfi = tot[1];
   nbr.ensure(tot[0]);
   nf_idx.ensure(tot[1]);
   diag_slot.ensure(nloc);
-  k_node_pattern<true><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc,
-                                                     nullptr, nullptr, node_ptr.get(), nf_ptr.get(), nbr.get(),
-                                                     nf_idx.get(), diag_slot.get(), flags, fem);
+  if (h_over == 0) {
+    k_pattern_compact<<<gw, kPatWarps * 32, 0, s>>>(pad_nbr, pad_nf, n_lo, nloc, node_ptr.get(), nf_ptr.get(), nbr.get(),
+                                                    nf_idx.get(), diag_slot.get());
+  } else {
+    k_node_pattern<true><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc,
+                                                       nullptr, nullptr, node_ptr.get(), nf_ptr.get(), nbr.get(),
+                                                       nf_idx.get(), diag_slot.get(), flags, fem, nullptr, nullptr,
+                                                       nullptr);
+  }
   FS_LAUNCH_CHECK();
+  pt.mark("pattern write");
   // symmetric split (pattern.cuh): deg and nfc are free again, reuse them as counters
   const int gt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 8LL * sms)));
   k_split_count<<<gt, 256, 0, s>>>(node_ptr.get(), nbr.get(), n_lo, nloc, deg, nfc);
@@ -429,35 +573,23 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   k_split_trans<<<gt, 256, 0, s>>>(node_ptr.get(), nbr.get(), n_lo, nloc, pat.sptr.get(), pat.snbr.get(),
                                    pat.tptr.get(), pat.tlist.get(), flags);
   FS_LAUNCH_CHECK();
+  // SpMV streaming chunks (pattern.cuh): windows of kChunkNodes nodes, split where a window's
+  // stored or transposed block count exceeds kCapBlocks
+  const int64_t nw = ceil_div(nloc, kChunkNodes);
+  const int gc = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nw, 256), 8LL * sms)));
+  k_chunk_count<<<gc, 256, 0, s>>>(pat.sptr.get(), pat.tptr.get(), nloc, n_lo, deg, flags);
+  FS_LAUNCH_CHECK();
+  exclusive_scan_i32(deg, nfc, nw, s, tmp, tb);
+  int32_t nch32 = 0;
   FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  // SpMV streaming chunks (pattern.cuh): greedy runs of <= kChunkNodes nodes whose stored and
-  // transposed block counts fit kCapBlocks.  Host side, once per pattern.
-  std::vector<int64_t> hs(nloc + 1), ht(nloc + 1);
-  FS_CUDA(cudaMemcpyAsync(hs.data(), pat.sptr.get(), sizeof(int64_t) * (nloc + 1), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaMemcpyAsync(ht.data(), pat.tptr.get(), sizeof(int64_t) * (nloc + 1), cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(&nch32, nfc + nw, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
+  pt.mark("split + chunk count");
   if (h_flags[0] != kNoError) return;
-  pat.max_row_blocks = 0;
-  for (int64_t i = 0; i < nloc; ++i) pat.max_row_blocks = std::max<int64_t>(pat.max_row_blocks, hs[i + 1] - hs[i]);
-  std::vector<SpmvChunk> ch;
-  ch.reserve(nloc / kChunkNodes + 1);
-  for (int64_t n0 = 0; n0 < nloc;) {
-    int64_t n1 = n0;
-    while (n1 < nloc && n1 - n0 < kChunkNodes && hs[n1 + 1] - hs[n0] <= kCapBlocks && ht[n1 + 1] - ht[n0] <= kCapBlocks)
-      ++n1;
-    if (n1 == n0) {  // one node with more than kCapBlocks blocks
-      h_flags[0] = (static_cast<unsigned long long>(FSFEM_ERR_UNSUPPORTED) << 56) | static_cast<unsigned long long>(n_lo + n0);
-      return;
-    }
-    ch.push_back(SpmvChunk{static_cast<int32_t>(n0), static_cast<int32_t>(n1), static_cast<int32_t>(hs[n0]),
-                           static_cast<int32_t>(hs[n1]), static_cast<int32_t>(ht[n0]), static_cast<int32_t>(ht[n1]), 0,
-                           0});
-    n0 = n1;
-  }
-  pat.nchunks = static_cast<int64_t>(ch.size());
-  pat.chunks.ensure(std::max<size_t>(ch.size(), 1));
-  if (!ch.empty())
-    FS_CUDA(cudaMemcpyAsync(pat.chunks.get(), ch.data(), sizeof(SpmvChunk) * ch.size(), cudaMemcpyHostToDevice, s));
+  pat.nchunks = nch32;
+  pat.chunks.ensure(std::max<int64_t>(pat.nchunks, 1));
+  k_chunk_emit<<<gc, 256, 0, s>>>(pat.sptr.get(), pat.tptr.get(), nloc, nfc, pat.chunks.get());
+  FS_LAUNCH_CHECK();
   // push SpMV: slots of the stored blocks, per-chunk producer lists, fresh flags and epoch
   pat.tpos.ensure(pat.nsb + 4);
   pat.tbuf.ensure(3 * pat.ntb + 2);
@@ -473,48 +605,36 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
     k_tpos<<<gp, 256, 0, s>>>(pat.tlist.get(), pat.ntb, pat.tpos.get());
     FS_LAUNCH_CHECK();
   }
+  pat.df_ok = false;
   if (pat.nchunks > 0) {
+    const int nch = static_cast<int>(pat.nchunks);
     const int gd = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pat.nchunks, kDepWarps), 16LL * sms)));
-    k_chunk_deps<<<gd, kDepWarps * 32, 0, s>>>(pat.chunks.get(), static_cast<int>(pat.nchunks), pat.tlist.get(), n_lo,
-                                               pat.deps.get(), pat.ndeps.get());
+    k_chunk_deps<<<gd, kDepWarps * 32, 0, s>>>(pat.chunks.get(), nch, pat.tlist.get(), n_lo, pat.deps.get(),
+                                               pat.ndeps.get());
     FS_LAUNCH_CHECK();
-    // reverse lists for the dataflow SpMV (host, once per pattern)
-    const int64_t nch = pat.nchunks;
-    std::vector<int32_t> hnd(nch), hdeps(nch * kMaxDeps);
-    FS_CUDA(cudaMemcpyAsync(hnd.data(), pat.ndeps.get(), sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
-    FS_CUDA(cudaMemcpyAsync(hdeps.data(), pat.deps.get(), sizeof(int32_t) * nch * kMaxDeps, cudaMemcpyDeviceToHost, s));
+    // reverse lists for the dataflow SpMV (deg / nfc reused as counters)
+    const int gr = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pat.nchunks, 256), 8LL * sms)));
+    FS_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * (nch + 1), s));
+    FS_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(unsigned long long), s));
+    k_rdeps_count<<<gr, 256, 0, s>>>(pat.ndeps.get(), pat.deps.get(), nch, deg, flags + 1);
+    FS_LAUNCH_CHECK();
+    pat.dep_ptr.ensure(nch + 1);
+    exclusive_scan_i32(deg, pat.dep_ptr.get(), nch, s, tmp, tb);
+    const int64_t cap = static_cast<int64_t>(nch) * (kMaxDeps + 1);
+    pat.dep_list.ensure(cap);
+    pat.dep_tmp.ensure(cap);
+    FS_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * (nch + 1), s));
+    k_rdeps_fill<<<gr, 256, 0, s>>>(pat.ndeps.get(), pat.deps.get(), nch, pat.dep_ptr.get(), deg, pat.dep_tmp.get());
+    FS_LAUNCH_CHECK();
+    k_rdeps_sort<<<gd, kDepWarps * 32, 0, s>>>(pat.dep_ptr.get(), nch, pat.dep_tmp.get(), pat.dep_list.get());
+    FS_LAUNCH_CHECK();
+    pat.cnt.ensure(nch);
+    pat.dotc.ensure(nch);
+    FS_CUDA(cudaMemsetAsync(pat.cnt.get(), 0, sizeof(uint32_t) * nch, s));
+    FS_CUDA(cudaMemcpyAsync(h_flags + 3, flags + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
-    pat.df_ok = true;
-    std::vector<int32_t> hneed(nch), hptr(nch + 1, 0);
-    for (int64_t c = 0; c < nch; ++c) {
-      if (hnd[c] < 0) {
-        pat.df_ok = false;
-        break;
-      }
-      hneed[c] = hnd[c] + 1;
-      hptr[c + 1] += 1;  // c needs itself
-      for (int k = 0; k < hnd[c]; ++k) hptr[hdeps[c * kMaxDeps + k] + 1] += 1;
-    }
-    if (pat.df_ok) {
-      for (int64_t c = 0; c < nch; ++c) hptr[c + 1] += hptr[c];
-      std::vector<int2> hlist(hptr[nch]);
-      std::vector<int32_t> fill(hptr.begin(), hptr.end() - 1);
-      for (int64_t c = 0; c < nch; ++c) hlist[fill[c]++] = make_int2(static_cast<int32_t>(c), hneed[c]);
-      for (int64_t c = 0; c < nch; ++c)
-        for (int k = 0; k < hnd[c]; ++k) {
-          const int32_t d = hdeps[c * kMaxDeps + k];
-          hlist[fill[d]++] = make_int2(static_cast<int32_t>(c), hneed[c]);
-        }
-      pat.dep_ptr.ensure(nch + 1);
-      pat.dep_list.ensure(std::max<size_t>(hlist.size(), 1));
-      pat.cnt.ensure(nch);
-      pat.dotc.ensure(nch);
-      FS_CUDA(cudaMemcpyAsync(pat.dep_ptr.get(), hptr.data(), sizeof(int32_t) * (nch + 1), cudaMemcpyHostToDevice, s));
-      FS_CUDA(cudaMemcpyAsync(pat.dep_list.get(), hlist.data(), sizeof(int2) * hlist.size(), cudaMemcpyHostToDevice,
-                              s));
-      FS_CUDA(cudaMemsetAsync(pat.cnt.get(), 0, sizeof(uint32_t) * nch, s));
-      FS_CUDA(cudaStreamSynchronize(s));
-    }
+    pat.df_ok = h_flags[3] == 0;
+    pt.mark("chunks + tpos + deps");
   }
   FS_CUDA(cudaStreamSynchronize(s));
 }

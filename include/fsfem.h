@@ -259,6 +259,20 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* ctx, double* u, int u0_is_zero, double r
 fsfem_status fsfem_recover_stress(fsfem_ctx* ctx, const double* u, double* strain, double* stress,
                                   double* node_stress, double* node_vm, int64_t* n_domains);
 
+/* Debug export of the dense stiffness of smoothing domains (Eq. 9
+ * summand V_k Bbar_k^T c Bbar_k with Bbar_k of Eq. 7, 15x15 for an interior face and 12x12 for an
+ * exterior one, Eq. 12; FEM-T4: V_e B_e^T c B_e of a tet), computed on the
+ * device with the assembly's own arithmetic (same s vectors and M-form blocks as fsfem_assemble_csr).
+ *   ids [n, host]: domain ids -- face ids in fsfem_get_faces order (FS-FEM) or tet ids (FEM-T4);
+ *   K [n*225, host]: row-major 15x15 per domain, row / column 3I+a for field position I (faces:
+ *     face nodes a < b < c, then the opposite vertices of face_tet[0] and face_tet[1]; tets: the 4
+ *     nodes in the caller's tet order) and component a; rows / columns of an absent position
+ *     (exterior face: 5th, tet: 5th) are 0;
+ *   field [n*5, host] (may be NULL): the field node ids in the caller's numbering, -1 absent.
+ * Needs assemble_csr (uses its E, nu and method).  Errors: STATE, INVALID_ARG (null K or ids with
+ * n > 0, n < 0, an id out of range). */
+fsfem_status fsfem_domain_stiffness(fsfem_ctx* ctx, const int64_t* ids, int64_t n, double* K, int32_t* field);
+
 /* Nodal loads of a surface traction ("the nodal load is calculated"; 496-499: the
  * §4.1 beam's uniform pressure on its upper face).  node_flag [n_nodes] (bytes,
  * nonzero = on the loaded surface), traction [3, host] in N/m^2: every exterior face whose three

@@ -51,6 +51,8 @@ def lib():
             "ora_face_domain": (I32, [P, I64, P, P, P, P, P]),
             "ora_assemble_fs": (I32, [P, D, D, I64, I64]),
             "ora_assemble_fem": (I32, [P, D, D, I64, I64]),
+            "ora_face_stiffness": (I32, [P, I64, D, D, P, P]),
+            "ora_tet_stiffness": (I32, [P, I64, D, D, P, P]),
             "ora_csr_dims": (None, [P, P, P, P]),
             "ora_last_coo_count": (I64, [P]),
             "ora_set_csr": (I32, [P, I64, P, P, P]),
@@ -130,6 +132,14 @@ class Oracle:
         self._check(lib().ora_face_domain(self._h, f, _p(field), _p(bbar), ctypes.byref(Vf), ctypes.byref(P),
                                           _p(tri)))
         return dict(field=field, bbar=bbar, Vf=Vf.value, P=P.value, tri=tri[:P.value].copy())
+
+    def domain_stiffness(self, k: int, E: float, nu: float, tet: bool = False):
+        """K7: dense 15x15 stiffness of face k (FS-FEM) or tet k (FEM-T4) and its field nodes."""
+        K = np.empty((15, 15), np.float64)
+        field = np.empty(5, np.int32)
+        fn = lib().ora_tet_stiffness if tet else lib().ora_face_stiffness
+        self._check(fn(self._h, k, E, nu, _p(K), _p(field)))
+        return K, field
 
     def _csr(self):
         lo, nr, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -485,6 +485,44 @@ int ora_assemble_fs(ora_mesh* m, double E, double nu, int64_t node_lo, int64_t n
   return 0;
 }
 
+// FEM-T4 gradients of tet t: b[I] = grad N_I, *V = |Eq. 10 volume|.
+static void tet_gradients(const ora_mesh* m, int64_t t, double b[4][3], double* V) {
+  const int32_t* v = &m->tets[4 * t];
+  // Linear shape functions N_I = (a_I + b_I x + c_I y + d_I z): the coefficient vectors are
+  // the columns of inv([[1 x y z] per node]); gradients (b_I, c_I, d_I) via cofactors.
+  V3 X[4];
+  for (int I = 0; I < 4; ++I) X[I] = node(m, v[I]);
+  double Mx[4][4];
+  for (int I = 0; I < 4; ++I) {
+    Mx[I][0] = 1.0;
+    Mx[I][1] = X[I].x;
+    Mx[I][2] = X[I].y;
+    Mx[I][3] = X[I].z;
+  }
+  // det(Mx) with columns (1, x, y, z) = -(Eq. 10 determinant with columns (x, y, z, 1)).
+  const double V6 = -6.0 * eq10_volume(X[0], X[1], X[2], X[3]);
+  for (int I = 0; I < 4; ++I)
+    for (int h = 0; h < 3; ++h) {
+      // inverse(Mx)[1+h][I] = cofactor(I, 1+h) / det
+      double sub3[3][3];
+      int r = 0;
+      for (int rr = 0; rr < 4; ++rr) {
+        if (rr == I) continue;
+        int cc2 = 0;
+        for (int cc = 0; cc < 4; ++cc) {
+          if (cc == 1 + h) continue;
+          sub3[r][cc2++] = Mx[rr][cc];
+        }
+        ++r;
+      }
+      const double minor = det3(sub3[0][0], sub3[0][1], sub3[0][2], sub3[1][0], sub3[1][1], sub3[1][2],
+                                sub3[2][0], sub3[2][1], sub3[2][2]);
+      const double sign = ((I + 1 + h) % 2 == 0) ? 1.0 : -1.0;
+      b[I][h] = sign * minor / V6;
+    }
+  *V = std::fabs(V6) / 6.0;
+}
+
 int ora_assemble_fem(ora_mesh* m, double E, double nu, int64_t node_lo, int64_t node_hi) {
   if (!(E > 0.0) || !(nu > -1.0 && nu < 0.5)) return fail(m, 1, "material out of range");
   if (node_lo < 0 || node_hi > m->nn || node_lo >= node_hi) return fail(m, 1, "bad node range");
@@ -498,40 +536,9 @@ int ora_assemble_fem(ora_mesh* m, double E, double nu, int64_t node_lo, int64_t 
     for (int I = 0; I < 4; ++I)
       if (v[I] >= node_lo && v[I] < node_hi) any = true;
     if (!any) continue;
-    // Linear shape functions N_I = (a_I + b_I x + c_I y + d_I z): the coefficient vectors are
-    // the columns of inv([[1 x y z] per node]); gradients (b_I, c_I, d_I) via cofactors.
-    V3 X[4];
-    for (int I = 0; I < 4; ++I) X[I] = node(m, v[I]);
-    double Mx[4][4];
-    for (int I = 0; I < 4; ++I) {
-      Mx[I][0] = 1.0;
-      Mx[I][1] = X[I].x;
-      Mx[I][2] = X[I].y;
-      Mx[I][3] = X[I].z;
-    }
-    // det(Mx) with columns (1, x, y, z) = -(Eq. 10 determinant with columns (x, y, z, 1)).
-    const double V6 = -6.0 * eq10_volume(X[0], X[1], X[2], X[3]);
-    double b[4][3];
-    for (int I = 0; I < 4; ++I)
-      for (int h = 0; h < 3; ++h) {
-        // inverse(Mx)[1+h][I] = cofactor(I, 1+h) / det
-        double sub3[3][3];
-        int r = 0;
-        for (int rr = 0; rr < 4; ++rr) {
-          if (rr == I) continue;
-          int cc2 = 0;
-          for (int cc = 0; cc < 4; ++cc) {
-            if (cc == 1 + h) continue;
-            sub3[r][cc2++] = Mx[rr][cc];
-          }
-          ++r;
-        }
-        const double minor = det3(sub3[0][0], sub3[0][1], sub3[0][2], sub3[1][0], sub3[1][1], sub3[1][2],
-                                  sub3[2][0], sub3[2][1], sub3[2][2]);
-        const double sign = ((I + 1 + h) % 2 == 0) ? 1.0 : -1.0;
-        b[I][h] = sign * minor / V6;
-      }
-    dense_stiffness(4, b, std::fabs(V6) / 6.0, c, Ke);
+    double b[4][3], Ve;
+    tet_gradients(m, t, b, &Ve);
+    dense_stiffness(4, b, Ve, c, Ke);
     for (int i = 0; i < 12; ++i) {
       if (v[i / 3] < node_lo || v[i / 3] >= node_hi) continue;
       const int64_t gi = 3 * static_cast<int64_t>(v[i / 3]) + i % 3;
@@ -541,6 +548,47 @@ int ora_assemble_fem(ora_mesh* m, double E, double nu, int64_t node_lo, int64_t 
   coo_to_csr(coo, 3 * node_lo, 3 * (node_hi - node_lo), m->K);
   m->have_csr = true;
   m->have_rhs = false;
+  return 0;
+}
+
+// K7: one domain's dense stiffness, 15x15 with absent field positions zero.
+int ora_face_stiffness(ora_mesh* m, int64_t f, double E, double nu, double* K, int32_t* field) {
+  if (!(E > 0.0) || !(nu > -1.0 && nu < 0.5)) return fail(m, 1, "material out of range");
+  int32_t fld[5];
+  double bb[15], Vf;
+  int P;
+  const int st = ora_face_domain(m, f, fld, bb, &Vf, &P, nullptr);
+  if (st != 0) return st;
+  double c[6][6];
+  material(E, nu, c);
+  const int n = (fld[4] >= 0) ? 5 : 4;
+  double b[5][3];
+  for (int I = 0; I < n; ++I)
+    for (int h = 0; h < 3; ++h) b[I][h] = bb[3 * I + h];
+  std::vector<double> Kf;
+  dense_stiffness(n, b, Vf, c, Kf);  // Eq. 9 summand: B^T c B V_k
+  const int mm = 3 * n;
+  for (int i = 0; i < 225; ++i) K[i] = 0.0;
+  for (int i = 0; i < mm; ++i)
+    for (int j = 0; j < mm; ++j) K[15 * i + j] = Kf[static_cast<size_t>(i) * mm + j];
+  for (int I = 0; I < 5; ++I) field[I] = fld[I];
+  return 0;
+}
+
+int ora_tet_stiffness(ora_mesh* m, int64_t t, double E, double nu, double* K, int32_t* field) {
+  if (!(E > 0.0) || !(nu > -1.0 && nu < 0.5)) return fail(m, 1, "material out of range");
+  if (t < 0 || t >= m->nt) return fail(m, 1, "tet id out of range");
+  double c[6][6];
+  material(E, nu, c);
+  double b[4][3], Ve;
+  tet_gradients(m, t, b, &Ve);
+  std::vector<double> Ke;
+  dense_stiffness(4, b, Ve, c, Ke);
+  for (int i = 0; i < 225; ++i) K[i] = 0.0;
+  for (int i = 0; i < 12; ++i)
+    for (int j = 0; j < 12; ++j) K[15 * i + j] = Ke[static_cast<size_t>(i) * 12 + j];
+  for (int I = 0; I < 4; ++I) field[I] = m->tets[4 * t + I];
+  field[4] = -1;
   return 0;
 }
 

@@ -47,6 +47,13 @@ int ora_face_domain(ora_mesh* m, int64_t f, int32_t* field, double* bbar, double
 int ora_assemble_fs(ora_mesh* m, double E, double nu, int64_t node_lo, int64_t node_hi);
 /* O8 (conventional FEM-T4): K_e = V_e B^T c B per tet, same COO->CSR. */
 int ora_assemble_fem(ora_mesh* m, double E, double nu, int64_t node_lo, int64_t node_hi);
+/* K7: dense stiffness of one smoothing domain -- face f (Eq. 9 summand
+ * V_k Bbar^T c Bbar, 15x15 interior / 12x12 exterior) or, for FEM-T4,
+ * tet t (V_e B^T c B) -- into K[15*15] row-major, row/column 3I+a for field position I
+ * (faces: a, b, c, opp0, opp1; tets: the 4 nodes in tet order), absent positions zero;
+ * field[5] = node ids, -1 absent. */
+int ora_face_stiffness(ora_mesh* m, int64_t f, double E, double nu, double* K, int32_t* field);
+int ora_tet_stiffness(ora_mesh* m, int64_t t, double E, double nu, double* K, int32_t* field);
 /* Triplets emitted by the last ora_assemble_fs (Eq. 12: N_e*144 + N_i*225 for all rows). */
 int64_t ora_last_coo_count(const ora_mesh* m);
 /* Replace K by a caller CSR over all 3*nn rows (used by solver pins on hand-made matrices). */

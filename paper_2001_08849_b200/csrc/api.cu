@@ -41,6 +41,9 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
 void assemble_tiles_device(const Pattern& pat, const double* xyz, double lam, double mu, double* vals, bool tet,
                            cudaStream_t s);
 void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s);
+void domain_stiffness_device(const double* xyz, const int32_t* rec_a, const int32_t* rec_b, bool tet,
+                             const int64_t* ids, int64_t n, double lam, double mu, double* K, int32_t* field,
+                             cudaStream_t s);
 void recover_device(const int32_t* rec_a, const int32_t* rec_b, bool tet, const double* rec_s, const double* rec_V,
                     int64_t nrec,
                     const int64_t* nd_ptr, const int32_t* nd_idx, int64_t nloc, const double* u, double lam, double mu,
@@ -1470,6 +1473,39 @@ fsfem_status fsfem_recover_stress(fsfem_ctx* c, const double* u, double* strain,
     if (strain && d_strain != strain) from_device(strain, d_strain, sizeof(double) * 6 * nd, c->stream);
     if (node_stress) node_out(c, node_stress, d_nodes, c->n_lo, c->nloc, 6);
     if (node_vm) node_out(c, node_vm, d_vm, c->n_lo, c->nloc, 1);
+    FS_CUDA(cudaStreamSynchronize(c->stream));
+    return FSFEM_OK;
+  });
+}
+
+fsfem_status fsfem_domain_stiffness(fsfem_ctx* c, const int64_t* ids, int64_t n, double* K, int32_t* field) {
+  return guarded(c, [&]() -> fsfem_status {
+    if (c->stage < kAssembled) return fail(c, FSFEM_ERR_STATE, "assemble_csr first (uses its E, nu)");
+    if (n < 0 || (n > 0 && (!ids || !K))) return fail(c, FSFEM_ERR_INVALID_ARG, "null ids / K or n < 0");
+    if (n == 0) return FSFEM_OK;
+    const bool tet = c->method == FSFEM_METHOD_FEM_T4;
+    const int64_t nd = tet ? c->nt : c->nf;
+    for (int64_t q = 0; q < n; ++q)  // argument check
+      if (ids[q] < 0 || ids[q] >= nd) return fail(c, FSFEM_ERR_INVALID_ARG, "domain id out of range");
+    const double lam = c->E * c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
+    const double mu = c->E / (2.0 * (1.0 + c->nu));
+    DevBuf<int64_t> d_ids;
+    DevBuf<double> d_K;
+    DevBuf<int32_t> d_f, d_f2;
+    d_ids.ensure(n);
+    d_K.ensure(225 * n);
+    d_f.ensure(5 * n);
+    to_device(d_ids.get(), ids, sizeof(int64_t) * n, c->stream);
+    domain_stiffness_device(c->xyz.get(), tet ? c->tets.get() : c->face_nodes.get(), tet ? nullptr : c->face_opp.get(),
+                            tet, d_ids.get(), n, lam, mu, d_K.get(), d_f.get(), c->stream);
+    const int32_t* fo = d_f.get();
+    if (c->reordered) {  // back to the caller's node ids
+      d_f2.ensure(5 * n);
+      perm_ids_device(c->iperm.get(), fo, d_f2.get(), 5 * n, c->stream);
+      fo = d_f2.get();
+    }
+    from_device(K, d_K.get(), sizeof(double) * 225 * n, c->stream);
+    if (field) from_device(field, fo, sizeof(int32_t) * 5 * n, c->stream);
     FS_CUDA(cudaStreamSynchronize(c->stream));
     return FSFEM_OK;
   });

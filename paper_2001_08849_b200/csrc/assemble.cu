@@ -634,6 +634,68 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// M-form of one block (reading Q25): K = lam M + mu M^T + mu tr(M) I, M = sum s_i s_j^T.
+__device__ __forceinline__ void mform_block(const double* M, double lam, double mu, double* out) {
+  const double tr = M[0] + M[4] + M[8];
+#pragma unroll
+  for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      double v = fma(lam, M[3 * aa + cc], mu * M[3 * cc + aa]);
+      if (aa == cc) v = fma(mu, tr, v);
+      out[3 * aa + cc] = v;
+    }
+}
+
+template <bool kTet>
+__device__ __forceinline__ void domain_s(const double* __restrict__ X, const unsigned char* fv, double* out);
+
+// K7 debug export: the dense stiffness of selected domains with the assembly's own
+// arithmetic (domain_s, one M = s_I s_J^T per block, mform_block); thread per domain.
+template <bool kTet>
+__global__ void k_domain_stiffness(const double* __restrict__ xyz, const int32_t* __restrict__ rec_a,
+                                   const int32_t* __restrict__ rec_b, const int64_t* __restrict__ ids, int64_t n,
+                                   double lam, double mu, double* __restrict__ K, int32_t* __restrict__ field) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    int32_t fld[5];
+    field_of(rec_a, rec_b, kTet, ids[q], fld);
+    double X[15];
+    unsigned char fv[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      fv[p] = fld[p] >= 0 ? static_cast<unsigned char>(p) : 255;
+      const int32_t v = fld[p] >= 0 ? fld[p] : fld[0];
+      X[3 * p] = xyz[3 * (int64_t)v];
+      X[3 * p + 1] = xyz[3 * (int64_t)v + 1];
+      X[3 * p + 2] = xyz[3 * (int64_t)v + 2];
+    }
+    double sv[15];
+    domain_s<kTet>(X, fv, sv);
+    double* Kq = K + 225 * q;
+    for (int I = 0; I < 5; ++I)
+      for (int J = 0; J < 5; ++J) {
+        double blk[9];
+        if (fld[I] >= 0 && fld[J] >= 0) {
+          double M[9];
+#pragma unroll
+          for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) M[3 * aa + cc] = fma(sv[3 * I + aa], sv[3 * J + cc], 0.0);
+          mform_block(M, lam, mu, blk);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 9; ++e) blk[e] = 0.0;
+        }
+#pragma unroll
+        for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) Kq[15 * (3 * I + aa) + 3 * J + cc] = blk[3 * aa + cc];
+      }
+#pragma unroll
+    for (int p = 0; p < 5; ++p) field[5 * q + p] = fld[p];
+  }
+}
+
 // s_K of domain k from the staged coordinates.  FS: field (a, b, c, d, e) -- the face nodes and
 // the vertices opposite the face in its tets (a, b, c, d) and (a, b, c, e); each tet's weights
 // w_K = (V_e / 4) grad N_K^e = sign(det) (cross product of two edges) / 24 land on known field
@@ -930,16 +992,7 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
         }
       }
       if (tk.sub == 255) {
-        const double tr = M[0] + M[4] + M[8];
-        double* out = vals + 9 * (rows[tk.row].P + tk.slot);
-#pragma unroll
-        for (int aa = 0; aa < 3; ++aa)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) {
-            double v = fma(lam, M[3 * aa + cc], mu * M[3 * cc + aa]);
-            if (aa == cc) v = fma(mu, tr, v);
-            out[3 * aa + cc] = v;
-          }
+        mform_block(M, lam, mu, vals + 9 * (rows[tk.row].P + tk.slot));
       } else {  // diagonal sub-list: the 6 independent entries of the symmetric partial
         double* dp = dpart + 6 * (kDiagSplit * tk.row + tk.sub);
         dp[0] = M[0];
@@ -958,16 +1011,7 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
 #pragma unroll
         for (int v = 0; v < 6; ++v) d[v] += dpart[6 * (kDiagSplit * r + q) + v];
       const double Md[9] = {d[0], d[3], d[4], d[3], d[1], d[5], d[4], d[5], d[2]};
-      const double tr = Md[0] + Md[4] + Md[8];
-      double* out = vals + 9 * (rows[r].P + rows[r].sdiag);
-#pragma unroll
-      for (int aa = 0; aa < 3; ++aa)
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-          double v = fma(lam, Md[3 * aa + cc], mu * Md[3 * cc + aa]);
-          if (aa == cc) v = fma(mu, tr, v);
-          out[3 * aa + cc] = v;
-        }
+      mform_block(Md, lam, mu, vals + 9 * (rows[r].P + rows[r].sdiag));
     }
     named_sync(6, kGroup);              // dpart reused by the next tile
     named_arrive(3 + b, kAsmThreads);   // buffer b free (S, X and the blob slot of tile j)
@@ -1084,6 +1128,19 @@ void assemble_tiles_device(const Pattern& pat, const double* xyz, double lam, do
   const int g = static_cast<int>(std::min<int64_t>(pat.ntiles, static_cast<int64_t>(per_sm) * num_sms()));
   auto k = tet ? k_asm_tile<true> : k_asm_tile<false>;
   k<<<g, kAsmThreads, kAsmSmem, s>>>(pat.tile_bytes.get(), pat.tile_blob.get(), pat.ntiles, xyz, lam, mu, vals);
+  FS_LAUNCH_CHECK();
+}
+
+// K7 debug export (fsfem_domain_stiffness): ids, K [n][15][15] and field [n][5] on the device.
+void domain_stiffness_device(const double* xyz, const int32_t* rec_a, const int32_t* rec_b, bool tet,
+                             const int64_t* ids, int64_t n, double lam, double mu, double* K, int32_t* field,
+                             cudaStream_t s) {
+  if (n <= 0) return;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 128), 16LL * num_sms())));
+  if (tet)
+    k_domain_stiffness<true><<<grid, 128, 0, s>>>(xyz, rec_a, rec_b, ids, n, lam, mu, K, field);
+  else
+    k_domain_stiffness<false><<<grid, 128, 0, s>>>(xyz, rec_a, rec_b, ids, n, lam, mu, K, field);
   FS_LAUNCH_CHECK();
 }
 

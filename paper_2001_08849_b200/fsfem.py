@@ -29,7 +29,7 @@ EXPORTS = ["fsfem_status_string", "fsfem_create", "fsfem_destroy", "fsfem_last_e
            "fsfem_comm_init_loopback", "fsfem_get_partition", "fsfem_set_deterministic", "fsfem_set_loop", "fsfem_set_overlap", "fsfem_set_method", "fsfem_set_reorder", "fsfem_set_pcg_variant", "fsfem_set_exchange", "fsfem_get_halo",
            "fsfem_nccl_get_unique_id", "fsfem_build_faces", "fsfem_get_faces", "fsfem_assemble_csr",
            "fsfem_get_csr", "fsfem_apply_bc", "fsfem_pcg_solve", "fsfem_get_report", "fsfem_spmv", "fsfem_recover_stress",
-           "fsfem_surface_loads"]
+           "fsfem_surface_loads", "fsfem_domain_stiffness"]
 
 
 class FsfemReport(ctypes.Structure):
@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
         "fsfem_get_report": (I, [P, ctypes.POINTER(FsfemReport)]),
         "fsfem_spmv": (I, [P, P, P]),
         "fsfem_recover_stress": (I, [P, P, P, P, P, P, P]),
+        "fsfem_domain_stiffness": (I, [P, P, ctypes.c_int64, P, P]),
         "fsfem_surface_loads": (I, [P, P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -286,6 +287,10 @@ def fsfem_recover_stress(ctx, u, strain, stress, node_stress, node_vm) -> int:
     return nd.value
 
 
+def fsfem_domain_stiffness(ctx, ids, K, field) -> None:
+    _raise(ctx, load_library().fsfem_domain_stiffness(ctx, _ptr(ids), _nelem(ids), _ptr(K), _ptr(field)))
+
+
 def fsfem_surface_loads(ctx, node_flag, traction, loads) -> None:
     t = np.ascontiguousarray(traction, np.float64)
     _raise(ctx, load_library().fsfem_surface_loads(ctx, _ptr(node_flag), _ptr(t), _ptr(loads)))
@@ -395,6 +400,14 @@ class FsFem:
         ns, vm = np.zeros((self.n_nodes, 6)), np.zeros(self.n_nodes)
         fsfem_recover_stress(self.ctx, u, eps, sig, ns, vm)
         return eps, sig, ns, vm
+
+    def domain_stiffness(self, ids):
+        """K7 debug export: (K [n, 15, 15], field [n, 5]) of faces (FS-FEM) or tets (FEM-T4) ids."""
+        ids = np.ascontiguousarray(ids, np.int64).reshape(-1)
+        K = np.empty((len(ids), 15, 15))
+        field = np.empty((len(ids), 5), np.int32)
+        fsfem_domain_stiffness(self.ctx, ids, K, field)
+        return K, field
 
     def surface_loads(self, node_flag, traction):
         """Nodal loads [n_nodes, 3] of a uniform traction on the flagged exterior faces."""

@@ -104,6 +104,10 @@ def test_high_valence_node_limits(P):
     xyz, tets = _icosphere_star(2)  # 320 tets around node 0
     g = P.FsFem()
     g.build_faces(xyz, tets)
+    # 960 face instances in node 0's bucket: the CTA (large-bucket) sort ran; faces still bit-exact
+    ofn, oft, ofo = Oracle(xyz, tets).build_faces()
+    fn, ft, fo = g.get_faces()
+    assert np.array_equal(fn, ofn) and np.array_equal(ft, oft) and np.array_equal(fo, ofo)
     with pytest.raises(P.FsfemError) as e:
         g.assemble_csr(E, NU)
     assert e.value.status == "UNSUPPORTED"
@@ -118,4 +122,23 @@ def test_high_valence_node_limits(P):
     c = g.get_csr()
     assert np.array_equal(c.row_ptr, orp) and np.array_equal(c.col_idx, oci)
     assert np.abs(c.vals - ova).max() <= 1e-12 * np.abs(ova).max()
+    g.close()
+
+
+def test_face_bucket_limits(P):
+    """Face extraction buckets by the smallest vertex: 3840 instances (1280 tets around node 0) use
+    the large-bucket sort and match the oracle; beyond kBigCap = 4096 instances (5120 tets,
+    15360 instances) build_faces reports UNSUPPORTED (include/fsfem.h)."""
+    xyz, tets = _icosphere_star(3)
+    g = P.FsFem()
+    g.build_faces(xyz, tets)
+    ofn, oft, ofo = Oracle(xyz, tets).build_faces()
+    fn, ft, fo = g.get_faces()
+    assert np.array_equal(fn, ofn) and np.array_equal(ft, oft) and np.array_equal(fo, ofo)
+    g.close()
+    xyz, tets = _icosphere_star(4)
+    g = P.FsFem()
+    with pytest.raises(P.FsfemError) as e:
+        g.build_faces(xyz, tets)
+    assert e.value.status == "UNSUPPORTED"
     g.close()

@@ -358,19 +358,34 @@ def run_gpu(args):
     last = reps[-1][2]
     # algorithmic bytes as the library counts them for its symmetric block storage
     spmv_bytes = int(last["spmv_bytes"])
-    achieved = spmv_bytes / (spmv_avg_ms / 1e3) / 1e9
+    cluster_loop = int(last["pcg_loop"]) == 2
     kind = int(last["spmv_kernel"])
-    roof = {"kernel": SPMV_KERNELS.get(kind, str(kind)), "bound": "hbm", "achieved": achieved, "peak": peak,
+    if cluster_loop:
+        # the whole recurrence is one launch of the cluster kernel: its bytes per iteration are the
+        # SpMV's plus the vector traffic of S9 (88 B per dof beyond the SpMV's x read / y write)
+        it_bytes = spmv_bytes + 88 * 3 * m.n_nodes
+        achieved = it_bytes * iters / (t_pcg / 1e3) / 1e9
+        roof = {"kernel": "k_pcg_cluster (whole PCG loop in one thread-block-cluster launch)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "algorithmic_bytes_per_iteration": it_bytes, "iterations_per_launch": iters,
+                "avg_launch_ms": t_pcg, "peak_kind": peak_kind, "launches_per_step": 1,
+                "share_of_step": t_pcg / (ms / args.steps),
+                "timing": "CUDA events around the PCG loop of every timed step (fsfem_report.t_pcg_ms)",
+                "note": "operator and vectors are L2-resident at this size; the HBM peak is an upper bound only"}
+    achieved = spmv_bytes / (max(spmv_avg_ms, 1e-12) / 1e3) / 1e9
+    roof_spmv = {"kernel": SPMV_KERNELS.get(kind, str(kind)), "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profile(args.config, kind),
             "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms, "launches_timed": spmv_n,
             "peak_kind": peak_kind, "launches_per_step": iters + 1,
             "share_of_step": spmv_dev_ms / max(spmv_dev_n, 1) * (iters + 1) / (ms / args.steps),
             "timing": "CUDA events around the first SpMV of every 32-iteration CUDA-graph batch, live in the timed steps",
             "device_timer": {"avg_launch_ms": spmv_dev_avg_ms, "launches": spmv_dev_n,
-                             "achieved": spmv_bytes / (spmv_dev_avg_ms / 1e3) / 1e9,
-                             "frac": spmv_bytes / (spmv_dev_avg_ms / 1e3) / 1e9 / peak,
+                             "achieved": spmv_bytes / (max(spmv_dev_avg_ms, 1e-12) / 1e3) / 1e9,
+                             "frac": spmv_bytes / (max(spmv_dev_avg_ms, 1e-12) / 1e3) / 1e9 / peak,
                              "how": "%globaltimer from the first CTA start to the last CTA end of EVERY PCG SpMV"},
             "full_csr_equivalent_bytes": 12 * nnz + 32 * 3 * m.n_nodes}
+    if not cluster_loop:
+        roof = roof_spmv
     asm_bytes = int(last["assembly_bytes"])
     asm_aux = int(last["assembly_aux_bytes"])
     survey_bytes = 24 * m.n_nodes + 16 * m.n_tets + 8 * nnz  # mesh + full CSR values
@@ -387,8 +402,11 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config), "n_nodes": m.n_nodes, "n_tets": m.n_tets,
                        "n_faces": nf, "nnz": nnz, "parallelism": f"row-block x{world} ({args.exchange})" if world > 1 else "single GPU",
-                       "pcg": "Jacobi-PCG (standard recurrence, host-polled CUDA-graph batches of 32 iterations)",
-                       "l2": "inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)"},
+                       "pcg": ("Jacobi-PCG (standard recurrence, whole loop in one thread-block-cluster kernel)"
+                               if cluster_loop else
+                               "Jacobi-PCG (standard recurrence, host-polled CUDA-graph batches of 32 iterations)"),
+                       "l2": ("inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)" if 8 * nnz > 126e6 else
+                              "inputs smaller than L2: the operator stays L2-resident between iterations")},
             "components": {"assembly_faces_per_s": nf / (t_num / 1e3), "assembly_ms": t_num,
                            "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,
                            "pcg_it_per_s": iters / (t_pcg / 1e3), "pcg_iterations": iters, "pcg_ms": t_pcg,

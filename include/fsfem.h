@@ -92,6 +92,8 @@ typedef struct {
   double t_spmv_dev_ms;      /* summed duration of EVERY PCG SpMV launch of the solve, timed on the
                                 device (%globaltimer: first CTA start to last CTA end)          */
   int64_t spmv_dev_launches; /* number of launches in t_spmv_dev_ms                              */
+  int64_t pcg_loop;          /* loop that ran the last pcg_solve: FSFEM_LOOP_DEVICE, _HOST or
+                                _CLUSTER (see fsfem_set_loop)                                     */
 } fsfem_report;
 
 /* Human-readable name of a status code (static string). */
@@ -190,12 +192,17 @@ fsfem_status fsfem_set_pcg_variant(fsfem_ctx* ctx, int variant);
 
 /* PCG loop control.  FSFEM_LOOP_DEVICE: the whole solve is ONE CUDA-graph launch whose while
  * node repeats a body of 8 iterations until the device-side recurrence stops -- no host
- * synchronisation inside the solve.  FSFEM_LOOP_HOST (default): graph batches of 32 iterations,
- * the host polls the state between batches (always used with NCCL ranks).  Results are
- * bitwise identical and the measured speed is the same; the host loop is the
- * default because profilers cannot see kernels inside graphs with conditional nodes.
- * Errors: INVALID_ARG. */
-enum { FSFEM_LOOP_DEVICE = 0, FSFEM_LOOP_HOST = 1 };
+ * synchronisation inside the solve.  FSFEM_LOOP_HOST: graph batches of 32 iterations, the host
+ * polls the state between batches (always used with NCCL ranks).  These two give bitwise
+ * identical results at the same measured speed.  FSFEM_LOOP_CLUSTER: the whole
+ * recurrence in ONE kernel launch on one thread-block cluster (up to 16 CTAs, reductions over
+ * distributed shared memory, cluster barriers between the steps) -- for small meshes, where the
+ * multi-kernel loop is launch-bound; single rank, standard recurrence, non-deterministic mode
+ * only (otherwise the host loop runs).  Its reductions are grouped differently, so its rounding
+ * (and possibly the iteration count) differs slightly from the other two; it is itself bitwise
+ * reproducible.  FSFEM_LOOP_AUTO (default): CLUSTER when applicable and the operator has at
+ * most 8000 stored + transposed blocks (where it was measured faster: cfg1), HOST otherwise.  Errors: INVALID_ARG. */
+enum { FSFEM_LOOP_DEVICE = 0, FSFEM_LOOP_HOST = 1, FSFEM_LOOP_CLUSTER = 2, FSFEM_LOOP_AUTO = 3 };
 fsfem_status fsfem_set_loop(fsfem_ctx* ctx, int mode);
 
 /* S1: extract the unique faces of the mesh.

@@ -41,6 +41,10 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
 void assemble_tiles_device(const Pattern& pat, const double* xyz, double lam, double mu, double* vals, bool tet,
                            cudaStream_t s);
 void tet_s_device(const double* xyz, const int32_t* tets, int64_t nt, double* tet_s, double* tet_V, cudaStream_t s);
+int cluster_pcg_size(int64_t nloc);
+void cluster_pcg_split(const Pattern& pat, int C, int64_t* split, cudaStream_t s);
+void launch_pcg_cluster(const Pattern& pat, const double* vals, const double* dinv, double* x, double* r, double* p,
+                        double* q, const int64_t* split, int C, PcgState* st, cudaStream_t s);
 void domain_stiffness_device(const double* xyz, const int32_t* rec_a, const int32_t* rec_b, bool tet,
                              const int64_t* ids, int64_t n, double lam, double mu, double* K, int32_t* field,
                              cudaStream_t s);
@@ -165,6 +169,9 @@ static NcclApi& nccl() {
 using namespace fsfem;
 
 enum Stage { kCreated = 0, kFaces = 1, kAssembled = 2, kBc = 3 };
+// FSFEM_LOOP_AUTO picks the cluster kernel up to this many stored + transposed blocks (measured,
+// cfg1, 1.4k blocks: 9.3 vs 15.2 us per iteration; cfg2, 74k: 29 vs 17 us)
+constexpr int64_t kClusterAutoBlocks = 8000;
 
 struct fsfem_ctx {
   int device = 0;
@@ -235,7 +242,8 @@ struct fsfem_ctx {
   long long graph_launches = 0;  // kernels per replay of the graph (counted at capture)
   // device-side loop (default): one graph whose while node repeats a body of kDevBatch iterations
   // until the recurrence stops -- no host synchronisation inside the solve
-  int loop_mode = FSFEM_LOOP_HOST;  // device loop: same speed measured, not ncu-visible
+  int loop_mode = FSFEM_LOOP_AUTO;  // cluster kernel for small meshes, else host batches
+  DevBuf<int64_t> cl_split;         // row split of the cluster PCG kernel
   cudaGraphExec_t dgraph = nullptr;
   std::vector<uintptr_t> dgraph_key;
   long long dgraph_body_launches = 0;
@@ -850,8 +858,8 @@ fsfem_status fsfem_set_overlap(fsfem_ctx* c, int on) {
 
 fsfem_status fsfem_set_loop(fsfem_ctx* c, int mode) {
   return guarded(c, [&]() -> fsfem_status {
-    if (mode != FSFEM_LOOP_DEVICE && mode != FSFEM_LOOP_HOST)
-      return fail(c, FSFEM_ERR_INVALID_ARG, "loop mode must be 0 (device) or 1 (host batches)");
+    if (mode < FSFEM_LOOP_DEVICE || mode > FSFEM_LOOP_AUTO)
+      return fail(c, FSFEM_ERR_INVALID_ARG, "loop mode must be 0 (device), 1 (host), 2 (cluster) or 3 (auto)");
     c->loop_mode = mode;
     return FSFEM_OK;
   });
@@ -1268,9 +1276,19 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     start(u0_is_zero != 0);
     read_state();
 
-    // The loop: device-side while node (default) or host-polled batches of kBatch iterations.
+    // The loop: one cluster kernel (small meshes), a device-side while node, or host-polled
+    // batches of kBatch iterations.
     const std::vector<uintptr_t> key = graph_key_of(cs);
-    bool device_loop = c->loop_mode == FSFEM_LOOP_DEVICE && !c->dgraph_failed && !(c0->nranks > 1 && !c0->loop);
+    const bool cluster_ok = cs.size() == 1 && c->nranks == 1 && !det && !cg1;
+    const bool cluster = cluster_ok && (c->loop_mode == FSFEM_LOOP_CLUSTER ||
+                                        (c->loop_mode == FSFEM_LOOP_AUTO && c->pat.nsb + c->pat.ntb <= kClusterAutoBlocks));
+    int cl_C = 0;
+    if (cluster) {
+      cl_C = cluster_pcg_size(c->nloc);
+      c->cl_split.ensure(cl_C + 1);
+      cluster_pcg_split(c->pat, cl_C, c->cl_split.get(), c->stream);
+    }
+    bool device_loop = !cluster && c->loop_mode == FSFEM_LOOP_DEVICE && !c->dgraph_failed && !(c0->nranks > 1 && !c0->loop);
     if (device_loop && (!c->dgraph || key != c->dgraph_key)) {
       if (c->dgraph) cudaGraphExecDestroy(c->dgraph);
       c->dgraph = nullptr;
@@ -1312,7 +1330,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       }
       cudaGraphDestroy(g);
     }
-    if (!device_loop && (!c->graph || key != c->graph_key)) {
+    if (!cluster && !device_loop && (!c->graph || key != c->graph_key)) {
       if (c->graph) cudaGraphExecDestroy(c->graph);
       c->graph = nullptr;
       cudaGraph_t g;
@@ -1341,7 +1359,11 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
     double ev_ms = 0.0;
     int64_t ev_n = 0;
     for (;;) {
-      if (device_loop) {
+      if (cluster) {
+        launch_pcg_cluster(c->pat, c->vals.get(), c->dinv.get(), own_x(c), c->r.get(), c->p_full.get(), c->q.get(),
+                           c->cl_split.get(), cl_C, c->st.get(), c->stream);
+        read_state();
+      } else if (device_loop) {
         FS_CUDA(cudaGraphLaunch(c->dgraph, c->stream));
         read_state();
         const long long bodies = std::max<long long>(1, (c0->h_st->iters + kDevBatch - 1) / kDevBatch);
@@ -1420,6 +1442,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       r->rep.spmv_dev_launches = static_cast<int64_t>(h.spmv_cnt);
       r->rep.t_spmv_ms = device_loop ? r->rep.t_spmv_dev_ms : ev_ms;  // CUDA events (host-polled loop)
       r->rep.spmv_launches = device_loop ? r->rep.spmv_dev_launches : ev_n;
+      r->rep.pcg_loop = cluster ? FSFEM_LOOP_CLUSTER : (device_loop ? FSFEM_LOOP_DEVICE : FSFEM_LOOP_HOST);
       r->rep.kernel_launches = launch_count();
     }
     if (std::getenv("FSFEM_GAP_PRINT"))

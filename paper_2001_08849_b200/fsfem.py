@@ -43,7 +43,7 @@ class FsfemReport(ctypes.Structure):
                 ("assembly_bytes", ctypes.c_int64), ("spmv_kernel", ctypes.c_int64),
                 ("residual_floor", ctypes.c_double), ("restarts", ctypes.c_int64),
                 ("assembly_aux_bytes", ctypes.c_int64), ("t_spmv_dev_ms", ctypes.c_double),
-                ("spmv_dev_launches", ctypes.c_int64)]
+                ("spmv_dev_launches", ctypes.c_int64), ("pcg_loop", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

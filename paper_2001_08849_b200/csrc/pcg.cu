@@ -610,7 +610,12 @@ __device__ __forceinline__ int ld_acquire_cta_s32(const int* p) {
 #endif
 constexpr int kDfBatch = FSFEM_DF_BATCH;
 constexpr int kDfMinChunksPerCta = 16;
-constexpr int kDfThreads = kThreads + 96;  // 8 compute warps, loader, phase-2 and counter warps
+#ifndef FSFEM_DF_P2W
+#define FSFEM_DF_P2W 1
+#endif
+constexpr int kDfP2W = FSFEM_DF_P2W;  // phase-2 warps (2: chunks alternate between them)
+static_assert(kDfP2W == 1 || kDfP2W == 2, "one or two phase-2 warps");
+constexpr int kDfThreads = kThreads + 32 * (2 + kDfP2W);  // 8 compute warps, loader, counter, phase 2
 struct P2Layout {  // phase-2 buffer: node pointers, P1 sums, own x (p.q), pushed slots of one chunk
   static constexpr int kPtr = 0;                               // kChunkNodes + 4 int64
   static constexpr int kY = kPtr + (kChunkNodes + 4) * 8;      // 3 kChunkNodes + 4 double
@@ -737,7 +742,9 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       DF_T(tC)
       while (ld_acquire_cta_s32(&sh_p1done) < jd) __nanosleep(32);
       DF_T(tA)
+#ifndef FSFEM_DF_NOFENCE
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
       DF_T(tB)
       uint32_t old[kDfBatch][R];
 #pragma unroll
@@ -766,13 +773,17 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
           }
       if (jd < K) prefetch(jd);  // in flight during the fence and the next wait
       if (__any_sync(0xffffffffu, any_last)) {
+#ifndef FSFEM_DF_NOFENCE
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
         for (int k = 0; k < nready; ++k)
           asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ready + my_ready[k]), "r"(epoch) : "memory");
       }
     }
-  } else if (warp == kWarps + 1) {
+  } else if (warp == kWarps + 1 || (kDfP2W == 2 && warp == kWarps + 3)) {
     // ---------------- phase-2 warp: the CTA's own chunks in order, lane = node ----------------
+    // (two phase-2 warps: warp kWarps + 1 takes the even, warp kWarps + 3 the odd chunks, each
+    // with its own buffer j & 1 and no prefetch)
     // chunk d's node pointers, pushed slots and P1 sums are bulk-copied into buffer j & 1 once d
     // is ready; the copy of the next chunk is issued before the current one is summed.
     auto ready_now = [&](int d) { return __shfl_sync(0xffffffffu, lane == 0 ? ld_acquire_u32(ready + d) : 0u, 0) == epoch; };
@@ -810,9 +821,10 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       __syncwarp();
     };
     int issued = 0;
-    for (int j = 0; j < K; ++j) {
+    const int pw = warp == kWarps + 1 ? 0 : 1;
+    for (int j = kDfP2W == 1 ? 0 : pw; j < K; j += kDfP2W) {
       DF_T(tC)
-      if (issued == j) {  // this chunk's copy must be in flight: wait for it to be ready
+      if (kDfP2W == 2 || issued == j) {  // this chunk's copy must be in flight: wait for it to be ready
         while (!ready_now(blockIdx.x + j * gridDim.x)) __nanosleep(32);
         issue(j);
         ++issued;
@@ -820,7 +832,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       // readiness of the next chunk: the acquire load is issued now and looked at after this
       // chunk's sums, so its latency overlaps them
       uint32_t nflag = 0u;
-      const bool probe = issued == j + 1 && j + 1 < K;
+      const bool probe = kDfP2W == 1 && issued == j + 1 && j + 1 < K;
       if (probe && lane == 0) nflag = ld_acquire_u32(ready + blockIdx.x + (j + 1) * gridDim.x);
       DF_T(tA)
       ++nitems;
@@ -904,6 +916,9 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       int rounds = (nus + G * kPushItems - 1) / (G * kPushItems);
 #pragma unroll 1
       for (int o = G; o < 32; o <<= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+#ifdef FSFEM_DF_MINWORK
+      rounds = 0;  // timing experiment: no per-block work (wrong product)
+#endif
       for (int r = 0; r < rounds; ++r) {
         double xs[kPushItems];
 #pragma unroll

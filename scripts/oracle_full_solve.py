@@ -3,7 +3,8 @@
 Writes tests/golden/oracle_cfg<N>.json: faces, nnz, PCG iterations, residuals, tip deflection
 and a deterministic sample of displacement entries.  Calls only oracle/ and fsfem_inputs/
 (never the CUDA path).  Used by tests (parity at full size) and by bench.py's CPU baseline
-(iteration count of the full solve).  Usage: python scripts/oracle_full_solve.py 4 [chunks] [--fem]
+(iteration count of the full solve).  Usage: python scripts/oracle_full_solve.py 4 [chunks] [--fem] [--u-only]
+--u-only: write only tests/golden/oracle_cfg<N>_u.npy (the whole displacement vector; any config).
 --fem: the oracle's FEM-T4 companion (O8) instead of FS-FEM ->
 tests/golden/oracle_cfg<N>_fem.json (the FS >= FEM tip-deflection pin).
 """
@@ -22,7 +23,7 @@ from oracle import Oracle  # noqa: E402
 E, NU = 1.0e6, 0.3
 
 
-def main(cfg: int, chunks: int = 4, fem: bool = False):
+def main(cfg: int, chunks: int = 4, fem: bool = False, u_only: bool = False):
     m = config_mesh(cfg)
     o = Oracle(m.xyz, m.tets)
     t = {}
@@ -60,13 +61,14 @@ def main(cfg: int, chunks: int = 4, fem: bool = False):
                method="FEM-T4" if fem else "FS-FEM",
                note="written by scripts/oracle_full_solve.py from oracle/ only")
     path = os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}{'_fem' if fem else ''}.json")
-    with open(path, "w") as fh:
-        json.dump(out, fh, indent=1)
-    if cfg <= 4 and not fem:
+    if not u_only:
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+    if (cfg <= 4 or u_only) and not fem:
         np.save(os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}_u.npy"), u)
     print(json.dumps({k: v for k, v in out.items() if not k.startswith("u_sample")}, indent=1))
 
 
 if __name__ == "__main__":
     pos = [a for a in sys.argv[1:] if not a.startswith("--")]
-    main(int(pos[0]), int(pos[1]) if len(pos) > 1 else 4, fem="--fem" in sys.argv)
+    main(int(pos[0]), int(pos[1]) if len(pos) > 1 else 4, fem="--fem" in sys.argv, u_only="--u-only" in sys.argv)

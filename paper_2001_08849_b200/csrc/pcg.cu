@@ -613,6 +613,9 @@ constexpr int kDfMinChunksPerCta = 16;
 #ifndef FSFEM_DF_P2W
 #define FSFEM_DF_P2W 1
 #endif
+#ifndef FSFEM_DF_GREEDY
+#define FSFEM_DF_GREEDY 1
+#endif
 constexpr int kDfP2W = FSFEM_DF_P2W;  // phase-2 warps (2: chunks alternate between them)
 static_assert(kDfP2W == 1 || kDfP2W == 2, "one or two phase-2 warps");
 constexpr int kDfThreads = kThreads + 32 * (2 + kDfP2W);  // 8 compute warps, loader, counter, phase 2
@@ -715,7 +718,8 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   } else if (warp == kWarps + 2) {
     // ---------------- counter warp: dependency counts, in batches ----------------
     // A gpu-scope fence costs microseconds under this load, so the warp takes every chunk whose
-    // phase 1 is complete (up to kDfBatch) per round: one release fence for all of their writes
+    // phase 1 is complete (at least one, up to kDfBatch; FSFEM_DF_GREEDY = 0 waits for a full
+    // batch: 2 us slower per launch at cfg4) per round: one release fence for all of their writes
     // (ordered before the loader's observation of the mbarriers), relaxed increments, and one
     // acquire fence before the completed chunks are published as ready.
     constexpr int R = 2;  // rounds of 32 dependants per chunk kept in flight (more: slow path)
@@ -737,10 +741,19 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         }
     };
     prefetch(0);
-    for (int j = 0; j < K; j += kDfBatch) {
+    for (int j = 0; j < K;) {
+#if FSFEM_DF_GREEDY
+      // every chunk complete so far (at least one, at most kDfBatch): no wait for a full batch
+      DF_T(tC)
+      int avail;
+      while ((avail = ld_acquire_cta_s32(&sh_p1done)) <= j) __nanosleep(32);
+      const int jd = min(min(K, j + kDfBatch), avail);
+#else
       const int jd = min(K, j + kDfBatch);
       DF_T(tC)
       while (ld_acquire_cta_s32(&sh_p1done) < jd) __nanosleep(32);
+#endif
+      const int nb = jd - j;
       DF_T(tA)
 #ifndef FSFEM_DF_NOFENCE
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -751,7 +764,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       for (int b = 0; b < kDfBatch; ++b)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          old[b][r] = e[b][r].x >= 0 ? atomicInc(cnt + e[b][r].x, static_cast<uint32_t>(e[b][r].y) - 1u) : 0u;
+          old[b][r] = b < nb && e[b][r].x >= 0 ? atomicInc(cnt + e[b][r].x, static_cast<uint32_t>(e[b][r].y) - 1u) : 0u;
       for (int b = 0; b < jd - j; ++b)  // dependants beyond R * 32 (rare)
         for (int q = qq0[b] + 32 * R + lane; q < qq1[b]; q += 32) {
           const int2 ee = dep_list[q];
@@ -767,7 +780,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       for (int b = 0; b < kDfBatch; ++b)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (e[b][r].x >= 0 && old[b][r] == static_cast<uint32_t>(e[b][r].y) - 1u) {
+          if (b < nb && e[b][r].x >= 0 && old[b][r] == static_cast<uint32_t>(e[b][r].y) - 1u) {
             my_ready[nready++] = e[b][r].x;
             any_last = true;
           }
@@ -779,6 +792,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         for (int k = 0; k < nready; ++k)
           asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ready + my_ready[k]), "r"(epoch) : "memory");
       }
+      j = jd;
     }
   } else if (warp == kWarps + 1 || (kDfP2W == 2 && warp == kWarps + 3)) {
     // ---------------- phase-2 warp: the CTA's own chunks in order, lane = node ----------------
@@ -973,8 +987,8 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
 #if FSFEM_DF_TIMING
   if (lane == 0 && (warp == 0 || warp >= kWarps) && (blockIdx.x % 37) == 0)
     printf("df blk %d %s K %d items %d: A %lld B %lld C %lld end %lld\n", blockIdx.x,
-           warp == kWarps ? "load" : (warp == kWarps + 1 ? "p2" : (warp > kWarps ? "count" : "comp")), K, nitems, tA,
-           tB, tC, clock64() - t_begin);
+           warp == kWarps ? "load" : (warp == kWarps + 1 || warp == kWarps + 3 ? "p2" : (warp > kWarps ? "count" : "comp")),
+           K, nitems, tA, tB, tC, clock64() - t_begin);
 #endif
   // last CTA out: advances the epoch; PCG: p.q = sum of the per-chunk partials in chunk order
   __syncthreads();

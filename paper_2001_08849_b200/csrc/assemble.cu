@@ -309,8 +309,8 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t 
 // is arbitrary (it only names shared-memory slots), while every summation order is fixed by the
 // rows' ascending domain lists F(i).
 __global__ void __launch_bounds__(kBldThreads) k_tile_build(
-    const int32_t* __restrict__ order, const int32_t* __restrict__ tstart, int64_t ntiles,
-    const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a,
+    const int32_t* __restrict__ order, const int2* __restrict__ trange, const int32_t* __restrict__ which,
+    int64_t nwork, const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a,
     const int32_t* __restrict__ rec_b, bool tet, const int64_t* __restrict__ sptr, const int32_t* __restrict__ snbr,
     const int32_t* __restrict__ sdiag, int64_t n_lo, int64_t* __restrict__ size, unsigned char* __restrict__ blob) {
   extern __shared__ __align__(16) unsigned char bsm[];
@@ -329,13 +329,14 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
   __shared__ int64_t rP[kTileRows], rF[kTileRows + 1];
   __shared__ int sh_flag, sh_ntask, sh_nent, sh_nv;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int nrows = tstart[t + 1] - tstart[t];
+  for (int64_t wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const int64_t t = which ? which[wi] : wi;  // tile t = own rows order[trange[t].x, trange[t].y)
+    const int nrows = trange[t].y - trange[t].x;
     if (threadIdx.x == 0) {
       int64_t fsum = 0;
       int bb = 0;
       for (int r = 0; r < nrows; ++r) {
-        const int32_t il = order[tstart[t] + r];
+        const int32_t il = order[trange[t].x + r];
         ril[r] = il;
         rnode[r] = static_cast<int32_t>(n_lo + il);
         rP[r] = sptr[il];
@@ -1065,44 +1066,69 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
     FS_CUDA(cudaFuncSetAttribute(k_asm_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));
     attr = true;
   }
-  DevBuf<int32_t>& d_ts = pat.tile_start;
+  // Build every tile; a tile over a cap is cut in two (first half in place, second half appended)
+  // and only the cut tiles are built again (rare: high-valence rows).
+  std::vector<int2> tr;
+  for (size_t k = 0; k + 1 < ts.size(); ++k) tr.push_back(make_int2(ts[k], ts[k + 1]));
+  DevBuf<int2>& d_tr = pat.tile_range;
   std::vector<int64_t> sz;
-  for (;;) {  // build every tile; split the tiles that exceed a cap and rebuild (rare)
-    const int64_t nt = static_cast<int64_t>(ts.size()) - 1;
-    d_ts.ensure(nt + 1);
-    pat.tile_bytes.ensure(nt);
-    pat.tile_blob.ensure(nt * static_cast<int64_t>(kBlobCap));
-    FS_CUDA(cudaMemcpyAsync(d_ts.get(), ts.data(), sizeof(int32_t) * (nt + 1), cudaMemcpyHostToDevice, s));
-    const int g = static_cast<int>(std::min<int64_t>(nt, 8LL * num_sms()));
-    k_tile_build<<<g, kBldThreads, bsmem, s>>>(order.get(), d_ts.get(), nt, pat.nf_ptr.get(), pat.nf_idx.get(), rec_a,
-                                               rec_b, tet, pat.sptr.get(), pat.snbr.get(), pat.sdiag.get(), pat.n_lo,
-                                               pat.tile_bytes.get(), pat.tile_blob.get());
+  std::vector<int32_t> redo;  // tiles to (re)build; empty: all
+  for (;;) {
+    const int64_t nt = static_cast<int64_t>(tr.size());
+    bool all = redo.empty();
+    const int64_t cap = nt + nt / 8 + 64;  // room for cut tiles without a reallocation
+    if (pat.tile_bytes.n < static_cast<size_t>(nt) || pat.tile_blob.n < static_cast<size_t>(nt) * kBlobCap) {
+      pat.tile_bytes.ensure(cap);
+      pat.tile_blob.ensure(cap * static_cast<int64_t>(kBlobCap));
+      all = true;  // a new allocation holds no built tile
+    }
+    d_tr.ensure(nt);
+    FS_CUDA(cudaMemcpyAsync(d_tr.get(), tr.data(), sizeof(int2) * nt, cudaMemcpyHostToDevice, s));
+    const int32_t* which = nullptr;
+    int64_t nwork = nt;
+    if (!all) {
+      pat.tile_redo.ensure(redo.size());
+      FS_CUDA(cudaMemcpyAsync(pat.tile_redo.get(), redo.data(), sizeof(int32_t) * redo.size(), cudaMemcpyHostToDevice,
+                              s));
+      which = pat.tile_redo.get();
+      nwork = static_cast<int64_t>(redo.size());
+    }
+    const int g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nwork, 8LL * num_sms())));
+    k_tile_build<<<g, kBldThreads, bsmem, s>>>(order.get(), d_tr.get(), which, nwork, pat.nf_ptr.get(),
+                                               pat.nf_idx.get(), rec_a, rec_b, tet, pat.sptr.get(), pat.snbr.get(),
+                                               pat.sdiag.get(), pat.n_lo, pat.tile_bytes.get(), pat.tile_blob.get());
     FS_LAUNCH_CHECK();
     sz.resize(nt);
     FS_CUDA(cudaMemcpyAsync(sz.data(), pat.tile_bytes.get(), sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, s));
     FS_CUDA(cudaStreamSynchronize(s));
     pt.mark("tile build + D2H sizes");
-    std::vector<int32_t> nts;
-    bool split = false;
-    for (int64_t k = 0; k < nt; ++k) {
-      nts.push_back(ts[k]);
+    std::vector<int32_t> built;
+    if (all) {
+      built.resize(nt);
+      for (int64_t k = 0; k < nt; ++k) built[k] = static_cast<int32_t>(k);
+    } else {
+      built.swap(redo);
+    }
+    redo.clear();
+    for (const int32_t k : built) {
       if (sz[k] == -2) {  // one row whose domains exceed the tile caps
         int32_t hord = 0;
-        FS_CUDA(cudaMemcpy(&hord, order.get() + ts[k], sizeof(int32_t), cudaMemcpyDeviceToHost));
+        FS_CUDA(cudaMemcpy(&hord, order.get() + tr[k].x, sizeof(int32_t), cudaMemcpyDeviceToHost));
         h_flags[0] = (static_cast<unsigned long long>(FSFEM_ERR_UNSUPPORTED) << 56) |
                      static_cast<unsigned long long>(pat.n_lo + hord);
         return;
       }
       if (sz[k] == -1) {
-        nts.push_back((ts[k] + ts[k + 1]) / 2);
-        split = true;
+        const int mid = (tr[k].x + tr[k].y) / 2;
+        tr.push_back(make_int2(mid, tr[k].y));
+        tr[k].y = mid;
+        redo.push_back(k);
+        redo.push_back(static_cast<int32_t>(tr.size() - 1));
       }
     }
-    nts.push_back(ts[nt]);
-    if (!split) break;
-    ts.swap(nts);
+    if (redo.empty()) break;
   }
-  const int64_t nt = static_cast<int64_t>(ts.size()) - 1;
+  const int64_t nt = static_cast<int64_t>(tr.size());
   int64_t tot = 0, mx = 0;
   for (int64_t k = 0; k < nt; ++k) {
     tot += sz[k];

@@ -80,7 +80,8 @@ struct Pattern {
   int64_t tile_blob_max = 0;    // largest tile blob (bytes)
   int64_t tile_blob_bytes = 0;  // sum of the blob sizes (read once per numeric assembly)
   DevBuf<int64_t> tile_bytes;   // [ntiles]
-  DevBuf<int32_t> tile_order, tile_tmp, tile_start;  // builder scratch (kept: no cudaFree per mesh)
+  DevBuf<int32_t> tile_order, tile_tmp, tile_redo;  // builder scratch (kept: no cudaFree per mesh)
+  DevBuf<int2> tile_range;                           // [ntiles] own-row range of tile t in tile_order
   DevBuf<unsigned char> tile_blob;
 };
 

@@ -1284,7 +1284,10 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
   // Small enough (<= kKeep passes per thread, cfg4): every load -- r, q, D^-1 and also x, p -- is
   // issued before the grid barrier and z = D^-1 r, x, p stay in registers across it, so phase 2
   // only stores (64 instead of 80 B per dof, no load after the barrier).
-  constexpr int kKeep = 2;
+#ifndef FSFEM_UPD_KEEP
+#define FSFEM_UPD_KEEP 2
+#endif
+  constexpr int kKeep = FSFEM_UPD_KEEP;
   const bool keep = n <= static_cast<int64_t>(kKeep) * kVec * T;
   double zk_[kKeep][kVec], xk_[kKeep][kVec], pk_[kKeep][kVec];
   if (keep) {
@@ -1664,7 +1667,10 @@ int update_direction_grid() {
   if (g == 0) {
     int per_sm = 0;
     FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_direction, kThreads, 0));
-    g = std::max(1, std::min(4, per_sm)) * num_sms();
+#ifndef FSFEM_UPD_PER_SM
+#define FSFEM_UPD_PER_SM 4
+#endif
+    g = std::max(1, std::min(FSFEM_UPD_PER_SM, per_sm)) * num_sms();
   }
   return g;
 }

@@ -184,7 +184,8 @@ def fsfem_get_partition(ctx, nranks: int) -> np.ndarray:
 
 
 def fsfem_set_loop(ctx, mode: int) -> None:
-    """0: device-side while loop (default), 1: host-polled graph batches."""
+    """0: device-side while loop, 1: host-polled graph batches, 2: one thread-block-cluster launch,
+    3: auto (default: cluster for small meshes, else host batches)."""
     _raise(ctx, load_library().fsfem_set_loop(ctx, int(mode)))
 
 

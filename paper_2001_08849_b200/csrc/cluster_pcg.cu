@@ -48,6 +48,29 @@ __device__ __forceinline__ double cta_sum(double v, double* sh) {
   return t;
 }
 
+// Two block sums with one pair of barriers.
+__device__ __forceinline__ void cta_sum2(double& a, double& b, double* sh /*[2 * kCWarps]*/) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    sh[threadIdx.x >> 5] = a;
+    sh[kCWarps + (threadIdx.x >> 5)] = b;
+  }
+  __syncthreads();
+  double ta = 0.0, tb = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < kCWarps; ++k) {
+    ta += sh[k];
+    tb += sh[kCWarps + k];
+  }
+  a = ta;
+  b = tb;
+}
+
 // Sum over the cluster's CTAs, in rank order, of slot `k` of every CTA's red[]: lane c of each
 // warp loads CTA c's value over DSMEM, then the warp adds them in sequence.
 __device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, double* red, int k, unsigned nr) {
@@ -68,7 +91,7 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(
     double* __restrict__ x, double* __restrict__ r, double* p, double* __restrict__ q,
     const int64_t* __restrict__ split, PcgState* st) {
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ double sh[kCWarps];
+  __shared__ double sh[2 * kCWarps];
   __shared__ double red[4];  // this CTA's partials: p.q, r.r, r.z
   const unsigned rank = cl.block_rank(), nr = cl.num_blocks();
   const int64_t i0 = split[rank], i1 = split[rank + 1];
@@ -172,10 +195,10 @@ __global__ void __launch_bounds__(kCThreads, 1) k_pcg_cluster(
       rrp = fma(rk, rk, rrp);
       rzp = fma(rk, zk, rzp);
     }
-    const double rrc = cta_sum(rrp, sh), rzc = cta_sum(rzp, sh);
+    cta_sum2(rrp, rzp, sh);
     if (threadIdx.x == 0) {
-      red[1] = rrc;
-      red[2] = rzc;
+      red[1] = rrp;
+      red[2] = rzp;
     }
     cl.sync();
     const double RR = cluster_sum(cl, red, 1, nr), RZ = cluster_sum(cl, red, 2, nr);

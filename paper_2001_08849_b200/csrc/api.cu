@@ -1079,11 +1079,10 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     c->rep.stored_blocks = c->pat.nsb;
     c->rep.transposed_blocks = c->pat.ntb;
     c->rep.spmv_kernel = spmv_kind(c->pat);
-    // the gather kernel reads the transposed list (8 B per transposed block), the push kernels
-    // (dataflow, lagged) the slot of every stored block (4 B); their pushed products are
-    // intermediate traffic
+    // the gather kernel reads the transposed list (8 B per transposed block), the dataflow kernel
+    // the slot of every stored block (4 B); its pushed products are intermediate traffic
     c->rep.spmv_bytes = 72 * c->pat.nsb + 4 * c->pat.nsb +
-                        (c->rep.spmv_kernel >= 2 ? 4 * c->pat.nsb : 8 * c->pat.ntb) + 16 * (c->nloc + 1) +
+                        (c->rep.spmv_kernel == 2 ? 4 * c->pat.nsb : 8 * c->pat.ntb) + 16 * (c->nloc + 1) +
                         24 * c->nn + 24 * c->nloc;
     c->rep.assembly_bytes = 24 * c->nn + 16 * c->nt + 72 * c->pat.nsb;
     c->rep.assembly_aux_bytes = c->pat.tile_blob_bytes;

@@ -56,8 +56,6 @@ struct Pattern {
   DevBuf<int32_t> ndeps;     // [nchunks] their number, or -1 (more than kMaxDeps: no dataflow SpMV)
   DevBuf<uint32_t> cflags;   // [nchunks] epoch at which the chunk became ready for phase 2
   DevBuf<uint32_t> sync;     // [2] epoch, last-CTA ticket
-  // lagged push SpMV (pcg.cu k_spmv_lag): [0] last-CTA ticket, [1 + w] finished chunks of wave w
-  DevBuf<uint32_t> lagw;     // [nchunks + 2], zero between launches
   // chunk d needs ndeps[d] + 1 finished phase-1 chunks (its producers and itself);
   // dep_ptr/dep_list = for each chunk c the chunks d that need it (c itself first), with that count.
   bool df_ok = false;        // every chunk's producer list fits kMaxDeps

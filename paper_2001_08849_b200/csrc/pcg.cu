@@ -1026,318 +1026,6 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Lagged push SpMV (k_spmv_lag).  Same per-block work as k_spmv_df's phase 1 (row i forms
-// y'_i = sum_{j >= i} K_ij x_j from the TMA-streamed stored blocks and pushes K_ij^T x_i into the
-// slot of K_ji in row j's transposed list), but the row sums of the pushed slots ("phase 2") run
-// in the compute warps themselves, kLagL rounds behind phase 1: in round j a CTA does phase 1 of
-// its j-th chunk and phase 2 of its (j - kLagL)-th chunk, with the slot loads of phase 2 issued
-// in the same latency window as phase 1's x gathers.
-// Readiness is tracked per WAVE of the persistent grid (wave w = chunks [wG, (w+1)G) for G CTAs,
-// chunk c = blockIdx + wG): the producer rows of a chunk lie in chunks <= itself (row i < j), so
-// its phase 2 may run once its wave and every earlier wave has finished phase 1.  The loader warp
-// publishes each finished chunk with one release increment of its wave counter and, one round
-// ahead, clears the compute warps for the next round's phase 2 (acquire load of the wave counter
-// -> mbarrier).  This replaces the dataflow kernel's per-chunk producer lists, counter warp,
-// phase-2 warp and phase-2 buffers, so three CTAs fit on an SM (24 compute warps instead of 16).
-// Fixed summation order everywhere (per-lane item order, fixed group trees, p.q per thread in
-// chunk order, CTA partials in CTA order): bitwise reproducible for a given grid.
-#ifndef FSFEM_LAG_L
-#define FSFEM_LAG_L 2
-#endif
-#ifndef FSFEM_LAG_STAGES
-#define FSFEM_LAG_STAGES 2
-#endif
-#ifndef FSFEM_LAG_MINB
-#define FSFEM_LAG_MINB 3
-#endif
-constexpr int kLagL = FSFEM_LAG_L;          // rounds between a chunk's phase 1 and its phase 2
-constexpr int kLagS = FSFEM_LAG_STAGES;     // TMA ring depth
-constexpr int kLagP2 = 2;                   // slots per lane issued with the round's loads
-#ifndef FSFEM_LAG_ITEMS
-#define FSFEM_LAG_ITEMS 4
-#endif
-constexpr int kLagItems = FSFEM_LAG_ITEMS;  // phase-1 items per lane per round
-constexpr int kLagThreads = kThreads + 32;  // 8 compute warps + loader warp
-static_assert(kLagL >= 2 && kLagL <= 4, "a round's phase 2 is cleared while the previous round runs");
-static_assert(kLagS >= 2 && kLagS <= 4, "mbarrier header holds 3 * stages barriers");
-constexpr int kLagPst = (128 + 32 * kLagS + 127) / 128 * 128;  // barriers, stage infos
-constexpr int kLagSmem = 128 + kLagPst + kLagS * PushLayout::kBytes;
-
-__device__ __forceinline__ void red_release_add_u32(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <bool kPcg>
-__global__ void __launch_bounds__(kLagThreads, FSFEM_LAG_MINB) k_spmv_lag(
-    const SpmvChunk* __restrict__ chunks, int nchunks, const int64_t* __restrict__ sptr,
-    const int64_t* __restrict__ tptr, const int32_t* __restrict__ snbr, const int32_t* __restrict__ tpos,
-    const double* __restrict__ vals, uint32_t* lagw /*[0]: ticket, [1 + w]: wave w's finished chunks*/,
-    double* part, double* tbuf, const double* __restrict__ x, int64_t own_off, double* y, PcgState* st) {
-  static_assert(kChunkNodes <= kWarps * (32 / kGroupLanes), "one pass of the compute warps per chunk");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  pdl_trigger();
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [kLagS] stage loaded
-  uint64_t* empty = full + kLagS;                        // [kLagS] round done by every compute warp
-  uint64_t* okb = full + 2 * kLagS;                      // [kLagS] round's phase 2 cleared
-  PushInfo* pinfo = reinterpret_cast<PushInfo*>(smem + 128);
-  unsigned char* pst = smem + kLagPst;
-  __shared__ int sh_done;
-  __shared__ bool sh_last;
-  __shared__ double sh_red[32];
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < kLagS; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kWarps);
-      mbar_init(&okb[k], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_wait();
-  if (threadIdx.x == 0) sh_done = kPcg ? (ld_cg(&st->done_d) != 0.0) : 0;
-  __syncthreads();
-  if (sh_done) return;  // uniform over the grid
-  if (kPcg) spmv_time_start(st);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* xown = x + own_off;
-  const int G = gridDim.x;
-  const int K = nchunks > static_cast<int>(blockIdx.x) ? (nchunks - 1 - blockIdx.x) / G + 1 : 0;
-  const int J = K > 0 ? K + kLagL : 0;  // rounds
-  uint32_t* waves = lagw + 1;
-  double dot = 0.0;
-#ifndef FSFEM_LAG_TIMING
-#define FSFEM_LAG_TIMING 0
-#endif
-  long long tw_spin = 0, tw_ok = 0, tw_full = 0, tw_pub = 0;
-  const long long t_begin = FSFEM_LAG_TIMING ? clock64() : 0;
-#define LAG_T(acc, stmt)                                  \
-  if (FSFEM_LAG_TIMING) {                                 \
-    const long long ta_ = clock64();                      \
-    stmt;                                                 \
-    acc += clock64() - ta_;                               \
-  } else {                                                \
-    stmt;                                                 \
-  }
-  if (warp == kWarps) {
-    // ---------------- loader warp ----------------
-    if (lane == 0) {
-      for (int j = 0; j < kLagS && j < K; ++j)
-        issue_chunk_push(chunks[blockIdx.x + j * G], sptr, snbr, tpos, vals, xown, pst + j * PushLayout::kBytes,
-                         &full[j], &pinfo[j]);
-      if (J > 0) mbar_arrive(&okb[0]);  // round 0 has no phase 2 (cleared: armed = 1)
-    }
-    int armed = 1;  // rounds [0, armed) cleared for phase 2
-    for (int j = 0; j < J; ++j) {
-      const int sj = j % kLagS;
-      mbar_wait(&empty[sj], (j / kLagS) & 1);  // round j done: P1(chunk j), P2(chunk j - L)
-      if (lane == 0) {
-        if (j + kLagS < K) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_chunk_push(chunks[blockIdx.x + (j + kLagS) * G], sptr, snbr, tpos, vals, xown,
-                           pst + sj * PushLayout::kBytes, &full[sj], &pinfo[sj]);
-        }
-        // round j + 1 must be cleared before the next wait (its compute warps need it): the wave of
-        // its phase-2 chunk (and, by induction, every earlier one) has finished phase 1 everywhere
-        for (; armed <= j + 1 && armed < J; ++armed) {
-          const int w = armed - kLagL;
-          if (w >= 0) {
-            const uint32_t nw = static_cast<uint32_t>(min(G, nchunks - w * G));
-            LAG_T(tw_spin, while (ld_acquire_u32(waves + w) < nw) __nanosleep(20));
-          }
-          mbar_arrive(&okb[armed % kLagS]);
-        }
-        // publish: this CTA's chunk of wave j finished phase 1 (its pushes are visible)
-        if (j < K) LAG_T(tw_pub, red_release_add_u32(waves + j, 1u));
-        // clear round j + 2 already if its wave is complete (one probe, no wait), so that warps
-        // finishing round j + 1 early go on; its barrier was last waited on in round j + 2 - S <= j
-        if (armed == j + 2 && armed < J) {
-          const int w = armed - kLagL;
-          if (w < 0 || ld_acquire_u32(waves + w) >= static_cast<uint32_t>(min(G, nchunks - w * G))) {
-            mbar_arrive(&okb[armed % kLagS]);
-            ++armed;
-          }
-        }
-      }
-      armed = __shfl_sync(0xffffffffu, armed, 0);
-      // chunk j - L's pushed slots are dead: drop their whole L2 lines without write-back
-      if (j >= kLagL) {
-        const SpmvChunk ch = chunks[blockIdx.x + (j - kLagL) * G];
-        const uintptr_t lo = reinterpret_cast<uintptr_t>(tbuf + 3 * static_cast<int64_t>(ch.Pt0));
-        const uintptr_t hi = reinterpret_cast<uintptr_t>(tbuf + 3 * static_cast<int64_t>(ch.Pt1));
-        for (uintptr_t ad = ((lo + 127) & ~uintptr_t(127)) + 128 * lane; ad + 128 <= hi; ad += 128 * 32)
-          asm volatile("discard.global.L2 [%0], 128;" ::"l"(ad) : "memory");
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- compute warps ----------------
-    constexpr int G8 = kGroupLanes, NPW = 32 / kGroupLanes;
-    const int grp = lane / G8, gl = lane % G8;
-    const int m = warp * NPW + grp;  // this group's node inside every chunk
-    const uint64_t vpol = policy_evict_last();
-    // phase-2 queue of this group: own-node index (or -1) and slot range, kLagL rounds deep
-    int qn[kLagL], qe0[kLagL], qe1[kLagL];
-#pragma unroll
-    for (int l = 0; l < kLagL; ++l) qn[l] = -1, qe0[l] = 0, qe1[l] = 0;
-    for (int j = 0; j < J; ++j) {
-      const int s = j % kLagS;
-      // ---- phase 2 of chunk j - L: slot, y' and x loads first ----
-      const int nd = qn[0], e0 = qe0[0], e1 = qe1[0];
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, xq0 = 0.0, xq1 = 0.0, xq2 = 0.0;
-      double tv[kLagP2][3];
-      if (j >= kLagL) {
-        LAG_T(tw_ok, mbar_wait(&okb[s], (j / kLagS) & 1));
-#pragma unroll
-        for (int u = 0; u < kLagP2; ++u) {
-          const int e = e0 + gl + G8 * u;
-          tv[u][0] = tv[u][1] = tv[u][2] = 0.0;
-          if (e < e1) {
-            const double* pt = tbuf + 3 * static_cast<int64_t>(e);
-            tv[u][0] = __ldcg(pt);
-            tv[u][1] = __ldcg(pt + 1);
-            tv[u][2] = __ldcg(pt + 2);
-          }
-        }
-        if (nd >= 0 && gl == 0) {
-          const int64_t o = 3 * static_cast<int64_t>(nd);
-          t0 = __ldcg(y + o);  // y'_nd, stored by this thread kLagL rounds ago
-          t1 = __ldcg(y + o + 1);
-          t2 = __ldcg(y + o + 2);
-          xq0 = __ldg(xown + o);
-          xq1 = __ldg(xown + o + 1);
-          xq2 = __ldg(xown + o + 2);
-        }
-      }
-      // ---- phase 1 of chunk j ----
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      int new_n = -1, new_e0 = 0, new_e1 = 0;
-      int64_t il = 0;
-      bool act = false;
-      if (j < K) {
-        LAG_T(tw_full, mbar_wait(&full[s], (j / kLagS) & 1));
-        const unsigned char* stg = pst + s * PushLayout::kBytes;
-        const PushInfo in = pinfo[s];
-        const int64_t* sp = reinterpret_cast<const int64_t*>(stg + PushLayout::kPtr) + in.dptr;
-        const int32_t* sn = reinterpret_cast<const int32_t*>(stg + PushLayout::kSnbr) + in.dsn;
-        const int32_t* tq = reinterpret_cast<const int32_t*>(stg + PushLayout::kTp) + in.dtp;
-        const double* sv = reinterpret_cast<const double*>(stg + PushLayout::kVals) + in.dval;
-        const double* sx = reinterpret_cast<const double*>(stg + PushLayout::kXo) + in.dxo;
-        act = m < in.nn;
-        const int mm = act ? m : 0;
-        il = static_cast<int64_t>(in.n0) + mm;
-        if (act) {  // queue the node for phase 2 in round j + L
-          new_n = static_cast<int>(il);
-          new_e0 = static_cast<int>(__ldg(tptr + il));
-          new_e1 = static_cast<int>(__ldg(tptr + il + 1));
-        }
-        const int ls = act ? static_cast<int>(sp[m]) - in.Ps0 : 0;
-        const int nus = act ? 3 * static_cast<int>(sp[m + 1] - sp[m]) : 0;
-        const double xi0 = sx[3 * mm], xi1 = sx[3 * mm + 1], xi2 = sx[3 * mm + 2];
-        int rounds = (nus + G8 * kLagItems - 1) / (G8 * kLagItems);
-#pragma unroll 1
-        for (int o = G8; o < 32; o <<= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
-        for (int r = 0; r < rounds; ++r) {
-          double xs[kLagItems];
-#pragma unroll
-          for (int u = 0; u < kLagItems; ++u) {
-            const int k = G8 * (kLagItems * r + u) + gl;
-            xs[u] = 0.0;
-            if (k < nus) {
-              const int b = k / 3, cc = k - 3 * b;
-              xs[u] = ldg_vec(x + 3 * sn[ls + b] + cc, vpol);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kLagItems; ++u) {
-            const int k = G8 * (kLagItems * r + u) + gl;
-            if (k < nus) {
-              const int b = k / 3, cc = k - 3 * b;
-              const double* pb = sv + 9 * (ls + b) + cc;
-              const double v0 = pb[0], v1 = pb[3], v2 = pb[6];
-              s0 = fma(v0, xs[u], s0);
-              s1 = fma(v1, xs[u], s1);
-              s2 = fma(v2, xs[u], s2);
-              const int tp = tq[ls + b];
-              if (tp >= 0) tbuf[3 * static_cast<int64_t>(tp) + cc] = fma(v2, xi2, fma(v1, xi1, v0 * xi0));
-            }
-          }
-        }
-      }
-      // ---- phase 2 sums (slots in ascending order per lane), then both group trees ----
-      if (j >= kLagL) {
-#pragma unroll
-        for (int u = 0; u < kLagP2; ++u) {
-          t0 += tv[u][0];
-          t1 += tv[u][1];
-          t2 += tv[u][2];
-        }
-        for (int e = e0 + gl + G8 * kLagP2; e < e1; e += G8) {  // nodes with > 16 transposed blocks
-          const double* pt = tbuf + 3 * static_cast<int64_t>(e);
-          t0 += __ldcg(pt);
-          t1 += __ldcg(pt + 1);
-          t2 += __ldcg(pt + 2);
-        }
-      }
-#pragma unroll
-      for (int o = G8 / 2; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-        t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-      }
-      if (gl == 0) {
-        if (act) {  // y'_il (this thread reads it back in round j + L)
-          y[3 * il] = s0;
-          y[3 * il + 1] = s1;
-          y[3 * il + 2] = s2;
-        }
-        if (nd >= 0) {
-          const int64_t o = 3 * static_cast<int64_t>(nd);
-          st_vec(y + o, t0, vpol);
-          st_vec(y + o + 1, t1, vpol);
-          st_vec(y + o + 2, t2, vpol);
-          if (kPcg) dot = fma(xq0, t0, fma(xq1, t1, fma(xq2, t2, dot)));
-        }
-      }
-#pragma unroll
-      for (int l = 0; l + 1 < kLagL; ++l) qn[l] = qn[l + 1], qe0[l] = qe0[l + 1], qe1[l] = qe1[l + 1];
-      qn[kLagL - 1] = new_n;
-      qe0[kLagL - 1] = new_e0;
-      qe1[kLagL - 1] = new_e1;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-  }
-#if FSFEM_LAG_TIMING
-  if (lane == 0 && (warp == 0 || warp == kWarps) && (blockIdx.x % 37) == 0)
-    printf("lag blk %d %s K %d: total %lld spin %lld pub %lld okwait %lld fullwait %lld\n", blockIdx.x,
-           warp == kWarps ? "load" : "comp", K, clock64() - t_begin, tw_spin, tw_pub, tw_ok, tw_full);
-#endif
-  // p.q: per-thread sums in chunk order, CTA tree, CTA partials summed in CTA order by the last CTA
-  const double cta = block_sum(dot, sh_red);
-  if (threadIdx.x == 0) {
-    if (kPcg) part[blockIdx.x] = cta;
-    __threadfence();
-    sh_last = atomicAdd(lagw, 1u) == static_cast<uint32_t>(G) - 1u;
-  }
-  __syncthreads();
-  if (!sh_last) return;
-  __threadfence();
-  const int nwaves = (nchunks + G - 1) / G;
-  for (int w = threadIdx.x; w < nwaves; w += blockDim.x) waves[w] = 0u;  // every CTA is past its waits
-  if (kPcg) {
-    double a = 0.0;
-    for (int b = threadIdx.x; b < G; b += blockDim.x) a += ld_cg(part + b);
-    const double pq = block_sum(a, sh_red);
-    spmv_finish(st, pq);
-    if (threadIdx.x == 0) spmv_time_end(st);
-  }
-  if (threadIdx.x == 0) lagw[0] = 0u;
-}
-
 // Small meshes (fewer chunks than SMs: the configurations whose PCG is launch-latency bound):
 // a plain warp-per-node kernel without the TMA pipeline -- no mbarrier set-up, no staging, one
 // node per warp with all its loads issued directly.  Same items and fixed warp-tree order as
@@ -1816,18 +1504,6 @@ int df_grid() {
   return g;
 }
 
-int lag_grid() {
-  static int g = 0;
-  if (g == 0) {
-    int per_sm = 0;
-    FS_CUDA(cudaFuncSetAttribute(k_spmv_lag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLagSmem));
-    FS_CUDA(cudaFuncSetAttribute(k_spmv_lag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLagSmem));
-    FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_lag<true>, kLagThreads, kLagSmem));
-    g = std::max(1, per_sm) * num_sms();
-  }
-  return g;
-}
-
 int spmv_grid(int64_t nchunks) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(FSFEM_SPMV_MINB * num_sms(), nchunks)));
 }
@@ -1840,9 +1516,7 @@ int spmv_kind(const Pattern& pat) {
   static int forced = -1;
   if (forced < 0) {
     const char* e = std::getenv("FSFEM_SPMV_KERNEL");
-    forced = !e ? 0
-                : (std::strcmp(e, "gather") == 0 ? 1
-                                                 : (std::strcmp(e, "dataflow") == 0 ? 2 : (std::strcmp(e, "lag") == 0 ? 3 : 0)));
+    forced = !e ? 0 : (std::strcmp(e, "gather") == 0 ? 1 : (std::strcmp(e, "dataflow") == 0 ? 2 : 0));
     FS_CUDA(cudaFuncSetAttribute(k_spmv_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
     FS_CUDA(cudaFuncSetAttribute(k_spmv_df<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDfSmem));
   }
@@ -1850,9 +1524,7 @@ int spmv_kind(const Pattern& pat) {
 #define FSFEM_SMALL_CHUNKS_PER_SM 1
 #endif
   if (pat.nchunks < FSFEM_SMALL_CHUNKS_PER_SM * num_sms()) return 0;
-  if (forced == 1) return 1;
-  if (forced == 3) return 3;
-  if (!pat.df_ok) return 1;
+  if (forced == 1 || !pat.df_ok) return 1;
   if (forced == 2) return 2;
   return pat.nchunks >= static_cast<int64_t>(kDfMinChunksPerCta) * df_grid() ? 2 : 1;
 }
@@ -1872,35 +1544,6 @@ void launch_spmv(const Pattern& pat, const double* vals, const double* x_full, i
     kern<<<g, kThreads, 0, s>>>(pat.sptr.get(), pat.snbr.get(), pat.tptr.get(), pat.tlist.get(), vals, pat.nloc, x_full,
                                 own_off, y, st, part);
     FS_LAUNCH_CHECK();
-    return;
-  }
-  if (spmv_kind(pat) == 3) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(std::max(1, std::min(nch, lag_grid())));
-    cfg.blockDim = dim3(kLagThreads);
-    cfg.dynamicSmemBytes = kLagSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;  // rounds wait for other CTAs' waves
-    attr[0].val.cooperative = FSFEM_COOP;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = FSFEM_PDL ? 2 : 1;
-    const SpmvChunk* chp = pat.chunks.get();
-    const int64_t* spp = pat.sptr.get();
-    const int64_t* tpp = pat.tptr.get();
-    const int32_t* snp = pat.snbr.get();
-    const int32_t* tps = pat.tpos.get();
-    uint32_t* lw = pat.lagw.get();
-    double* tb = pat.tbuf.get();
-    if (pcg)
-      FS_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_lag<true>, chp, nch, spp, tpp, snp, tps, vals, lw, part, tb, x_full,
-                                 own_off, y, st));
-    else
-      FS_CUDA(cudaLaunchKernelEx(&cfg, k_spmv_lag<false>, chp, nch, spp, tpp, snp, tps, vals, lw, part, tb, x_full,
-                                 own_off, y, st));
-    count_launch();
     return;
   }
   if (spmv_kind(pat) == 2) {

@@ -597,8 +597,6 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   pat.ndeps.ensure(std::max<int64_t>(pat.nchunks, 1));
   pat.cflags.ensure(std::max<int64_t>(pat.nchunks, 1));
   pat.sync.ensure(2);
-  pat.lagw.ensure(pat.nchunks + 2);
-  FS_CUDA(cudaMemsetAsync(pat.lagw.get(), 0, sizeof(uint32_t) * (pat.nchunks + 2), s));
   FS_CUDA(cudaMemsetAsync(pat.tpos.get(), 0xff, sizeof(int32_t) * (pat.nsb + 4), s));
   FS_CUDA(cudaMemsetAsync(pat.cflags.get(), 0, sizeof(uint32_t) * std::max<int64_t>(pat.nchunks, 1), s));
   FS_CUDA(cudaMemsetAsync(pat.sync.get(), 0, sizeof(uint32_t) * 2, s));

@@ -73,7 +73,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("kernel", ["gather", "dataflow", "lag"])
+@pytest.mark.parametrize("kernel", ["gather", "dataflow"])
 def test_halo_cfg3_large_kernels(kernel):
     env = dict(os.environ, FSFEM_SPMV_KERNEL=kernel)
     out = subprocess.run([sys.executable, "-c", _SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"), nranks=2)],

@@ -1,9 +1,7 @@
-"""The large-mesh SpMV kernels of pcg.cu against the oracle, whichever the library picks by default.
+"""Both large-mesh SpMV kernels of pcg.cu against the oracle, whichever the library picks by default.
 
-`k_spmv` (gather: K_ji read transposed from row j), `k_spmv_df` (dataflow push: row i pushes
-K_ij^T x_i, row j sums its slots once the producer chunks are done) and `k_spmv_lag` (lagged
-push: the slot sums run in the compute warps a fixed number of rounds behind, gated per wave of
-the persistent grid) are selected with
+`k_spmv` (gather: K_ji read transposed from row j) and `k_spmv_df` (dataflow push: row i pushes
+K_ij^T x_i, row j sums its slots once the producer chunks are done) are selected with
 FSFEM_SPMV_KERNEL, read once per process, so each case runs in its own interpreter.  Checked:
 K x against the oracle's CSR product (1e-12 relative to max|K x|), the cfg3 solve against the
 oracle's full solve, and run-to-run bitwise equality (every sum has a fixed order in both).
@@ -50,7 +48,7 @@ def _run(kernel, cfg, tmp_path):
     return np.load(out)
 
 
-@pytest.mark.parametrize("kernel", ["gather", "dataflow", "lag"])
+@pytest.mark.parametrize("kernel", ["gather", "dataflow"])
 def test_spmv_kernel_cfg3(kernel, tmp_path):
     from fsfem_inputs import config_mesh
     from oracle import Oracle
@@ -70,15 +68,14 @@ def test_spmv_kernel_cfg3(kernel, tmp_path):
     assert np.array_equal(r["y0"], r["y1"]) and np.array_equal(r["u0"], r["u1"]) and r["it"][0] == r["it"][1]
 
 
-def test_gather_and_push_kernels_agree_cfg4(tmp_path):
-    """cfg4 (bench workload): the three kernels give the same K x to rounding (different, fixed
+def test_gather_and_dataflow_agree_cfg4(tmp_path):
+    """cfg4 (bench workload): the two kernels give the same K x to rounding (different, fixed
     summation orders) and solutions within the parity bar of each other."""
     a = _run("gather", 4, tmp_path)
-    for k in ("dataflow", "lag"):
-        b = _run(k, 4, tmp_path)
-        assert np.abs(a["y0"] - b["y0"]).max() <= 1e-12 * np.abs(a["y0"]).max()
-        assert np.linalg.norm(a["u0"] - b["u0"]) <= 1e-7 * np.linalg.norm(a["u0"])
-        assert np.array_equal(b["y0"], b["y1"]) and np.array_equal(b["u0"], b["u1"])
+    b = _run("dataflow", 4, tmp_path)
+    assert np.abs(a["y0"] - b["y0"]).max() <= 1e-12 * np.abs(a["y0"]).max()
+    assert np.linalg.norm(a["u0"] - b["u0"]) <= 1e-7 * np.linalg.norm(a["u0"])
+    assert np.array_equal(b["y0"], b["y1"]) and np.array_equal(b["u0"], b["u1"])
 
 
 _PART_SCRIPT = r"""
@@ -109,7 +106,7 @@ np.savez({out!r}, **res)
 """
 
 
-@pytest.mark.parametrize("kernel", ["gather", "dataflow", "lag"])
+@pytest.mark.parametrize("kernel", ["gather", "dataflow"])
 def test_spmv_kernel_row_partition(kernel, tmp_path):
     """Partition-only contexts (2 and 3 ranks' rows on one GPU, halo columns below the rank's
     range stored in the rows): each rank's rows of K x equal the single-context product."""
@@ -119,7 +116,7 @@ def test_spmv_kernel_row_partition(kernel, tmp_path):
     r = np.load(out)
     full = r["full"]
     n_nodes = full.size // 3
-    want = {"gather": 1, "dataflow": 2, "lag": 3}[kernel]
+    want = 1 if kernel == "gather" else 2
     for nranks in (2, 3):
         rng = r[f"r{nranks}"]
         for k in range(nranks):

@@ -378,7 +378,7 @@ def run_gpu(args):
             "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms, "launches_timed": spmv_n,
             "peak_kind": peak_kind, "launches_per_step": iters + 1,
             "share_of_step": spmv_dev_ms / max(spmv_dev_n, 1) * (iters + 1) / (ms / args.steps),
-            "timing": "CUDA events around the first SpMV of every 32-iteration CUDA-graph batch, live in the timed steps",
+            "timing": "CUDA events around the second SpMV of every 32-iteration CUDA-graph batch (after an update kernel, like every SpMV but the batch's first), live in the timed steps",
             "device_timer": {"avg_launch_ms": spmv_dev_avg_ms, "launches": spmv_dev_n,
                              "achieved": spmv_bytes / (max(spmv_dev_avg_ms, 1e-12) / 1e3) / 1e9,
                              "frac": spmv_bytes / (max(spmv_dev_avg_ms, 1e-12) / 1e3) / 1e9 / peak,

@@ -23,10 +23,10 @@ namespace fsfem {
 // kernels' host drivers (faces.cu, symbolic.cu, assemble.cu, bc.cu)
 void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, int64_t nt, cudaStream_t s,
                         DevBuf<unsigned char>& scratch, DevBuf<int32_t>& face_nodes, DevBuf<int32_t>& face_tet,
-                        DevBuf<int32_t>& face_opp, DevBuf<int32_t>& tet_face, int64_t* n_faces, int64_t* n_interior,
-                        unsigned long long* h_flags);
-void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
-                          const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
+                        DevBuf<int32_t>& face_opp, DevBuf<int32_t>& tet_face, DevBuf<int32_t>& tet_across,
+                        int64_t* n_faces, int64_t* n_interior, unsigned long long* h_flags);
+void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* tet_across,
+                          int64_t n_lo, int64_t nloc, cudaStream_t s,
                           DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags, int fem);
 void export_csr_device(const Pattern& pat, const double* svals, int64_t* row_ptr, int32_t* col_idx, double* vals,
                        cudaStream_t s);
@@ -197,6 +197,7 @@ struct fsfem_ctx {
   DevBuf<double> xyz;
   DevBuf<int32_t> tets;
   DevBuf<int32_t> face_nodes, face_tet, face_opp, tet_face;
+  DevBuf<int32_t> tet_across;  // [4 nt] vertex across face l of tet t (-1: boundary), for the pattern
   // pattern (symmetric block storage, pattern.cuh)
   bool have_pattern = false;
   Pattern pat;
@@ -959,7 +960,7 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
     int64_t nf = 0, ni = 0;
     c->h_flags[0] = kNoError;
     build_faces_device(c->xyz.get(), n_nodes, c->tets.get(), n_tets, c->stream, c->scratch, c->face_nodes, c->face_tet,
-                       c->face_opp, c->tet_face, &nf, &ni, c->h_flags);
+                       c->face_opp, c->tet_face, c->tet_across, &nf, &ni, c->h_flags);
     fsfem_status s = decode_flags(c, c->h_flags[0], "build_faces");
     if (s != FSFEM_OK) return s;
     PhaseTimer pt(c->stream, "faces");
@@ -988,18 +989,21 @@ fsfem_status fsfem_build_faces(fsfem_ctx* c, const double* xyz, int64_t n_nodes,
       DevBuf<double> xyz_i;
       xyz_i.ensure(3 * n_nodes);
       permute_rows_device(c->iperm.get(), c->xyz.get(), xyz_i.get(), n_nodes, 3, true, c->stream);
-      DevBuf<int32_t> tets_i, fn_i, fo_i;
+      DevBuf<int32_t> tets_i, fn_i, fo_i, ta_i;
       tets_i.ensure(4 * n_tets);
       fn_i.ensure(3 * nf);
       fo_i.ensure(2 * nf);
+      ta_i.ensure(4 * n_tets);
       perm_ids_device(c->perm.get(), c->tets.get(), tets_i.get(), 4 * n_tets, c->stream);
       perm_ids_device(c->perm.get(), c->face_nodes.get(), fn_i.get(), 3 * nf, c->stream);
       perm_ids_device(c->perm.get(), c->face_opp.get(), fo_i.get(), 2 * nf, c->stream);
+      perm_ids_device(c->perm.get(), c->tet_across.get(), ta_i.get(), 4 * n_tets, c->stream);
       FS_CUDA(cudaStreamSynchronize(c->stream));
       swap_buf(c->xyz, xyz_i);
       swap_buf(c->tets, tets_i);
       swap_buf(c->face_nodes, fn_i);
       swap_buf(c->face_opp, fo_i);
+      swap_buf(c->tet_across, ta_i);
       c->reordered = true;
     }
     c->rep.reordered = c->reordered ? 1 : 0;
@@ -1044,8 +1048,8 @@ fsfem_status fsfem_assemble_csr(fsfem_ctx* c, double E, double nu, int64_t* row_
     if (!c->have_pattern) {
       FS_CUDA(cudaEventRecord(c->ev0, c->stream));
       c->h_flags[0] = kNoError;
-      build_pattern_device(c->tets.get(), c->nt, c->tet_face.get(), c->face_tet.get(), c->face_opp.get(), c->n_lo,
-                           c->nloc, c->stream, c->scratch, c->pat, c->h_flags, c->method == FSFEM_METHOD_FEM_T4);
+      build_pattern_device(c->tets.get(), c->nt, c->tet_face.get(), c->tet_across.get(), c->n_lo, c->nloc, c->stream,
+                           c->scratch, c->pat, c->h_flags, c->method == FSFEM_METHOD_FEM_T4);
       fsfem_status s = decode_flags(c, c->h_flags[0], "symbolic");
       if (s != FSFEM_OK) return s;
       const bool tet = c->method == FSFEM_METHOD_FEM_T4;
@@ -1337,10 +1341,12 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
       FS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       set_capturing(true);
       try {
-        // the first SpMV of every batch is bracketed by events (a live per-launch sample); an event
-        // pair around every SpMV would cost ~14 us per iteration at cfg4
+        // the second SpMV of every batch is bracketed by events (a live per-launch sample that
+        // follows an update kernel, as every SpMV but the batch's first does; the first one also
+        // carries the graph's launch latency); an event pair around every SpMV would cost ~14 us
+        // per iteration at cfg4
         for (int it = 0; it < kBatch; ++it)
-          pcg_iteration(cs, it == 0 ? c->spmv_ev[0] : nullptr, it == 0 ? c->spmv_ev[1] : nullptr);
+          pcg_iteration(cs, it == 1 ? c->spmv_ev[0] : nullptr, it == 1 ? c->spmv_ev[1] : nullptr);
       } catch (...) {
         set_capturing(false);
         cudaStreamEndCapture(c->stream, &g);
@@ -1374,7 +1380,7 @@ fsfem_status fsfem_pcg_solve(fsfem_ctx* c, double* u, int u0_is_zero, double rel
           FS_CUDA(cudaGraphLaunch(c->graph, c->stream));
           count_launch(c->graph_launches);
           read_state();
-          if (c0->h_st->iters > before) {  // the sampled SpMV (iteration 0 of the batch) ran
+          if (c0->h_st->iters > before + 1) {  // the sampled SpMV (iteration 1 of the batch) ran
             ev_ms += elapsed(c->spmv_ev[0], c->spmv_ev[1]);
             ++ev_n;
           }

@@ -293,21 +293,41 @@ __device__ int cta_excl_scan(int v, int* total) {
   return base + inc - v;
 }
 
-__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1;
-    else hi = mid;
+// Slot of x in the open-addressing set keys[0..mask] (inserted if absent).
+__device__ __forceinline__ int hinsert_at(int32_t* keys, unsigned mask, int32_t x) {
+  unsigned h = hslot(x, mask);
+  for (;;) {
+    const int32_t old = atomicCAS(&keys[h], -1, x);
+    if (old == -1 || old == x) return static_cast<int>(h);
+    h = (h + 1) & mask;
   }
-  return lo;
 }
+// idx of x, or -1 if x is not in the set (an empty slot ends the probe: no deletions).
+__device__ __forceinline__ int hfind_or(const int32_t* keys, const int32_t* idx, unsigned mask, int32_t x) {
+  unsigned h = hslot(x, mask);
+  for (unsigned n = 0; n <= mask; ++n) {
+    const int32_t k = keys[h];
+    if (k == x) return idx[h];
+    if (k == -1) return -1;
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
+// Shared memory of the builder (int32 words unless noted).
+constexpr int kStStride = 256;  // slot table row stride (local vertex ids < kMaxVerts < 256)
+constexpr int kBldSmem = static_cast<int>(sizeof(int32_t)) *
+                             (2 * kHashD + kMaxDom + 2 * kHashV + kMaxVerts + kTileRows + 2 * (kMaxBlk + 1) +
+                              2 * kMaxTask) +
+                         al16(5 * kMaxDom) + 2 * kTileRows * kStStride;
 
 // One CTA per tile, one pass: the blob at blob + t * kBlobCap and its size into size[t] (or
 // -1 = too big for the caps: split the tile, -2 = a single row that cannot fit: UNSUPPORTED).
 // The tile's domains and vertices are collected in shared-memory hash sets: their local numbering
 // is arbitrary (it only names shared-memory slots), while every summation order is fixed by the
-// rows' ascending domain lists F(i).
+// rows' ascending domain lists F(i).  The tile rows enter the vertex set first with local ids
+// 0..nrows-1; the slot of stored column J in row r comes from a table indexed by J's local id
+// (filled from the rows' stored column lists), not from a search of the global list.
 __global__ void __launch_bounds__(kBldThreads) k_tile_build(
     const int32_t* __restrict__ order, const int2* __restrict__ trange, const int32_t* __restrict__ which,
     int64_t nwork, const int64_t* __restrict__ nf_ptr, const int32_t* __restrict__ nf_idx, const int32_t* __restrict__ rec_a,
@@ -317,56 +337,78 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
   int32_t* HK = reinterpret_cast<int32_t*>(bsm);  // [kHashD] domain keys
   int32_t* HI = HK + kHashD;                       // [kHashD] local domain index
   int32_t* U = HI + kHashD;                        // [kMaxDom] local -> domain id
-  int32_t* F5 = U + kMaxDom;                       // [kMaxDom * 5] field nodes
-  int32_t* VK = F5 + 5 * kMaxDom;                  // [kHashV] vertex keys
-  int32_t* VI = VK + kHashV;                       // [kHashV] local vertex index
+  int32_t* VK = U + kMaxDom;                       // [kHashV] vertex keys
+  int32_t* VI = VK + kHashV;                       // [kHashV] local vertex index (-1: not numbered yet)
   int32_t* VL = VI + kHashV;                       // [kMaxVerts + kTileRows] local -> node id
   int32_t* bcnt = VL + kMaxVerts + kTileRows;      // [kMaxBlk + 1] entries per block
   int32_t* cur = bcnt + kMaxBlk + 1;               // [kMaxBlk + 1] entry offsets / cursors
   int32_t* tkey = cur + kMaxBlk + 1;               // [kMaxTask] task keys (count, index)
   int32_t* tinfo = tkey + kMaxTask;                // [kMaxTask] row << 24 | sub-list << 16 | slot
+  unsigned char* FV = reinterpret_cast<unsigned char*>(tinfo + kMaxTask);      // [kMaxDom][5] local vertices
+  uint16_t* ST = reinterpret_cast<uint16_t*>(FV + al16(5 * kMaxDom));          // [kTileRows][kStStride] slots
   __shared__ int32_t rnode[kTileRows], ril[kTileRows], rds[kTileRows], rsd[kTileRows], rbb[kTileRows + 1];
   __shared__ int64_t rP[kTileRows], rF[kTileRows + 1];
   __shared__ int sh_flag, sh_ntask, sh_nent, sh_nv;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
     const int64_t t = which ? which[wi] : wi;  // tile t = own rows order[trange[t].x, trange[t].y)
-    const int nrows = trange[t].y - trange[t].x;
-    if (threadIdx.x == 0) {
-      int64_t fsum = 0;
-      int bb = 0;
-      for (int r = 0; r < nrows; ++r) {
-        const int32_t il = order[trange[t].x + r];
-        ril[r] = il;
-        rnode[r] = static_cast<int32_t>(n_lo + il);
-        rP[r] = sptr[il];
-        rds[r] = static_cast<int32_t>(sptr[il + 1] - sptr[il]);
-        rsd[r] = rds[r] > 0 ? sdiag[il] : -1;
-        rbb[r] = bb;
-        bb += rds[r];
-        rF[r] = fsum;
-        fsum += nf_ptr[il + 1] - nf_ptr[il];
+    const int2 trg = trange[t];
+    const int nrows = trg.y - trg.x;
+    if (w == 0) {  // rows: lane r loads row r, lane scans give the block / domain-list offsets
+      int ds = 0;
+      int64_t nfr = 0;
+      if (lane < nrows) {
+        const int32_t il = order[trg.x + lane];
+        const int64_t P = sptr[il];
+        ds = static_cast<int>(sptr[il + 1] - P);
+        nfr = nf_ptr[il + 1] - nf_ptr[il];
+        ril[lane] = il;
+        rnode[lane] = static_cast<int32_t>(n_lo + il);
+        rP[lane] = P;
+        rds[lane] = ds;
+        rsd[lane] = ds > 0 ? sdiag[il] : -1;
       }
-      rbb[nrows] = bb;
-      rF[nrows] = fsum;
-      sh_flag = (fsum > kDiagCap || bb > kMaxBlk) ? 1 : 0;
-      sh_nv = 0;
+      int bb = ds;
+      int64_t fs = nfr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, bb, o);
+        const int64_t z = __shfl_up_sync(0xffffffffu, fs, o);
+        if (lane >= o) {
+          bb += y;
+          fs += z;
+        }
+      }
+      if (lane < nrows) {
+        rbb[lane] = bb - ds;
+        rF[lane] = fs - nfr;
+      }
+      if (lane == 31) {
+        rbb[nrows] = bb;
+        rF[nrows] = fs;
+        sh_flag = (fs > kDiagCap || bb > kMaxBlk) ? 1 : 0;
+        sh_nv = nrows;
+      }
     }
     for (int k = threadIdx.x; k < kHashD; k += blockDim.x) HK[k] = -1;
-    for (int k = threadIdx.x; k < kHashV; k += blockDim.x) VK[k] = -1;
+    for (int k = threadIdx.x; k < kHashV; k += blockDim.x) {
+      VK[k] = -1;
+      VI[k] = -1;
+    }
     __syncthreads();
     if (sh_flag) {
       if (threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
       __syncthreads();
       continue;
     }
-    // domains: hash set of the rows' lists, then a local numbering of the occupied slots
+    // domains: hash set of the rows' lists; the rows enter the vertex set with local ids 0..nrows-1
     const int nA = static_cast<int>(rF[nrows]);
     for (int k = threadIdx.x; k < nA; k += blockDim.x) {
       int r = 0;
       while (rF[r + 1] <= k) ++r;
       hinsert(HK, kHashD - 1, nf_idx[nf_ptr[ril[r]] + (k - rF[r])]);
     }
+    if (threadIdx.x < nrows) VI[hinsert_at(VK, kHashV - 1, rnode[threadIdx.x])] = threadIdx.x;
     __syncthreads();
     int ndom = 0;
     {
@@ -393,74 +435,79 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       int32_t fld[5];
       field_of(rec_a, rec_b, tet, U[k], fld);
 #pragma unroll
-      for (int p = 0; p < 5; ++p) {
-        F5[5 * k + p] = fld[p];
-        // the set stays at most half full (a tile with more vertices is split anyway)
+      for (int p = 0; p < 5; ++p)  // the set stays at most half full (a tile with more is split)
         if (fld[p] >= 0 && sh_nv < kHashV / 2 && hinsert(VK, kHashV - 1, fld[p])) atomicAdd(&sh_nv, 1);
-      }
     }
-    for (int r = threadIdx.x; r < nrows; r += blockDim.x)
-      if (hinsert(VK, kHashV - 1, rnode[r])) atomicAdd(&sh_nv, 1);
     __syncthreads();
     if (sh_nv >= kHashV / 2) {
       if (threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
       __syncthreads();
       continue;
     }
-    // vertices: tile rows first (local r), the others after them
+    // vertices: tile rows first (local r, already numbered), the others after them
     int nverts = 0;
     {
       constexpr int per = kHashV / kBldThreads;
       int c = 0;
-      auto row_of = [&](int32_t v) {
-        for (int r = 0; r < nrows; ++r)
-          if (rnode[r] == v) return r;
-        return -1;
-      };
       for (int q = 0; q < per; ++q) {
-        const int32_t v = VK[threadIdx.x * per + q];
-        c += (v >= 0 && row_of(v) < 0) ? 1 : 0;
+        const int h = threadIdx.x * per + q;
+        c += (VK[h] >= 0 && VI[h] < 0) ? 1 : 0;
       }
       int no = 0;
       int base = nrows + cta_excl_scan(c, &no);
       for (int q = 0; q < per; ++q) {
         const int h = threadIdx.x * per + q;
-        const int32_t v = VK[h];
-        if (v < 0) continue;
-        const int r = row_of(v);
-        if (r >= 0) {
-          VI[h] = r;
-        } else {
+        if (VK[h] >= 0 && VI[h] < 0) {
           VI[h] = base;
-          if (base < kMaxVerts + kTileRows) VL[base] = v;
+          if (base < kMaxVerts + kTileRows) VL[base] = VK[h];
           ++base;
         }
       }
       for (int r = threadIdx.x; r < nrows; r += blockDim.x) VL[r] = rnode[r];
       nverts = nrows + no;
     }
-    // entries per stored block: off-diagonal (i, J): one per domain of F(i) holding J (stored J);
-    // diagonal: one per domain of F(i).  Warp per row, lane per domain.
+    __syncthreads();
+    if (nverts > kMaxVerts) {
+      if (threadIdx.x == 0) size[t] = -(nrows > 1 ? 1 : 2);
+      __syncthreads();
+      continue;
+    }
+    // local vertices of every domain's field positions; slot table of the rows' stored columns
+    for (int k = threadIdx.x; k < ndom; k += blockDim.x) {
+      int32_t fld[5];
+      field_of(rec_a, rec_b, tet, U[k], fld);
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        const int v = fld[p] >= 0 ? hfind_or(VK, VI, kHashV - 1, fld[p]) : -1;
+        FV[5 * k + p] = static_cast<unsigned char>(v >= 0 ? v : 255);
+      }
+    }
+    for (int r = w; r < nrows; r += kBldThreads / 32) {
+      const int64_t P = rP[r];
+      for (int s = lane; s < rds[r]; s += 32) {
+        const int v = hfind_or(VK, VI, kHashV - 1, snbr[P + s]);
+        if (v >= 0) ST[r * kStStride + v] = static_cast<uint16_t>(s);
+      }
+    }
     for (int b = threadIdx.x; b <= kMaxBlk; b += blockDim.x) bcnt[b] = 0;
     __syncthreads();
+    // entries per stored block: off-diagonal (i, J): one per domain of F(i) holding J (stored J);
+    // diagonal: one per domain of F(i).  Warp per row, lane per domain.
     for (int r = w; r < nrows; r += kBldThreads / 32) {
       const int32_t i = rnode[r];
       const int64_t fb = nf_ptr[ril[r]];
       const int len = static_cast<int>(rF[r + 1] - rF[r]);
-      const int64_t P = rP[r];
-      const int ds = rds[r];
       for (int k0 = 0; k0 < len; k0 += 32) {
         const int k = k0 + lane;
         if (k < len) {
           const int kl = hfind(HK, HI, kHashD - 1, nf_idx[fb + k]);
-          int pi = 0;
-#pragma unroll
-          for (int p = 0; p < 5; ++p) pi = F5[5 * kl + p] == i ? p : pi;
 #pragma unroll
           for (int q = 0; q < 5; ++q) {
-            const int32_t J = F5[5 * kl + q];
-            if (J < 0 || (J < i && J >= n_lo)) continue;
-            const int slot = q == pi ? rsd[r] : lower_bound_i32(snbr + P, ds, J);
+            const int v = FV[5 * kl + q];
+            if (v == 255) continue;
+            const int32_t J = VL[v];
+            if (J < i && J >= n_lo) continue;
+            const int slot = v == r ? rsd[r] : ST[r * kStStride + v];
             atomicAdd(&bcnt[rbb[r] + slot], 1);
           }
         }
@@ -534,10 +581,7 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
     for (int r = threadIdx.x; r < nrows; r += blockDim.x)
       reinterpret_cast<TileRow*>(bl + L.o_rows)[r] = TileRow{rP[r], ril[r], rsd[r]};
     for (int v = threadIdx.x; v < nverts; v += blockDim.x) reinterpret_cast<int32_t*>(bl + L.o_verts)[v] = VL[v];
-    for (int k = threadIdx.x; k < 5 * ndom; k += blockDim.x) {
-      const int32_t v = F5[k];
-      bl[L.o_fv + k] = static_cast<unsigned char>(v >= 0 ? hfind(VK, VI, kHashV - 1, v) : 255);
-    }
+    for (int k = threadIdx.x; k < 5 * ndom; k += blockDim.x) bl[L.o_fv + k] = FV[k];
     {
       TileTask* tasks = reinterpret_cast<TileTask*>(bl + L.o_task);
       for (int a = threadIdx.x; a < ntask; a += blockDim.x) {  // rank sort (keys are distinct)
@@ -569,7 +613,6 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
       const int32_t i = rnode[r];
       const int64_t fb = nf_ptr[ril[r]];
       const int len = static_cast<int>(rF[r + 1] - rF[r]);
-      const int64_t P = rP[r];
       const int ds = rds[r];
       for (int k0 = 0; k0 < len; k0 += 32) {
         const int k = k0 + lane;
@@ -578,12 +621,14 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
           kl = hfind(HK, HI, kHashD - 1, nf_idx[fb + k]);
           int pi = 0;
 #pragma unroll
-          for (int p = 0; p < 5; ++p) pi = F5[5 * kl + p] == i ? p : pi;
+          for (int p = 0; p < 5; ++p) pi = FV[5 * kl + p] == r ? p : pi;
 #pragma unroll
           for (int q = 0; q < 5; ++q) {
-            const int32_t J = F5[5 * kl + q];
-            if (J < 0 || (J < i && J >= n_lo)) continue;
-            tslot[q] = q == pi ? rsd[r] : lower_bound_i32(snbr + P, ds, J);
+            const int v = FV[5 * kl + q];
+            if (v == 255) continue;
+            const int32_t J = VL[v];
+            if (J < i && J >= n_lo) continue;
+            tslot[q] = v == r ? rsd[r] : ST[r * kStStride + v];
             tcode[q] = 5 * pi + q;
           }
         }
@@ -1058,8 +1103,7 @@ void build_assembly_tiles(Pattern& pat, const double* xyz, const int32_t* rec_a,
   for (int64_t a = 0; a < nloc; a += kTileRows) ts.push_back(static_cast<int32_t>(a));
   ts.push_back(static_cast<int32_t>(nloc));
   static bool attr = false;
-  const int bsmem = static_cast<int>(sizeof(int32_t) * (2 * kHashD + kMaxDom + 5 * kMaxDom + 2 * kHashV + kMaxVerts +
-                                                       kTileRows + 2 * (kMaxBlk + 1) + 2 * kMaxTask));
+  const int bsmem = kBldSmem;
   if (!attr) {
     FS_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
     FS_CUDA(cudaFuncSetAttribute(k_asm_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem));

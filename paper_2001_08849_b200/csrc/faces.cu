@@ -195,6 +195,35 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_bucket_sort(const int32_t* 
       }
       continue;
     }
+    if (n <= 32) {  // one instance per lane: bitonic network on (key, payload) in registers
+      unsigned long long k = lane < n ? keys[beg + lane] : ~0ull;
+      uint32_t p = lane < n ? pay[beg + lane] : 0xffffffffu;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+          const unsigned long long ko = __shfl_xor_sync(0xffffffffu, k, j);
+          const uint32_t po = __shfl_xor_sync(0xffffffffu, p, j);
+          const bool keep_min = ((lane & j) == 0) == ((lane & size) == 0);
+          const bool other_less = key_less(ko, po, k, p);
+          if (keep_min ? other_less : !other_less) {
+            k = ko;
+            p = po;
+          }
+        }
+      }
+      if (lane < n) {
+        keys[beg + lane] = k;
+        pay[beg + lane] = p;
+      }
+      const unsigned long long k1 = __shfl_up_sync(0xffffffffu, k, 1), k2 = __shfl_up_sync(0xffffffffu, k, 2);
+      const bool start = lane < n && (lane == 0 || k1 != k);
+      const bool too_long = lane < n && lane >= 2 && k2 == k;
+      const int starts = __popc(__ballot_sync(0xffffffffu, start));
+      if (__any_sync(0xffffffffu, too_long) && lane == 0) report_error(err, FSFEM_ERR_TOPOLOGY, a);
+      if (lane == 0) ucnt[a] = starts;
+      continue;
+    }
     for (int i = lane; i < n; i += 32) {
       sk[w][i] = keys[beg + i];
       sp[w][i] = pay[beg + i];
@@ -253,6 +282,7 @@ __global__ void __launch_bounds__(256) k_face_emit(const int32_t* __restrict__ o
                                                    const uint32_t* __restrict__ pay, const int32_t* __restrict__ tets,
                                                    int32_t* __restrict__ face_nodes, int32_t* __restrict__ face_tet,
                                                    int32_t* __restrict__ face_opp, int32_t* __restrict__ tet_face,
+                                                   int32_t* __restrict__ tet_across,
                                                    unsigned long long* __restrict__ n_interior) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -290,10 +320,13 @@ __global__ void __launch_bounds__(256) k_face_emit(const int32_t* __restrict__ o
           if (knext == k) {
             face_tet[2 * fid + 1] = static_cast<int32_t>(pnext >> 2);
             face_opp[2 * fid + 1] = tets[pnext];
+            tet_across[p] = tets[pnext];  // the vertex across face l of tet t, seen from each side
+            tet_across[pnext] = tets[p];
             ++interior;
           } else {
             face_tet[2 * fid + 1] = -1;
             face_opp[2 * fid + 1] = -1;
+            tet_across[p] = -1;
           }
         }
       }
@@ -309,8 +342,8 @@ __global__ void __launch_bounds__(256) k_face_emit(const int32_t* __restrict__ o
 // Host driver of S1.  All device buffers belong to the context.
 void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, int64_t nt, cudaStream_t s,
                         DevBuf<unsigned char>& scratch, DevBuf<int32_t>& face_nodes, DevBuf<int32_t>& face_tet,
-                        DevBuf<int32_t>& face_opp, DevBuf<int32_t>& tet_face, int64_t* n_faces, int64_t* n_interior,
-                        unsigned long long* h_flags /* pinned [4] */) {
+                        DevBuf<int32_t>& face_opp, DevBuf<int32_t>& tet_face, DevBuf<int32_t>& tet_across,
+                        int64_t* n_faces, int64_t* n_interior, unsigned long long* h_flags /* pinned [4] */) {
   const int64_t nk = 4 * nt;
   const int sms = num_sms();
   // scratch layout
@@ -396,8 +429,9 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
   face_tet.ensure(2 * nf);
   face_opp.ensure(2 * nf);
   tet_face.ensure(4 * nt);
+  tet_across.ensure(4 * nt);
   k_face_emit<<<grid_b, 256, 0, s>>>(off, foff, nn, keys, pay, d_tets, face_nodes.get(), face_tet.get(),
-                                     face_opp.get(), tet_face.get(), flags + 1);
+                                     face_opp.get(), tet_face.get(), tet_across.get(), flags + 1);
   FS_LAUNCH_CHECK();
   FS_CUDA(cudaMemcpyAsync(h_flags + 1, flags + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));

@@ -71,7 +71,34 @@ __device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int 
     count += __popc(ball);
   }
   __syncwarp();
-  for (int i = lane; i < count; i += 32) {
+  if (count <= 64) {  // bitonic network in registers: element 2 lane + k, padded with kSentinel
+    int32_t a0 = 2 * lane < count ? src[2 * lane] : kSentinel;
+    int32_t a1 = 2 * lane + 1 < count ? src[2 * lane + 1] : kSentinel;
+#pragma unroll
+    for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        if (j == 1) {
+          const bool up = ((2 * lane) & size) == 0;
+          const int32_t lo = min(a0, a1), hi = max(a0, a1);
+          a0 = up ? lo : hi;
+          a1 = up ? hi : lo;
+        } else {
+          const int32_t b0 = __shfl_xor_sync(0xffffffffu, a0, j >> 1);
+          const int32_t b1 = __shfl_xor_sync(0xffffffffu, a1, j >> 1);
+          const bool lower = ((2 * lane) & j) == 0, up = ((2 * lane) & size) == 0;
+          a0 = lower == up ? min(a0, b0) : max(a0, b0);
+          a1 = lower == up ? min(a1, b1) : max(a1, b1);
+        }
+      }
+    }
+    __syncwarp();
+    if (2 * lane < count) src[2 * lane] = a0;
+    if (2 * lane + 1 < count) src[2 * lane + 1] = a1;
+    __syncwarp();
+    return count;
+  }
+  for (int i = lane; i < count; i += 32) {  // longer lists: rank sort (values are distinct)
     const int32_t v = src[i];
     int r = 0;
     for (int j = 0; j < count; ++j) r += src[j] < v ? 1 : 0;
@@ -87,8 +114,8 @@ __device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int 
 // sorted lists at node_ptr / nf_ptr and the diagonal slot.
 template <bool kWrite>
 __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
-    const int32_t* __restrict__ tets, const int32_t* __restrict__ tet_face, const int32_t* __restrict__ face_tet,
-    const int32_t* __restrict__ face_opp, const int32_t* __restrict__ nt_ptr, const int32_t* __restrict__ nt_idx,
+    const int32_t* __restrict__ tets, const int32_t* __restrict__ tet_face, const int32_t* __restrict__ tet_across,
+    const int32_t* __restrict__ nt_ptr, const int32_t* __restrict__ nt_idx,
     int64_t n_lo, int64_t nloc, int32_t* __restrict__ deg, int32_t* __restrict__ nfc,
     const int64_t* __restrict__ node_ptr, const int64_t* __restrict__ nf_ptr, int32_t* __restrict__ nbr,
     int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err, int fem,
@@ -102,7 +129,8 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
       if (lane == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, n_lo + il);
       continue;
     }
-    // candidates: 4 vertices + 4 across-face nodes per tet
+    // candidates: 4 vertices + 4 across-face nodes per tet (the vertex of the neighbour tet
+    // opposite face l, from the face table; -1 on the boundary)
     for (int k = lane; k < ntet; k += 32) {
       const int32_t t = nt_idx[b + k];
       const int4 v = reinterpret_cast<const int4*>(tets)[t];
@@ -110,14 +138,12 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
       cand[w][8 * k + 1] = v.y;
       cand[w][8 * k + 2] = v.z;
       cand[w][8 * k + 3] = v.w;
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        const int32_t f = tet_face[4 * t + l];
-        const int32_t ta = face_tet[2 * f], tb = face_tet[2 * f + 1];
-        int32_t across = kSentinel;  // FEM-T4 couples only the nodes of a tet
-        if (tb >= 0 && !fem) across = (ta == t) ? face_opp[2 * f + 1] : face_opp[2 * f];
-        cand[w][8 * k + 4 + l] = across;
-      }
+      const int4 o = reinterpret_cast<const int4*>(tet_across)[t];
+      const bool cpl = !fem;  // FEM-T4 couples only the nodes of a tet
+      cand[w][8 * k + 4] = cpl && o.x >= 0 ? o.x : kSentinel;
+      cand[w][8 * k + 5] = cpl && o.y >= 0 ? o.y : kSentinel;
+      cand[w][8 * k + 6] = cpl && o.z >= 0 ? o.z : kSentinel;
+      cand[w][8 * k + 7] = cpl && o.w >= 0 ? o.w : kSentinel;
     }
     __syncwarp();
     const int dn = warp_sort_unique(cand[w], tmp[w], 8 * ntet, lane);
@@ -463,8 +489,8 @@ __global__ void k_export_csr(const int64_t* __restrict__ node_ptr, const int32_t
 }  // namespace
 
 // Host driver of S5 for the own node range [n_lo, n_lo + nloc).
-void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* face_tet,
-                          const int32_t* face_opp, int64_t n_lo, int64_t nloc, cudaStream_t s,
+void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_face, const int32_t* tet_across,
+                          int64_t n_lo, int64_t nloc, cudaStream_t s,
                           DevBuf<unsigned char>& scratch, Pattern& pat, unsigned long long* h_flags, int fem) {
   DevBuf<int64_t>& node_ptr = pat.node_ptr;
   DevBuf<int32_t>& nbr = pat.nbr;
@@ -518,7 +544,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   k_sort_segments<<<gw, kPatWarps * 32, 0, s>>>(ptr, nloc, idx, flags);
   FS_LAUNCH_CHECK();
   pt.mark("node tets");
-  k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc, deg,
+  k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, tet_across, ptr, idx, n_lo, nloc, deg,
                                                       nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags, fem,
                                                       pad_nbr, pad_nf, pad_over);
   FS_LAUNCH_CHECK();
@@ -544,7 +570,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
     k_pattern_compact<<<gw, kPatWarps * 32, 0, s>>>(pad_nbr, pad_nf, n_lo, nloc, node_ptr.get(), nf_ptr.get(), nbr.get(),
                                                     nf_idx.get(), diag_slot.get());
   } else {
-    k_node_pattern<true><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, face_tet, face_opp, ptr, idx, n_lo, nloc,
+    k_node_pattern<true><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, tet_across, ptr, idx, n_lo, nloc,
                                                        nullptr, nullptr, node_ptr.get(), nf_ptr.get(), nbr.get(),
                                                        nf_idx.get(), diag_slot.get(), flags, fem, nullptr, nullptr,
                                                        nullptr);

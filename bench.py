@@ -276,6 +276,11 @@ def run_gpu(args):
         dist.broadcast_object_list(uid, src=0)
         g.comm_init(uid[0], rank, world)
         g.set_exchange(1 if args.exchange == "halo" else 0)
+    if args.deterministic:
+        g.set_deterministic(True)
+    if args.method == "fem":
+        g.set_method(1)  # FSFEM_METHOD_FEM_T4, for comparison runs only
+    bc_mode = 1 if args.bc == "penalty" else 0
     dev = torch.device("cuda", local)
     xyz_d = torch.from_numpy(m.xyz).to(dev)
     tets_d = torch.from_numpy(m.tets).to(dev)
@@ -286,8 +291,8 @@ def run_gpu(args):
     def step(xyz, tets, dirichlet, loads, u):
         nf, ni = fsfem_build_faces(g.ctx, xyz, tets)
         rb, nr, nnz = fsfem_assemble_csr(g.ctx, E_MOD, NU)
-        fsfem_apply_bc(g.ctx, dirichlet, loads, 0)
-        rep = fsfem_pcg_solve(g.ctx, u, True, 1e-10, 0)
+        fsfem_apply_bc(g.ctx, dirichlet, loads, bc_mode)
+        rep = fsfem_pcg_solve(g.ctx, u, True, args.tol, 0)
         return nf, nnz, rep
 
     def barrier():
@@ -406,7 +411,9 @@ def run_gpu(args):
                                if cluster_loop else
                                "Jacobi-PCG (standard recurrence, host-polled CUDA-graph batches of 32 iterations)"),
                        "l2": ("inputs larger than L2 (CSR values alone 8*nnz bytes > 126 MB)" if 8 * nnz > 126e6 else
-                              "inputs smaller than L2: the operator stays L2-resident between iterations")},
+                              "inputs smaller than L2: the operator stays L2-resident between iterations"),
+                       "bc": args.bc, "tol": args.tol, "deterministic_dots": bool(args.deterministic),
+                       "method": "FS-FEM" if args.method == "fs" else "FEM-T4 (comparison)"},
             "components": {"assembly_faces_per_s": nf / (t_num / 1e3), "assembly_ms": t_num,
                            "assembly_hbm_frac": asm_bytes / (t_num / 1e3) / 1e9 / peak,
                            "pcg_it_per_s": iters / (t_pcg / 1e3), "pcg_iterations": iters, "pcg_ms": t_pcg,
@@ -446,6 +453,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
                     help="multi-GPU exchange of the search direction (fsfem_set_exchange)")
+    ap.add_argument("--bc", default="modify", choices=["modify", "penalty"],
+                    help="Dirichlet treatment (fsfem_apply_bc mode; PAPER.md:243-245)")
+    ap.add_argument("--tol", type=float, default=1e-10, help="PCG relative residual (north star: 1e-10)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="GPU-count-invariant dots (fsfem_set_deterministic)")
+    ap.add_argument("--method", default="fs", choices=["fs", "fem"],
+                    help="fs = FS-FEM (the product); fem = the FEM-T4 companion (comparison only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

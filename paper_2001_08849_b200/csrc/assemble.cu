@@ -693,6 +693,28 @@ __device__ __forceinline__ void mform_block(const double* M, double lam, double 
     }
 }
 
+// The same block written to global memory with 16-B stores (5 store instructions instead of 9;
+// blocks are 72 B, so every other one starts 16-B aligned).
+__device__ __forceinline__ void mform_block_store(const double* M, double lam, double mu, double* out) {
+  double k[9];
+  mform_block(M, lam, mu, k);
+  if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    double2* o = reinterpret_cast<double2*>(out);
+    o[0] = make_double2(k[0], k[1]);
+    o[1] = make_double2(k[2], k[3]);
+    o[2] = make_double2(k[4], k[5]);
+    o[3] = make_double2(k[6], k[7]);
+    out[8] = k[8];
+  } else {
+    out[0] = k[0];
+    double2* o = reinterpret_cast<double2*>(out + 1);
+    o[0] = make_double2(k[1], k[2]);
+    o[1] = make_double2(k[3], k[4]);
+    o[2] = make_double2(k[5], k[6]);
+    o[3] = make_double2(k[7], k[8]);
+  }
+}
+
 template <bool kTet>
 __device__ __forceinline__ void domain_s(const double* __restrict__ X, const unsigned char* fv, double* out);
 
@@ -1038,7 +1060,7 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
         }
       }
       if (tk.sub == 255) {
-        mform_block(M, lam, mu, vals + 9 * (rows[tk.row].P + tk.slot));
+        mform_block_store(M, lam, mu, vals + 9 * (rows[tk.row].P + tk.slot));
       } else {  // diagonal sub-list: the 6 independent entries of the symmetric partial
         double* dp = dpart + 6 * (kDiagSplit * tk.row + tk.sub);
         dp[0] = M[0];
@@ -1057,7 +1079,7 @@ __global__ void __launch_bounds__(kAsmThreads, 1) k_asm_tile(const int64_t* __re
 #pragma unroll
         for (int v = 0; v < 6; ++v) d[v] += dpart[6 * (kDiagSplit * r + q) + v];
       const double Md[9] = {d[0], d[3], d[4], d[3], d[1], d[5], d[4], d[5], d[2]};
-      mform_block(Md, lam, mu, vals + 9 * (rows[r].P + rows[r].sdiag));
+      mform_block_store(Md, lam, mu, vals + 9 * (rows[r].P + rows[r].sdiag));
     }
     named_sync(6, kGroup);              // dpart reused by the next tile
     named_arrive(3 + b, kAsmThreads);   // buffer b free (S, X and the blob slot of tile j)

@@ -289,6 +289,20 @@ void perm_ids_device(const int32_t* perm, const int32_t* in, int32_t* out, int64
   FS_LAUNCH_CHECK();
 }
 
+__global__ void k_perm_ids_inplace(const int32_t* __restrict__ perm, int32_t* ids, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = ids[k];
+    if (v >= 0) ids[k] = perm[v];
+  }
+}
+
+// ids[k] <- perm[ids[k]] in place (negative ids kept).
+void perm_ids_inplace_device(const int32_t* perm, int32_t* ids, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_perm_ids_inplace<<<grid_for(n), 256, 0, s>>>(perm, ids, n);
+  FS_LAUNCH_CHECK();
+}
+
 void perm_ids_valid_device(const int32_t* perm, const int32_t* in, int32_t* out, int64_t n, int64_t nn,
                            cudaStream_t s) {
   if (n <= 0) return;

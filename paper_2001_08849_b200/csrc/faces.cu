@@ -127,11 +127,15 @@ __global__ void k_face_count(const int4* __restrict__ tets, int64_t nt, int64_t 
 
 // Scatter each face instance into its bucket: key = (b << 32) | c, payload = 4t + l.
 // The slot inside a bucket is arbitrary (atomic cursor); the in-bucket sort fixes the order.
-__global__ void k_face_scatter(const int4* __restrict__ tets, int64_t nt, const int32_t* __restrict__ off,
+// Tets the count kernel skipped (ids out of range, repeated nodes) are skipped here too, so the
+// bucket offsets stay consistent and the build can run to its end before the host looks at errors.
+__global__ void k_face_scatter(const int4* __restrict__ tets, int64_t nt, int64_t nn, const int32_t* __restrict__ off,
                                int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys,
                                uint32_t* __restrict__ pay) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
     const int4 v = tets[t];
+    if (v.x < 0 || v.y < 0 || v.z < 0 || v.w < 0 || v.x >= nn || v.y >= nn || v.z >= nn || v.w >= nn) continue;
+    if (v.x == v.y || v.x == v.z || v.x == v.w || v.y == v.z || v.y == v.w || v.z == v.w) continue;
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       int a, b, c;
@@ -243,15 +247,18 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_bucket_sort(const int32_t* 
 
 // CTA per large bucket (dynamic shared memory, up to kBigCap instances).
 __global__ void __launch_bounds__(256) k_bucket_sort_big(const int32_t* __restrict__ off, const int32_t* __restrict__ big_list,
+                                                         const int32_t* __restrict__ n_big,
                                                          unsigned long long* __restrict__ keys, uint32_t* __restrict__ pay,
                                                          int32_t* __restrict__ ucnt, unsigned long long* __restrict__ err) {
   extern __shared__ unsigned long long dyn[];
-  const int32_t a = big_list[blockIdx.x];
+  const int nb = *n_big;  // written by k_bucket_sort (no host round trip)
+  for (int ib = blockIdx.x; ib < nb; ib += gridDim.x) {
+  const int32_t a = big_list[ib];
   const int32_t beg = off[a];
   const int n = off[a + 1] - beg;
   if (n > kBigCap) {
     if (threadIdx.x == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, a);
-    return;
+    continue;  // uniform over the CTA
   }
   unsigned long long* sk = dyn;
   unsigned long long* ok = sk + kBigCap;
@@ -274,6 +281,8 @@ __global__ void __launch_bounds__(256) k_bucket_sort_big(const int32_t* __restri
   if (too_long) report_error(err, FSFEM_ERR_TOPOLOGY, a);
   __syncthreads();
   if (threadIdx.x == 0) ucnt[a] = tot;
+  __syncthreads();  // sk / ok / tot are reused by the next bucket
+  }
 }
 
 // Warp per bucket: emit the faces of bucket a at face ids foff[a] + run index.
@@ -383,60 +392,56 @@ void build_faces_device(const double* d_xyz, int64_t nn, const int32_t* d_tets, 
 
   FS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nn + 1), s));
   FS_CUDA(cudaMemsetAsync(cur, 0, sizeof(int32_t) * (nn + 1), s));
-  FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
-  FS_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(unsigned long long) * 3, s));
+  FS_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));      // [0] validation errors
+  FS_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(unsigned long long) * 2, s));  // [1] interior, [2] big buckets
+  FS_CUDA(cudaMemsetAsync(flags + 3, 0xff, sizeof(unsigned long long), s));  // [3] sort errors
   PhaseTimer pt(s, "faces");
 
+  // One host round trip for the whole build: invalid tets are skipped by count and scatter alike,
+  // big buckets are found on the device, and the outputs are sized by the bound N_f <= 4 N_t.
   const int nbb = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(1, ceil_div(nn, 256))));
   k_bbox_partial<<<nbb, 256, 0, s>>>(d_xyz, nn, bbp);
   FS_LAUNCH_CHECK();
   k_bbox_final<<<1, 256, 0, s>>>(bbp, nbb, bb);
   FS_LAUNCH_CHECK();
-  const int grid_t = static_cast<int>(std::min<int64_t>(ceil_div(nt, 256), 8LL * sms));
+  const int grid_t = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nt, 256), 8LL * sms)));
   k_face_count<<<grid_t, 256, 0, s>>>(reinterpret_cast<const int4*>(d_tets), nt, nn, d_xyz, bb, cnt, flags);
   FS_LAUNCH_CHECK();
-  // errors (ids out of range) must stop here: the scatter would index out of bounds
-  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaStreamSynchronize(s));
-  pt.mark("bbox + count + D2H");
-  if (h_flags[0] != kNoError) return;  // caller decodes
   exclusive_scan_i32(cnt, off, nn, s, tmp, tmp_bytes);
-  k_face_scatter<<<grid_t, 256, 0, s>>>(reinterpret_cast<const int4*>(d_tets), nt, off, cur, keys, pay);
+  k_face_scatter<<<grid_t, 256, 0, s>>>(reinterpret_cast<const int4*>(d_tets), nt, nn, off, cur, keys, pay);
   FS_LAUNCH_CHECK();
-  const int grid_b = static_cast<int>(std::min<int64_t>(ceil_div(nn, kSortWarps), 16LL * sms));
+  const int grid_b = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nn, kSortWarps), 16LL * sms)));
   k_bucket_sort<<<grid_b, kSortWarps * 32, 0, s>>>(off, nn, keys, pay, ucnt, big,
-                                                   reinterpret_cast<int32_t*>(flags + 2), flags);
+                                                   reinterpret_cast<int32_t*>(flags + 2), flags + 3);
   FS_LAUNCH_CHECK();
-  FS_CUDA(cudaMemcpyAsync(h_flags + 2, flags + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaStreamSynchronize(s));
-  pt.mark("scan + scatter + bucket sort");
-  const int n_big = static_cast<int>(h_flags[2] & 0xffffffffu);
-  if (n_big > 0) {
+  {
     const size_t smem = (2 * sizeof(unsigned long long) + 2 * sizeof(uint32_t)) * kBigCap;
-    FS_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bucket_sort_big<<<n_big, 256, smem, s>>>(off, big, keys, pay, ucnt, flags);
+    static bool attr = false;
+    if (!attr) {
+      FS_CUDA(cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_bucket_sort_big<<<sms, 256, smem, s>>>(off, big, reinterpret_cast<const int32_t*>(flags + 2), keys, pay, ucnt,
+                                             flags + 3);
     FS_LAUNCH_CHECK();
   }
   exclusive_scan_i32(ucnt, foff, nn, s, tmp, tmp_bytes);
-  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  int32_t nf32 = 0;
-  FS_CUDA(cudaMemcpyAsync(&nf32, foff + nn, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaStreamSynchronize(s));
-  pt.mark("big buckets + scan + D2H");
-  if (h_flags[0] != kNoError) return;
-  const int64_t nf = nf32;
-  face_nodes.ensure(3 * nf);
-  face_tet.ensure(2 * nf);
-  face_opp.ensure(2 * nf);
+  face_nodes.ensure(3 * 4 * nt);
+  face_tet.ensure(2 * 4 * nt);
+  face_opp.ensure(2 * 4 * nt);
   tet_face.ensure(4 * nt);
   tet_across.ensure(4 * nt);
   k_face_emit<<<grid_b, 256, 0, s>>>(off, foff, nn, keys, pay, d_tets, face_nodes.get(), face_tet.get(),
                                      face_opp.get(), tet_face.get(), tet_across.get(), flags + 1);
   FS_LAUNCH_CHECK();
-  FS_CUDA(cudaMemcpyAsync(h_flags + 1, flags + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  int32_t nf32 = 0;
+  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
+  FS_CUDA(cudaMemcpyAsync(&nf32, foff + nn, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   FS_CUDA(cudaStreamSynchronize(s));
-  pt.mark("emit");
-  *n_faces = nf;
+  pt.mark("faces (one round trip)");
+  if (h_flags[0] == kNoError) h_flags[0] = h_flags[3];  // validation errors first (as before)
+  if (h_flags[0] != kNoError) return;  // caller decodes
+  *n_faces = nf32;
   *n_interior = static_cast<int64_t>(h_flags[1]);
 }
 

@@ -1239,20 +1239,18 @@ __global__ void __launch_bounds__(kThreads) k_cg_update(double* __restrict__ x, 
 //   CTA 0 records the scalars (finish_beta);
 //   phase 2: x += alpha p_old; p = dinv r + beta p_old (r and dinv are L2-warm from phase 1).
 // Same arithmetic as k_update + k_direction, one launch and one DRAM pass less over r and dinv.
+// Grid barrier (every CTA resident): one release atomic per CTA and acquire polls; CTA 0 adds
+// 2^31 - (G - 1), the others 1, so bit 31 of the counter flips exactly when all G have arrived and
+// its low bits return to 0 (no reset, no generation word, nothing serial after the last arrival).
 __device__ __forceinline__ void grid_barrier(PcgState* st) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned gen = *reinterpret_cast<volatile unsigned*>(&st->bar_gen);
-    __threadfence();
-    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
-      st->bar_count = 0u;
-      __threadfence();
-      atomicExch(&st->bar_gen, gen + 1u);
-    } else {
-      while (*reinterpret_cast<volatile unsigned*>(&st->bar_gen) == gen) {
-      }
-    }
-    __threadfence();
+    const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+    unsigned old, cur;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(&st->bar_count), "r"(inc) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&st->bar_count) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0u);
   }
   __syncthreads();
 }

@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   __shared__ uint32_t sh_epoch;
   __shared__ int sh_done;
   __shared__ int sh_p1done;  // chunks whose phase 1 the loader has seen complete
+  __shared__ double sh_p2dot[2];  // p.q of the CTA's chunks, per phase-2 warp (chunk order)
   if (threadIdx.x == 0) {
     for (int k = 0; k < kDfStages; ++k) {
       mbar_init(&full[k], 1);
@@ -835,6 +836,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       __syncwarp();
     };
     int issued = 0;
+    double p2dot = 0.0;
     const int pw = warp == kWarps + 1 ? 0 : 1;
     for (int j = kDfP2W == 1 ? 0 : pw; j < K; j += kDfP2W) {
       DF_T(tC)
@@ -881,7 +883,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
       }
       if (kPcg) {
         dt = warp_sum(dt);
-        if (lane == 0) dotc[blockIdx.x + j * gridDim.x] = dt;
+        p2dot += dt;  // this warp's chunks in order (uniform over the warp)
       }
       // the chunk's pushed products are dead: drop their whole L2 lines without write-back
       const uintptr_t lo = reinterpret_cast<uintptr_t>(tbuf + 3 * (int64_t)qi.Pt0);
@@ -894,6 +896,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
         ++issued;
       }
     }
+    if (kPcg && lane == 0) sh_p2dot[pw] = p2dot;
   } else {
     // ---------------- compute warps: P1 ----------------
 #ifdef FSFEM_DF_STREAMONLY
@@ -990,10 +993,12 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
            warp == kWarps ? "load" : (warp == kWarps + 1 || warp == kWarps + 3 ? "p2" : (warp > kWarps ? "count" : "comp")),
            K, nitems, tA, tB, tC, clock64() - t_begin);
 #endif
-  // last CTA out: advances the epoch; PCG: p.q = sum of the per-chunk partials in chunk order
+  // last CTA out: advances the epoch; PCG: p.q = the CTAs' partials (each the sum of its chunks'
+  // partials in chunk order) summed in CTA order -- a fixed order for the launch's fixed grid
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
+    if (kPcg) dotc[blockIdx.x] = kDfP2W == 1 ? sh_p2dot[0] : sh_p2dot[0] + sh_p2dot[1];
     __threadfence();
     last = atomicAdd(sync + 1, 1u) == gridDim.x - 1;
   }
@@ -1003,18 +1008,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   if (kPcg) {
     __shared__ double sh[32];
     double a = 0.0;
-    // 16 loads in flight per thread, added in chunk order (same order as a plain strided loop)
-    constexpr int U = 16;
-    for (int c0 = threadIdx.x; c0 < nchunks; c0 += U * blockDim.x) {
-      double v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * blockDim.x;
-        v[u] = c < nchunks ? __ldcg(dotc + c) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) a += v[u];
-    }
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) a += __ldcg(dotc + b);
     const double pq = block_sum(a, sh);
     spmv_finish(st, pq);
     if (threadIdx.x == 0) spmv_time_end(st);

@@ -403,7 +403,7 @@ def run_gpu(args):
             "device_timer": {"avg_launch_ms": spmv_dev_avg_ms, "launches": spmv_dev_n,
                              "achieved": spmv_bytes / (max(spmv_dev_avg_ms, 1e-12) / 1e3) / 1e9,
                              "frac": spmv_bytes / (max(spmv_dev_avg_ms, 1e-12) / 1e3) / 1e9 / peak,
-                             "how": "%globaltimer from the first CTA start to the last CTA end of EVERY PCG SpMV"},
+                             "how": "%globaltimer from CTA 0's start to the last CTA's end of EVERY PCG SpMV (fire-and-forget reductions)"},
             "full_csr_equivalent_bytes": 12 * nnz + 32 * 3 * m.n_nodes}
     if not cluster_loop:
         roof = roof_spmv

@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, FSFEM_SPMV_MINB) k_spmv(const SpmvCh
   if (kPcg) {
     double unused;
     if (cta_scalars(st, nullptr, unused)) return;
-    spmv_time_start(st);
+    if (split != 2) spmv_time_start(st);  // split SpMV: one interval from part 1's start to part 2's end
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // chunk walk: grid-strided (contiguous ranges per CTA were slower)

@@ -29,8 +29,8 @@ struct PcgState {
   const double* upd_part;  // [2 * upd_n]: gamma partials, then r.r partials
   int upd_n;
   int pad_;
-  // device timing of the PCG SpMV launches (%globaltimer, ns): earliest CTA start of the launch
-  // in flight, summed durations (first CTA start -> last CTA end) and their number
+  // device timing of the PCG SpMV launches (%globaltimer, ns): spmv_t0 unused, summed durations
+  // (CTA 0 start -> last CTA end) and their number
   unsigned long long spmv_t0;
   unsigned long long spmv_ns;
   unsigned long long spmv_cnt;
@@ -45,17 +45,23 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// SpMV launch timing: every CTA marks its start; the launch's last CTA closes the interval.
+// SpMV launch timing, fire-and-forget (nothing serial at the end of the launch): CTA 0 adds
+// -t_start and the launch's last CTA adds t_end to spmv_ns (mod 2^64, so the sum is exactly the
+// summed durations CTA 0 start -> last CTA end), and counts the launch.
+#ifndef FSFEM_SPMV_DEVTIME
+#define FSFEM_SPMV_DEVTIME 1
+#endif
 __device__ __forceinline__ void spmv_time_start(PcgState* st) {
-  if (st && threadIdx.x == 0) atomicMin(&st->spmv_t0, global_ns());
+  if (FSFEM_SPMV_DEVTIME && st && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long neg = 0ull - global_ns();
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(&st->spmv_ns), "l"(neg) : "memory");
+  }
 }
 __device__ __forceinline__ void spmv_time_end(PcgState* st) {  // one thread of the last CTA
+  if (!FSFEM_SPMV_DEVTIME) return;
   const unsigned long long t1 = global_ns();
-  const unsigned long long t0 = atomicExch(&st->spmv_t0, ~0ull);
-  if (t0 != ~0ull && t1 > t0) {
-    st->spmv_ns += t1 - t0;
-    st->spmv_cnt += 1;
-  }
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(&st->spmv_ns), "l"(t1) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(&st->spmv_cnt), "l"(1ull) : "memory");
   st->spmv_tend = t1;
 }
 

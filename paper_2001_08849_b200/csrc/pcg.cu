@@ -673,6 +673,14 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // everything below may read what the previous kernel wrote
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int K = nchunks > static_cast<int>(blockIdx.x) ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // the loader's first chunk descriptors are loaded while thread 0 reads the epoch and the done
+  // flag (one round trip instead of three in a row before the first bulk copy)
+  SpmvChunk pre[kDfStages + 1];
+  if (warp == kWarps && lane == 0)
+#pragma unroll
+    for (int j = 0; j <= kDfStages; ++j) pre[j] = j < K ? chunks[blockIdx.x + j * gridDim.x] : SpmvChunk{};
   if (threadIdx.x == 0) {
     sh_p1done = 0;
     sh_epoch = __ldcg(sync) + 1u;
@@ -682,9 +690,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
   if (sh_done) return;  // uniform over the grid
   if (kPcg) spmv_time_start(st);
   const uint32_t epoch = sh_epoch;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* xown = x + own_off;
-  const int K = nchunks > static_cast<int>(blockIdx.x) ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 #ifndef FSFEM_DF_TIMING
 #define FSFEM_DF_TIMING 0
 #endif
@@ -695,11 +701,11 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_spmv_df(
 #define DF_T(acc) if (FSFEM_DF_TIMING) { const long long tq1 = clock64(); acc += tq1 - tq0; tq0 = tq1; }
   if (warp == kWarps) {
     // ---------------- loader warp: P1 stages (TMA ring) ----------------
-    SpmvChunk nx = K > kDfStages ? chunks[blockIdx.x + kDfStages * gridDim.x] : SpmvChunk{};
-    for (int j = 0; j < kDfStages && j < K; ++j)
-      if (lane == 0)
-        issue_chunk_push(chunks[blockIdx.x + j * gridDim.x], sptr, snbr, tpos, vals, xown, pst + j * PushLayout::kBytes,
-                         &full[j], &pinfo[j]);
+    SpmvChunk nx = pre[kDfStages];  // (lane 0's copy is the one used)
+#pragma unroll
+    for (int j = 0; j < kDfStages; ++j)
+      if (lane == 0 && j < K)
+        issue_chunk_push(pre[j], sptr, snbr, tpos, vals, xown, pst + j * PushLayout::kBytes, &full[j], &pinfo[j]);
     for (int j = 0; j < K; ++j) {
       const int c = blockIdx.x + j * gridDim.x;
       const int sj = j % kDfStages;
@@ -1261,15 +1267,6 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
 #define FSFEM_GAP_TIMING 0
 #endif
   if (FSFEM_GAP_TIMING && threadIdx.x == 0) atomicMin(&st->upd_t0, global_ns());
-  if (threadIdx.x == 0) {
-    sh_sc[0] = ld_cg(&st->done_d);
-    sh_sc[1] = ld_cg(&st->alpha);
-    sh_sc[2] = ld_cg(&st->rho);
-    sh_sc[3] = ld_cg(&st->ff);
-  }
-  __syncthreads();
-  if (sh_sc[0] != 0.0) return;  // uniform over the grid: done_d is only written between launches
-  const double alpha = sh_sc[1], rho_old = sh_sc[2];
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   const uint64_t pol = policy_evict_last();
   double rr = 0.0, rz = 0.0;
@@ -1282,6 +1279,31 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
   constexpr int kKeep = FSFEM_UPD_KEEP;
   const bool keep = n <= static_cast<int64_t>(kKeep) * kVec * T;
   double zk_[kKeep][kVec], xk_[kKeep][kVec], pk_[kKeep][kVec];
+  // the first pass's loads are issued before the scalars are read, so the two latencies overlap
+  // (the loads are only wasted in the launches after convergence)
+  double rv0[kVec], qv0[kVec], dv0[kVec];
+  if (keep) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const int64_t k = b + j * T;
+      const bool ok = k < n;
+      rv0[j] = ok ? ld_vec(r + k, pol) : 0.0;
+      qv0[j] = ok ? ldg_vec(q + k, pol) : 0.0;
+      dv0[j] = ok ? ldg_vec(dinv + k, pol) : 0.0;
+      xk_[0][j] = ok ? ld_vec(x + k, pol) : 0.0;
+      pk_[0][j] = ok ? ld_vec(p + k, pol) : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    sh_sc[0] = ld_cg(&st->done_d);
+    sh_sc[1] = ld_cg(&st->alpha);
+    sh_sc[2] = ld_cg(&st->rho);
+    sh_sc[3] = ld_cg(&st->ff);
+  }
+  __syncthreads();
+  if (sh_sc[0] != 0.0) return;  // uniform over the grid: done_d is only written between launches
+  const double alpha = sh_sc[1], rho_old = sh_sc[2];
   if (keep) {
 #pragma unroll
     for (int ps = 0; ps < kKeep; ++ps) {
@@ -1291,11 +1313,17 @@ __global__ void __launch_bounds__(kThreads) k_update_direction(double* __restric
       for (int j = 0; j < kVec; ++j) {
         const int64_t k = b + j * T;
         const bool ok = k < n;
-        rv[j] = ok ? ld_vec(r + k, pol) : 0.0;
-        qv[j] = ok ? ldg_vec(q + k, pol) : 0.0;
-        dv[j] = ok ? ldg_vec(dinv + k, pol) : 0.0;
-        xk_[ps][j] = ok ? ld_vec(x + k, pol) : 0.0;
-        pk_[ps][j] = ok ? ld_vec(p + k, pol) : 0.0;
+        if (ps == 0) {
+          rv[j] = rv0[j];
+          qv[j] = qv0[j];
+          dv[j] = dv0[j];
+        } else {
+          rv[j] = ok ? ld_vec(r + k, pol) : 0.0;
+          qv[j] = ok ? ldg_vec(q + k, pol) : 0.0;
+          dv[j] = ok ? ldg_vec(dinv + k, pol) : 0.0;
+          xk_[ps][j] = ok ? ld_vec(x + k, pol) : 0.0;
+          pk_[ps][j] = ok ? ld_vec(p + k, pol) : 0.0;
+        }
       }
 #pragma unroll
       for (int j = 0; j < kVec; ++j) {

@@ -23,3 +23,22 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+def test_reference_arm_config_and_clock():
+    """Both arms print workload_config(); the reference arm's ms_per_step is its measured step
+    wall time (what the driver's clock sees), the extrapolation is reported beside it."""
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "1", "--warmup", "0"], check=True, timeout=600, capture_output=True, text=True,
+                         cwd=ROOT)
+    d = json.loads([ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")][0])
+    args = argparse.Namespace(config=1, exchange="allgather", bc="modify", tol=1e-10, deterministic=False,
+                              method="fs")
+    assert d["config"] == json.loads(json.dumps(bench.workload_config(args)))
+    from fsfem_inputs import config_mesh, kuhn_counts
+    c = kuhn_counts(*config_mesh(1).grid)
+    assert d["config"]["n_faces"] == c["n_faces"] == 568 and d["config"]["nnz"] == 12879  # SURVEY.md 8 table
+    assert d["ms_per_step"] < 60e3 and d["extrapolated_ms_per_full_step"] > 0

@@ -215,7 +215,10 @@ constexpr int kMaxVerts = 254;    // u8 local vertex ids, 255 = none
 constexpr int kDiagCap = 2048;    // sum over the tile rows of |F(i)|
 constexpr int kMaxBlk = 767;      // stored blocks of the tile rows
 constexpr int kMaxTask = 1024;
-constexpr int kDiagSplit = 4;     // strided sub-lists of a diagonal block
+#ifndef FSFEM_DIAG_SPLIT
+#define FSFEM_DIAG_SPLIT 6
+#endif
+constexpr int kDiagSplit = FSFEM_DIAG_SPLIT;  // strided sub-lists of a diagonal block
 constexpr int kBlobCap = 14336;   // bytes of one tile blob
 constexpr int kAsmWarps = 16;     // 8 producer + 8 consumer warps
 constexpr int kAsmThreads = 32 * kAsmWarps;

@@ -216,7 +216,7 @@ constexpr int kDiagCap = 2048;    // sum over the tile rows of |F(i)|
 constexpr int kMaxBlk = 767;      // stored blocks of the tile rows
 constexpr int kMaxTask = 1024;
 #ifndef FSFEM_DIAG_SPLIT
-#define FSFEM_DIAG_SPLIT 6
+#define FSFEM_DIAG_SPLIT 4
 #endif
 constexpr int kDiagSplit = FSFEM_DIAG_SPLIT;  // strided sub-lists of a diagonal block
 constexpr int kBlobCap = 14336;   // bytes of one tile blob

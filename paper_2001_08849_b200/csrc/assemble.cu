@@ -587,10 +587,49 @@ __global__ void __launch_bounds__(kBldThreads) k_tile_build(
     for (int k = threadIdx.x; k < 5 * ndom; k += blockDim.x) bl[L.o_fv + k] = FV[k];
     {
       TileTask* tasks = reinterpret_cast<TileTask*>(bl + L.o_task);
-      for (int a = threadIdx.x; a < ntask; a += blockDim.x) {  // rank sort (keys are distinct)
-        const int32_t key = tkey[a];
-        int rank = 0;
-        for (int c = 0; c < ntask; ++c) rank += tkey[c] < key ? 1 : 0;
+      // rank of task a = #{keys < key_a}, key = (1023 - count) << 20 | a: a counting sort over the
+      // 1024 count bins, then in-bin order by a (one warp, __match_any per round of 32 tasks).
+      // The vertex hash set is dead here (FV and ST hold what is needed): its arrays are reused.
+      int32_t* hist = VK;  // [1024] bin sizes -> bin starts
+      int32_t* run = VI;   // [1024] tasks of each bin ranked so far
+      for (int b = threadIdx.x; b < 1024; b += blockDim.x) {
+        hist[b] = 0;
+        run[b] = 0;
+      }
+      __syncthreads();
+      for (int a = threadIdx.x; a < ntask; a += blockDim.x) atomicAdd(&hist[tkey[a] >> 20], 1);
+      __syncthreads();
+      {
+        static_assert(kBldThreads * 4 == 1024, "four bins per thread");
+        int v[4], sum = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[q] = hist[4 * threadIdx.x + q];
+          sum += v[q];
+        }
+        int base = cta_excl_scan(sum, &tot);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hist[4 * threadIdx.x + q] = base;
+          base += v[q];
+        }
+      }
+      __syncthreads();
+      if (w == 0) {
+        for (int a0 = 0; a0 < ntask; a0 += 32) {
+          const int a = a0 + lane;
+          const int bin = a < ntask ? (tkey[a] >> 20) : 1024 + lane;  // padding lanes match nobody
+          const unsigned peers = __match_any_sync(0xffffffffu, bin);
+          const int before = __popc(peers & ((1u << lane) - 1u));
+          if (a < ntask) tkey[a] = hist[bin] + run[bin] + before;  // the key becomes the rank
+          __syncwarp();
+          if (a < ntask && lane == 31 - __clz(peers)) run[bin] += __popc(peers);
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int a = threadIdx.x; a < ntask; a += blockDim.x) {
+        const int rank = tkey[a];
         const int r = tinfo[a] >> 24, q = (tinfo[a] >> 16) & 255, sl = tinfo[a] & 0xffff;
         const int b = rbb[r] + sl;
         TileTask tk;

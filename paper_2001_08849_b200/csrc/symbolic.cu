@@ -21,6 +21,7 @@ namespace {
 constexpr int kPatWarps = 4;
 constexpr int kMaxTetsPerNode = 128;                 // UNSUPPORTED beyond (general meshes: ~20-60)
 constexpr int kCandCap = 8 * kMaxTetsPerNode;        // node candidates per node
+constexpr int kFastTetCap = 64;                      // tets per node of the fast pattern pass
 constexpr int kPadDeg = 64;  // padded pattern lists of pass 1 (longer lists: a second pattern pass)
 constexpr int kSentinel = 0x7fffffff;
 
@@ -46,9 +47,9 @@ __global__ void k_scatter_node_tets(const int32_t* __restrict__ tets, int64_t nt
 // addressing hash set in dst (the order of insertion does not matter: only set membership is
 // used), then the few distinct values are ranked (all distinct, so ranks are unique).
 // dst is scratch of capacity kCandCap.
-__device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int n, int lane) {
+__device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int n, int lane, int cap = kCandCap) {
   int H = 64;
-  while (H < 2 * n && H < kCandCap) H <<= 1;
+  while (H < 2 * n && H < cap) H <<= 1;
   for (int i = lane; i < H; i += 32) dst[i] = kSentinel;
   __syncwarp();
   for (int i = lane; i < n; i += 32) {
@@ -111,8 +112,10 @@ __device__ __forceinline__ int warp_sort_unique(int32_t* src, int32_t* dst, int 
 }
 
 // Warp per own node.  Pass 1 (kWrite = false) counts deg(i) and |F(i)|; pass 2 writes the
-// sorted lists at node_ptr / nf_ptr and the diagonal slot.
-template <bool kWrite>
+// sorted lists at node_ptr / nf_ptr and the diagonal slot.  kTetCap = tets per node the shared
+// scratch holds: the fast pass-1 instance (64) leaves twice as many warps resident as the full one
+// (kMaxTetsPerNode); a node beyond it sets bit 1 of *pad_over and the host reruns pass 1 in full.
+template <bool kWrite, int kTetCap = kMaxTetsPerNode>
 __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
     const int32_t* __restrict__ tets, const int32_t* __restrict__ tet_face, const int32_t* __restrict__ tet_across,
     const int32_t* __restrict__ nt_ptr, const int32_t* __restrict__ nt_idx,
@@ -120,13 +123,18 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
     const int64_t* __restrict__ node_ptr, const int64_t* __restrict__ nf_ptr, int32_t* __restrict__ nbr,
     int32_t* __restrict__ nf_idx, int32_t* __restrict__ diag_slot, unsigned long long* __restrict__ err, int fem,
     int32_t* __restrict__ pad_nbr, int32_t* __restrict__ pad_nf, int* __restrict__ pad_over) {
-  __shared__ int32_t cand[kPatWarps][kCandCap], tmp[kPatWarps][kCandCap];
+  static_assert(kTetCap <= kMaxTetsPerNode, "scratch cap");
+  constexpr int kCap = 8 * kTetCap;
+  __shared__ int32_t cand[kPatWarps][kCap], tmp[kPatWarps][kCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t il = blockIdx.x * (int64_t)kPatWarps + w; il < nloc; il += (int64_t)gridDim.x * kPatWarps) {
     const int32_t b = nt_ptr[il];
     const int ntet = nt_ptr[il + 1] - b;
-    if (ntet > kMaxTetsPerNode) {
-      if (lane == 0) report_error(err, FSFEM_ERR_UNSUPPORTED, n_lo + il);
+    if (ntet > kTetCap) {
+      if (lane == 0) {
+        if (ntet > kMaxTetsPerNode) report_error(err, FSFEM_ERR_UNSUPPORTED, n_lo + il);
+        else if (pad_over != nullptr) atomicOr(pad_over, 2);  // rerun with the full scratch
+      }
       continue;
     }
     // candidates: 4 vertices + 4 across-face nodes per tet (the vertex of the neighbour tet
@@ -146,12 +154,12 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
       cand[w][8 * k + 7] = cpl && o.w >= 0 ? o.w : kSentinel;
     }
     __syncwarp();
-    const int dn = warp_sort_unique(cand[w], tmp[w], 8 * ntet, lane);
+    const int dn = warp_sort_unique(cand[w], tmp[w], 8 * ntet, lane, kCap);
     if (!kWrite) {
       if (lane == 0) deg[il] = dn;
       if (pad_nbr != nullptr) {  // the sorted list at a fixed stride: pass 2 becomes a copy
         if (dn > kPadDeg) {
-          if (lane == 0) *pad_over = 1;
+          if (lane == 0) atomicOr(pad_over, 1);
         } else {
           for (int k = lane; k < dn; k += 32) pad_nbr[il * kPadDeg + k] = cand[w][k];
         }
@@ -179,13 +187,13 @@ __global__ void __launch_bounds__(kPatWarps * 32) k_node_pattern(
         for (int l = 0; l < 4; ++l) cand[w][4 * k + l] = tet_face[4 * t + l];
       }
       __syncwarp();
-      fn = warp_sort_unique(cand[w], tmp[w], 4 * ntet, lane);
+      fn = warp_sort_unique(cand[w], tmp[w], 4 * ntet, lane, kCap);
     }
     if (!kWrite) {
       if (lane == 0) nfc[il] = fn;
       if (pad_nf != nullptr) {
         if (fn > kPadDeg) {
-          if (lane == 0) *pad_over = 1;
+          if (lane == 0) atomicOr(pad_over, 1);
         } else {
           for (int k = lane; k < fn; k += 32) pad_nf[il * kPadDeg + k] = cand[w][k];
         }
@@ -544,21 +552,32 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   k_sort_segments<<<gw, kPatWarps * 32, 0, s>>>(ptr, nloc, idx, flags);
   FS_LAUNCH_CHECK();
   pt.mark("node tets");
-  k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, tet_across, ptr, idx, n_lo, nloc, deg,
-                                                      nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags, fem,
-                                                      pad_nbr, pad_nf, pad_over);
+  k_node_pattern<false, kFastTetCap><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, tet_across, ptr, idx, n_lo,
+                                                                   nloc, deg, nfc, nullptr, nullptr, nullptr, nullptr,
+                                                                   nullptr, flags, fem, pad_nbr, pad_nf, pad_over);
   FS_LAUNCH_CHECK();
   node_ptr.ensure(nloc + 1);
   nf_ptr.ensure(nloc + 1);
-  exclusive_scan_i32_to_i64(deg, node_ptr.get(), nloc, s, tmp, tb);
-  exclusive_scan_i32_to_i64(nfc, nf_ptr.get(), nloc, s, tmp, tb);
   int64_t tot[2];
-  FS_CUDA(cudaMemcpyAsync(&tot[0], node_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaMemcpyAsync(&tot[1], nf_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   int h_over = 0;
-  FS_CUDA(cudaMemcpyAsync(&h_over, pad_over, sizeof(int), cudaMemcpyDeviceToHost, s));
-  FS_CUDA(cudaStreamSynchronize(s));
+  auto scan_and_read = [&]() {
+    exclusive_scan_i32_to_i64(deg, node_ptr.get(), nloc, s, tmp, tb);
+    exclusive_scan_i32_to_i64(nfc, nf_ptr.get(), nloc, s, tmp, tb);
+    FS_CUDA(cudaMemcpyAsync(&tot[0], node_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaMemcpyAsync(&tot[1], nf_ptr.get() + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaMemcpyAsync(&h_over, pad_over, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FS_CUDA(cudaStreamSynchronize(s));
+  };
+  scan_and_read();
+  if (h_flags[0] == kNoError && (h_over & 2)) {  // a node in more than kFastTetCap tets: full pass 1
+    FS_CUDA(cudaMemsetAsync(pad_over, 0, sizeof(int), s));
+    k_node_pattern<false><<<gw, kPatWarps * 32, 0, s>>>(d_tets, tet_face, tet_across, ptr, idx, n_lo, nloc, deg,
+                                                        nfc, nullptr, nullptr, nullptr, nullptr, nullptr, flags, fem,
+                                                        pad_nbr, pad_nf, pad_over);
+    FS_LAUNCH_CHECK();
+    scan_and_read();
+  }
   pt.mark("pattern count + scans");
   if (h_flags[0] != kNoError) return;
   pat.nblk = tot[0];
@@ -566,7 +585,7 @@ void build_pattern_device(const int32_t* d_tets, int64_t nt, const int32_t* tet_
   nbr.ensure(tot[0]);
   nf_idx.ensure(tot[1]);
   diag_slot.ensure(nloc);
-  if (h_over == 0) {
+  if ((h_over & 1) == 0) {
     k_pattern_compact<<<gw, kPatWarps * 32, 0, s>>>(pad_nbr, pad_nf, n_lo, nloc, node_ptr.get(), nf_ptr.get(), nbr.get(),
                                                     nf_idx.get(), diag_slot.get());
   } else {
